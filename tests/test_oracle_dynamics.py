@@ -1,0 +1,158 @@
+"""Pins of the oracle's coupled dynamics (Algorithm 1 + symplectic Euler) against invariants
+and closed forms.  P:n = PAPER.md line n."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import sph_inputs as si
+
+
+@pytest.fixture(scope="module")
+def settled_c1():
+    """C1 tank (ell = 1, 50 % fill, 569 + 236) after the damped settle (A17)."""
+    t = si.make_tank(1.0)
+    s = O.settle(t, seconds=4.0)
+    return t, s
+
+
+def _momenta(sp, s):
+    m = sp.mass
+    P = m * s.vel.sum(0) + sp.m_body * s.body[3:5]
+    L = m * (s.pos[:, 0] * s.vel[:, 1] - s.pos[:, 1] * s.vel[:, 0]).sum() \
+        + sp.m_body * (s.body[0] * s.body[4] - s.body[1] * s.body[3]) + sp.J_body * s.body[5]
+    return P, L
+
+
+@pytest.mark.parametrize("u", [(0.0, 0.0, 0.0), (5.0, 2.0, 1.0)])
+def test_linear_and_angular_momentum_balance(u):
+    """P:144 (pair forces conserve momentum), Newton pairs P:192-203, Eq. tankdynamics:
+    P_tot changes by exactly dt (u_x, u_y) per step; with central pair forces and
+    kick-then-drift, L_tot = sum m r_i x v_i + m r x rdot + J thd changes by exactly
+    dt (r_n x u + tau) (this also pins the integrator variant A11 and the torque arm A12)."""
+    t = si.make_tank(1.0, jitter=0.05, seed=7)
+    t.vel = np.random.Generator(np.random.Philox(3)).normal(0, 0.01, t.pos.shape)
+    t.body = np.array([0.01, -0.02, 0.2, 0.003, -0.001, 0.02])
+    s = O.State.from_tank(t)
+    sp = t.params
+    P0, L0 = _momenta(sp, s)
+    dP = np.zeros(2)
+    dL = 0.0
+    imp = 0.0
+    for _ in range(200):
+        r = s.body[:2].copy()
+        dP += sp.dt * np.array(u[:2])
+        dL += sp.dt * (r[0] * u[1] - r[1] * u[0] + u[2])
+        v_before = s.vel.copy()
+        s.step(u)
+        imp += sp.mass * np.abs(s.vel - v_before).sum()
+    P1, L1 = _momenta(sp, s)
+    assert np.all(np.abs(P1 - P0 - dP) < 1e-12 * imp)
+    assert abs(L1 - L0 - dL) < 1e-12 * imp * sp.R
+
+
+def test_rigid_only_closed_form():
+    """N_f = 0: symplectic Euler on m rddot = u gives v_n = n dt u/m and
+    x_n = dt^2 (u/m) n(n+1)/2; same for theta with tau/J.  Sampling y_k before u_k
+    (reading A15)."""
+    sp = si.preset(1.0)
+    u = np.array([5.0, -2.0, 0.7])
+    s = O.State(sp, np.zeros((0, 2)), np.zeros((0, 2)), si.ghost_ring(236))
+    K, n_sub = 6, 50
+    y, ua = s.rollout(np.tile(u, (K, 1)), n_sub)
+    acc = np.array([u[0] / sp.m_body, u[1] / sp.m_body, u[2] / sp.J_body])
+    for k in range(K):
+        n = k * n_sub
+        assert y[k, 3:6] == pytest.approx(n * sp.dt * acc, rel=1e-12, abs=1e-300)
+        assert y[k, 0:3] == pytest.approx(sp.dt ** 2 * acc * n * (n + 1) / 2, rel=1e-12, abs=1e-300)
+    assert np.all(ua == u)
+    assert np.all(y[0] == 0.0)
+
+
+def test_ghost_kinematics_rigidity_and_special_cases():
+    """Eq. kinematicghost: R(theta)^T (r_g - r) = r_g^B; theta = pi/2
+    maps (0.2, 0) to offset (0, 0.2); |r_g - r| invariant; rdot_g - rdot is
+    perpendicular to the arm with magnitude |thd| |arm|."""
+    gb = si.ghost_ring(944)
+    body = np.array([0.3, -0.2, 0.7, 0.01, 0.02, -0.3])
+    gp, gv = O.ghosts(gb, body)
+    c, s = math.cos(0.7), math.sin(0.7)
+    arm = gp - body[:2]
+    back = np.stack([c * arm[:, 0] + s * arm[:, 1], -s * arm[:, 0] + c * arm[:, 1]], 1)
+    assert np.abs(back - gb).max() < 1e-12
+    assert np.abs(np.hypot(arm[:, 0], arm[:, 1]) - 0.2).max() < 1e-12
+    rel = gv - body[3:5]
+    assert np.abs((rel * arm).sum(1)).max() < 1e-15
+    assert np.abs(np.hypot(rel[:, 0], rel[:, 1]) - 0.3 * 0.2).max() < 1e-12
+    gp, gv = O.ghosts(np.array([[0.2, 0.0]]), np.array([0, 0, math.pi / 2, 0, 0, 0]))
+    assert gp[0] == pytest.approx([0.0, 0.2], abs=1e-16)
+
+
+def test_pd_gains_and_closed_loop_damping():
+    """K = [J w^2, 2 xi J w] with J = 133.84, w = 0.2 pi, xi = 0.7 -> 52.8379 and
+    117.7318.  On the rigid-only plant the ZOH closed loop (20 Hz sampling of a 0.1 Hz
+    loop) is close to the continuous 2nd-order system: overshoot exp(-pi xi/sqrt(1-xi^2))
+    = 4.6 % for a unit reference step."""
+    sp = si.preset(1.0)
+    assert sp.Kp == pytest.approx(52.8379, abs=1e-4)
+    assert sp.Kd == pytest.approx(117.7318, abs=1e-4)
+    s = O.State(sp, np.zeros((0, 2)), np.zeros((0, 2)), si.ghost_ring(236))
+    K = 400                                             # 20 s at T_s = 50 ms
+    th_ref = np.full(K, 0.1)
+    y, ua = s.rollout(np.zeros((K, 3)), 50, theta_ref=th_ref, Kp=sp.Kp, Kd=sp.Kd)
+    over = y[:, 2].max() / 0.1 - 1.0
+    assert 0.025 < over < 0.07
+    assert abs(y[-1, 2] - 0.1) < 2e-3
+    # ZOH torque law evaluated on the sample
+    assert ua[:, 2] == pytest.approx(sp.Kp * (th_ref - y[:, 2]) - sp.Kd * y[:, 5], rel=1e-12, abs=1e-12)
+
+
+def test_hydrostatic_momentum_identity_under_gravity():
+    """With an external acceleration g on the fluid (hydrostatic variant):
+    fluid-on-body force + sum_i m a_i = M_f g exactly (internal and wall pairs cancel)."""
+    t = si.make_tank(1.0, jitter=0.03, seed=2, gy=-0.05)
+    sp = t.params
+    body = np.array([0.0, 0.0, 0.1, 0.0, 0.0, 0.0])
+    gp, gv = O.ghosts(t.ghost_b, body)
+    rho, P = O.density(sp, t.pos, gp)
+    acc, Fb, _ = O.forces(sp, t.pos, t.vel, rho, P, gp, gv, body)
+    Mf = sp.mass * t.n_fluid
+    lhs = Fb + sp.mass * acc.sum(0)
+    scale = sp.mass * np.abs(acc).sum()
+    assert np.abs(lhs - Mf * np.array([0.0, -0.05])).max() < 1e-12 * scale
+
+
+def test_settled_state_is_at_rest_and_stays(settled_c1):
+    """P:324 ("velocities converge to zero") and zero-g rest: after the damped settle
+    the fluid is at rest at rho ~ rho0 and stays at rest for 200 free steps; the body barely
+    moves (momentum exchange only)."""
+    t, s0 = settled_c1
+    s = O.State(t.params, s0.pos, s0.vel, t.ghost_b)
+    v0 = np.abs(s.vel).max()
+    assert v0 < 1e-4
+    rho = s.step(want_rho=True)
+    assert np.abs(rho / t.params.rho0 - 1).max() < 1e-3
+    s.step(n=199)
+    # residual motion stays tiny against the acoustic speed c = sqrt(k) = 1.73 m/s
+    assert np.abs(s.vel).max() < 1e-4
+    assert np.abs(s.body[3:5]).max() < 1e-8
+
+
+def test_no_tunnelling_under_strong_actuation(settled_c1):
+    """every fluid particle stays within R + s of the tank centre (reading A4, F3)."""
+    t, s0 = settled_c1
+    s = O.State(t.params, s0.pos, s0.vel, t.ghost_b)
+    for _ in range(10):
+        s.step((100.0, 60.0, 5.0), n=50)
+        d = np.hypot(s.pos[:, 0] - s.body[0], s.pos[:, 1] - s.body[1])
+        assert d.max() < t.params.R + t.params.spacing
+
+
+def test_mass_is_conserved_by_construction():
+    """Mass: the particle count and m are constant (P:71 'mass ... constant'); the step
+    neither creates nor removes particles."""
+    t = si.make_tank(1.0, jitter=0.02, seed=1)
+    s = O.State.from_tank(t)
+    s.step(n=5)
+    assert s.pos.shape == t.pos.shape and np.isfinite(s.pos).all()
