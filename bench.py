@@ -1,0 +1,412 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native SPH hot path (contract: see DESIGN.md "Measurement").
+
+Metric (BASELINE.json): particle-updates/s, device-timed, whole job.  One fluid particle
+advanced one fast substep = one particle-update.  A bench "step" is one slow tick of the
+multi-rate loop: the sample/control kernel plus n_sub = 200 fast substeps
+(rebin, density, forces + wall + integration, body) for every rollout of the batch.
+
+Default workload (N = 1): C3 of SURVEY 8(d) -- 1024 independent rollouts of the C2 tank
+(ell = 4: 9,261 fluid + 944 ghosts), open-loop excitation inputs, settled start.
+With --gpus N (torchrun) each rank runs 1024 rollouts with global-id seeded inputs (weak
+scaling, config C5 layout) and the trajectories are gathered to rank 0 with NCCL.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import sph_inputs as si  # noqa: E402
+
+WORKLOADS = {
+    # name: (ell, rollouts per GPU, description)
+    "C3": (4.0, 1024, "C3: 1024 rollouts x C2 tank (ell=4, 9261 fluid + 944 ghosts), open-loop excitation, 1 GPU"),
+    "C2": (4.0, 1, "C2: single C2 tank (9261 + 944), excitation, latency-bound"),
+    "C4": (42.0, 1, "C4: single ell=42 tank (1,025,788 + 9,912)"),
+    "C1": (1.0, 1, "C1: single ell=1 tank (569 + 236)"),
+}
+METRIC = "particle-updates/sec (device-timed) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "particle-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--rollouts", type=int, default=0, help="override rollouts per GPU")
+    ap.add_argument("--rebin-every", type=int, default=1)
+    ap.add_argument("--skin", type=float, default=0.0, help="skin in units of h (adaptive rebin)")
+    ap.add_argument("--settle-seconds", type=float, default=2.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-substeps", type=int, default=20)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------------------------------
+# workload construction
+# ------------------------------------------------------------------------------------------
+def make_workload(name):
+    ell, _, _ = WORKLOADS[name]
+    t = si.make_tank(ell)
+    return t
+
+
+def settle_on_gpu(t, seconds, device):
+    """Damped settle (reading A17) of one tank on the GPU (product path, untimed)."""
+    from paper_2604_12505_b200 import SphContext
+    ctx = SphContext(t.params, t.pv32(), t.ghost_b, n_rollouts=1, device=device)
+    n = int(round(seconds / t.params.dt))
+    ctx.settle(math.exp(-10.0 * t.params.dt), n)
+    pv = ctx.get_particles(0)
+    st = ctx.get_status()[0]
+    ctx.close()
+    if st[0] != 0:
+        raise RuntimeError(f"settle failed with status {st[0]}")
+    return pv
+
+
+def inputs_for(global_ids, K):
+    return si.ensemble_inputs(global_ids, K)[0]           # [B, K, 3] float32, seed 1000 + id
+
+
+# ------------------------------------------------------------------------------------------
+# oracle baselines (test infrastructure; only here and in tests)
+# ------------------------------------------------------------------------------------------
+def _oracle_sample(args):
+    """Run the float64 oracle on one rollout of the workload for n substeps; returns
+    (particle-updates, seconds)."""
+    name, pv, gid, n_sub_total, u_seq_row = args
+    import oracle as O
+    t = make_workload(name)
+    s = O.State(t.params, pv[:, :2].astype(np.float64), pv[:, 2:].astype(np.float64), t.ghost_b)
+    n_sub = t.params.n_sub
+    t0 = time.perf_counter()
+    done = 0
+    k = 0
+    while done < n_sub_total:
+        m = min(n_sub, n_sub_total - done)
+        s.step(tuple(float(x) for x in u_seq_row[k % len(u_seq_row)]), n=m)
+        done += m
+        k += 1
+    dt = time.perf_counter() - t0
+    return t.n_fluid * n_sub_total, dt
+
+
+def cpu_baseline(name, pv, budget_s=15.0):
+    """Oracle timed on the host cores: independent rollouts of the same workload, one process
+    per core, each sized to ~budget_s of CPU work (bounded sample)."""
+    import concurrent.futures as cf
+    import oracle as O
+    O.build()
+    cores = max(1, min(os.cpu_count() or 1, 32))
+    u = inputs_for([0], 8)[0]
+    # calibrate on a few substeps
+    upd, sec = _oracle_sample((name, pv, 0, 4, u))
+    per_sub = sec / 4
+    n = max(4, int(budget_s / per_sub))
+    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+        t0 = time.perf_counter()
+        res = list(ex.map(_oracle_sample, [(name, pv, g, n, u) for g in range(cores)]))
+        wall = time.perf_counter() - t0
+    total = sum(r[0] for r in res)
+    return {"value": total / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{cores} independent rollouts x {n} substeps of the {name} tank "
+                      f"({WORKLOADS[name][0]:g}-refined, {int(res[0][0] / n)} fluid particles), "
+                      f"float64 C oracle, one process per core, {wall:.1f} s wall"}
+
+
+def run_reference(a):
+    """--impl reference: the oracle as it stands on the host cores, same metric/config."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    O.build()
+    name = a.workload
+    t = make_workload(name)
+    pv = t.pv32()      # lattice start (the settle is untimed and not part of the metric)
+    u = inputs_for([0], 8)[0]
+    import concurrent.futures as cf
+    cores = max(1, min(os.cpu_count() or 1, 32))
+    n_per = 20 if name != "C4" else 1
+    times = []
+    total_upd = 0
+    with cf.ProcessPoolExecutor(max_workers=cores) as ex:
+        for it in range(a.warmup + a.steps):
+            t0 = time.perf_counter()
+            res = list(ex.map(_oracle_sample, [(name, pv, g, n_per, u) for g in range(cores)]))
+            dt = time.perf_counter() - t0
+            if it >= a.warmup:
+                times.append(dt)
+                total_upd += sum(r[0] for r in res)
+    wall = sum(times)
+    value = total_upd / wall
+    ell, Bg, desc = WORKLOADS[name]
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * wall / max(a.steps, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": desc, "sample": f"{cores} rollouts x {n_per} substeps per step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{cores} independent rollouts x {n_per} substeps per step, "
+                                       f"{a.steps} steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+def algorithmic_bytes(kernel, N, G, B):
+    """Bytes the method must move per launch: float32 SoA arrays
+    touched once.  density: read x (8) write (rho, P/rho^2) (8) per particle + ghosts (16);
+    force: read x, v (16) + aux (8), write x, v (16) per particle + ghosts (16 + 8)."""
+    if kernel == "density":
+        return B * (16 * N + 16 * G)
+    if kernel == "force":
+        return B * (40 * N + 24 * G)
+    return None
+
+
+def traffic_from_profiles(kernel, workload):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2604_12505_b200 import SphContext
+    name = a.workload
+    ell, B, desc = WORKLOADS[name]
+    if a.rollouts:
+        B = a.rollouts
+    t = make_workload(name)
+    sp = t.params
+    pv0 = settle_on_gpu(t, a.settle_seconds, local)
+    gids = list(range(rank * B, (rank + 1) * B))
+    K_all = a.warmup + a.steps
+    u_host = inputs_for(gids, K_all)                       # [B, K_all, 3]
+    skin = a.skin * sp.h
+    ctx = SphContext(sp, pv0, t.ghost_b, n_rollouts=B, rebin_every=a.rebin_every,
+                     skin=skin, device=local)
+    u_dev = torch.from_numpy(u_host).to(dev)
+    y_dev = torch.empty((B, K_all, 6), dtype=torch.float32, device=dev)
+    ua_dev = torch.empty((B, K_all, 3), dtype=torch.float32, device=dev)
+    # warm-up (also captures the per-tick CUDA graph)
+    if a.warmup:
+        ctx.rollout(u_dev[:, :a.warmup].contiguous(), y_out=y_dev[:, :a.warmup].contiguous(),
+                    u_applied=ua_dev[:, :a.warmup].contiguous())
+    torch.cuda.synchronize(dev)
+    u_timed = u_dev[:, a.warmup:].contiguous()
+    y_timed = torch.empty((B, a.steps, 6), dtype=torch.float32, device=dev)
+    ua_timed = torch.empty((B, a.steps, 3), dtype=torch.float32, device=dev)
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    ctx.rollout(u_timed, y_out=y_timed, u_applied=ua_timed)
+    e1.record(ctx.stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    st = ctx.get_status()[0]
+    n_failed = int((st != 0).sum())
+    updates = world * B * t.n_fluid * sp.n_sub * a.steps
+    value = updates / (ms_max / 1e3)
+    # NCCL gather of the trajectory dataset (config C5; the only collective on the path)
+    gather_ms = None
+    if world > 1:
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        out = torch.empty((world * B, a.steps, 6), dtype=torch.float32, device=dev)
+        g0.record()
+        dist.all_gather_into_tensor(out, y_timed)
+        g1.record()
+        torch.cuda.synchronize(dev)
+        gather_ms = g0.elapsed_time(g1)
+    # ---- e2e: host buffers through the C ABI, per step H2D of u_k and D2H of y_k ----------
+    K_e2e = max(1, min(a.steps, 5))
+    u_pin = [torch.from_numpy(np.ascontiguousarray(u_host[:, a.warmup + k:a.warmup + k + 1])).pin_memory()
+             for k in range(K_e2e)]
+    y_pin = [torch.empty((B, 1, 6), dtype=torch.float32).pin_memory() for _ in range(K_e2e)]
+    ua_pin = [torch.empty((B, 1, 3), dtype=torch.float32).pin_memory() for _ in range(K_e2e)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    x0 = torch.cuda.Event(enable_timing=True)
+    x1 = torch.cuda.Event(enable_timing=True)
+    x0.record(ctx.stream)
+    for k in range(K_e2e):
+        ctx.rollout(u_pin[k].numpy(), y_out=y_pin[k].numpy(), u_applied=ua_pin[k].numpy())
+    x1.record(ctx.stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = x0.elapsed_time(x1)
+    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * t.n_fluid * sp.n_sub * K_e2e / (float(e2e_t.item()) / 1e3)
+    # ---- per-kernel device times (CUDA events on the context stream, same data) -----------
+    prof = ctx.profile(a.profile_substeps)
+    kern = {k: v for k, v in prof.items() if k != "substep"}
+    top = max(("density", "force"), key=lambda k: kern[k])
+    alg = algorithmic_bytes(top, t.n_fluid, t.n_ghost, B)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg / (kern[top] / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": f"k_{top}", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic_from_profiles(top, name),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6.65 TB/s",
+            "algorithmic_bytes_per_launch": alg, "kernel_ms": kern[top],
+            "kernel_share_of_substep": kern[top] / prof["substep"],
+            "kernel_ms_all": kern, "substep_ms_profiled": prof["substep"]}
+    launches = a.steps * (1 + sp.n_sub * ctx.launches_per_substep())
+    ctx.close()
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(name, pv0)
+        except Exception as ex:  # never fail the bench line on the baseline
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "oracle", "sample": f"failed: {ex}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (body f64)",
+        "data": "synthetic (seeded lattice tank, GPU damped settle, multisine+pulse excitation)",
+        "config": {"workload": desc, "rollouts_per_gpu": B, "fluid_per_rollout": t.n_fluid,
+                   "ghosts_per_rollout": t.n_ghost, "substeps_per_step": sp.n_sub,
+                   "dt": sp.dt, "rebin_every": a.rebin_every, "skin_h": a.skin,
+                   "parallelism": f"ensemble dp{world}",
+                   "l2": f"no flush: working set {ctx_bytes_gb(t, B):.2f} GB > 126 MB L2",
+                   "failed_rollouts": n_failed, "gather_ms": gather_ms},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 3 * 4,
+                "d2h_bytes_per_step": B * (6 + 3) * 4, "steps": K_e2e},
+        "gpu_launches": launches,
+        "clocks": ck,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def ctx_bytes_gb(t, B):
+    return B * t.n_fluid * 64 / 1e9
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+    try:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+if __name__ == "__main__":
+    main()

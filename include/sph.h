@@ -1,0 +1,183 @@
+/* include/sph.h -- C ABI of the B200-native SPH fuel-sloshing hot path (libsphb200.so).
+ *
+ * The library advances the coupled spacecraft + fluid model of arXiv 2604.12505 (P:n = line n
+ * of the paper text, PAPER.md):  Sigma: xdot = f(x,u), y = h(x,u)  (Eq. NLmodel),
+ * f = Algorithm 1 integrated with first-order symplectic Euler, the
+ * multi-rate sample / control loop of P:263 and P:325, for B independent rollouts at once
+ * (batched ensemble) on one GPU.  Every step of the path runs in the library's sm_100a
+ * kernels; the caller provides device memory (e.g. a torch tensor) and a CUDA stream.
+ *
+ * Conventions
+ *  - SI units, 2-D: rho in kg/m^2, P in N/m.  Particle state is float32; body state is float64.
+ *  - Particle data crosses the ABI in CANONICAL order (the order the caller supplied at init);
+ *    internal sorting by cell is invisible.
+ *  - Body state layout (6 doubles) = y = [r_x r_y theta rdot_x rdot_y thetadot].
+ *  - Input u = [u_x u_y tau] in the world frame at the CoM.
+ *  - Errors: every call returns sph_status; nothing throws or aborts across the ABI.
+ *    Argument / configuration errors return SPH_EINVAL before any device work.
+ *    Numerical failure is per rollout (status 1 non-finite, 2 |x| > 1e9, 3 particle left the
+ *    grid = tunnelled): that rollout freezes, the others continue, calls return SPH_OK and
+ *    sph_get_status reports it; SPH_EBLOWUP only if every rollout failed.
+ *  - Ownership: the caller owns the device workspace and every host buffer; the library never
+ *    frees them.  The context owns only CUDA handles (graphs, events) and small staging
+ *    buffers for host-pointer calls.
+ *  - Streams: all device work is enqueued on the context's stream; calls that return host data
+ *    synchronise that stream.  One context per host thread; several contexts per process are
+ *    allowed.
+ *  - Determinism: identical inputs give bitwise identical outputs, independent of the number
+ *    of rollouts in the batch and of a rollout's position in it.
+ */
+#ifndef SPH_H
+#define SPH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPH_OK = 0,
+    SPH_EINVAL = 1,   /* bad argument or configuration                      */
+    SPH_ENOMEM = 2,   /* workspace too small / staging allocation failed     */
+    SPH_ECUDA = 3,    /* CUDA runtime error (message in sph_last_error)      */
+    SPH_EBLOWUP = 4,  /* every rollout has a non-zero numerical status       */
+    SPH_ESTATE = 6    /* call not valid in the context's current state       */
+} sph_status;
+
+typedef struct sph_ctx sph_ctx;
+
+/* Fluid parameters: Table 2 plus the readings of DESIGN.md. */
+typedef struct {
+    double rho0;        /* base density rho_0 (Eq. EOS)                        */
+    double k;           /* stiffness k (Eq. EOS)                                           */
+    double alpha;       /* artificial viscosity factor (Eq. viscous)           */
+    double beta;        /* boundary viscosity factor (Eq. viscous_b2f)          */
+    double gamma1;      /* ghost density correction (Eq. density_update), (0,1] */
+    double eps;         /* epsilon of the viscous denominators, > 0                */
+    double h;           /* smoothing length h > 0 (cubic support 2h, spiky support h)      */
+    double mass;        /* fluid particle mass m > 0 (reading R1: rho0 s^2)                */
+    double w_cb_const;  /* cubic-spline constant C in C/h^2 (reading A1: 5/(14 pi))        */
+    double ghost_pressure_sign; /* -1 repulsive wall (reading A4), +1 literal Alg. 1       */
+    double gravity[2];  /* external acceleration on the fluid, world frame (0 = zero-g)    */
+} sph_fluid_params;
+
+/* Rigid spacecraft: Table 1.  Tank = circle of radius tank_radius at the CoM. */
+typedef struct {
+    double m;            /* mass > 0                 */
+    double J;            /* inertia > 0              */
+    double tank_radius;  /* inner wall radius R > 0  */
+} sph_body_params;
+
+/* Time stepping.  rebin_every = 1 rebuilds the cell list every substep; 0 rebuilds
+ * adaptively when a particle may have moved more than skin/2 since the last rebuild (cells
+ * are then 2h + skin wide, neighbour sets stay exact). */
+typedef struct {
+    double dt;                /* fast step > 0                                 */
+    int substeps_per_sample;  /* n_sub = T_s / dt >= 1 (multi-rate)    */
+    int rebin_every;          /* 1 = every substep, 0 = adaptive with skin     */
+    double skin;              /* >= 0, only used when rebin_every == 0         */
+} sph_time_params;
+
+/* PD attitude law tau_k = Kp (theta_ref_k - theta_k) - Kd thetadot_k, ZOH. */
+typedef struct {
+    double Kp, Kd;
+    const float* theta_ref;   /* [B][K]; same memory space as the call's other pointers */
+} sph_pd_attitude;
+
+/* Bytes of device workspace needed for B rollouts of n_fluid + n_ghost particles. 0 on bad args. */
+size_t sph_workspace_bytes(const sph_fluid_params* fp, const sph_body_params* bp,
+                           const sph_time_params* tp, int n_fluid, int n_ghost, int n_rollouts);
+
+/* Create a context for B = n_rollouts identical tanks (the benchmark scenario):
+ * fluid_pv  host float[n_fluid][4] = (x, y, vx, vy) world frame, canonical order;
+ * ghost_body_xy host double[n_ghost][2] = body-frame ghost positions (fixed),
+ *           uniformly spaced on the wall circle in angular order;
+ * body at rest at the origin, theta = 0.  cuda_stream = cudaStream_t (NULL = default).
+ * d_workspace: device memory of at least sph_workspace_bytes(...) bytes, 256-B aligned. */
+sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
+                         const sph_time_params* tp, int n_fluid, const float* fluid_pv,
+                         int n_ghost, const double* ghost_body_xy, int n_rollouts,
+                         void* cuda_stream, void* d_workspace, size_t workspace_bytes,
+                         sph_ctx** out);
+
+/* Replace the particle state of one rollout (rollout = -1: all) from host float[n_fluid][4]
+ * in canonical order; body (host double[6]) may be NULL to keep it.  Clears its status. */
+sph_status sph_set_state(sph_ctx* ctx, int rollout, const float* fluid_pv, const double* body);
+
+/* Set all body states from host double[B][6]. */
+sph_status sph_set_body_state(sph_ctx* ctx, const double* body);
+
+/* Copy one rollout's particles to host float[n_fluid][4] (canonical order).  rho (nullable):
+ * host float[n_fluid], the densities evaluated in the last substep. */
+sph_status sph_get_particles(sph_ctx* ctx, int rollout, float* fluid_pv, float* rho);
+
+/* Copy one rollout's ghost world state (Eq. kinematicghost at the current body state) to host
+ * float[n_ghost][4] = (x, y, vx, vy). */
+sph_status sph_get_ghosts(sph_ctx* ctx, int rollout, float* ghost_pv);
+
+/* Apply n_substeps substeps of the symplectic-Euler map with u held (ZOH).  u: [B][3]
+ * (device pointer if ptr_on_device, else host). */
+sph_status sph_step(sph_ctx* ctx, const float* u, int n_substeps, int ptr_on_device);
+
+/* Multi-rate rollout (dataset D_N of Eq. dataset): for k < K sample
+ * y_k = y(k T_s) BEFORE applying u_k, set u_k = u_seq[b][k] (tau overridden by the PD law when
+ * pd != NULL), then run n_sub substeps.  u_seq [B][K][3], y_out [B][K][6], u_applied [B][K][3]
+ * (nullable), all float32, device pointers if ptr_on_device else host. */
+sph_status sph_rollout_batch(sph_ctx* ctx, const float* u_seq, int K, const sph_pd_attitude* pd,
+                             float* y_out, float* u_applied, int ptr_on_device);
+
+/* Current body states, host double[B][6] (P:70 output y). */
+sph_status sph_get_body_state(sph_ctx* ctx, double* out);
+
+/* Damped settling (reading A17): n_steps substeps with the body pinned at rest and the
+ * fluid velocities multiplied by `damping` after each substep. */
+sph_status sph_settle(sph_ctx* ctx, double damping, int n_steps);
+
+/* Per-rollout numerical status (host int32[B]); bad_step (host int64[B], nullable) = substep
+ * index of the failure; bad_particle (host int32[B], nullable) = canonical particle id. */
+sph_status sph_get_status(sph_ctx* ctx, int32_t* rollout_status, int64_t* bad_step,
+                          int32_t* bad_particle);
+
+/* Parity / debug (reading A19).  Canonical float32 cell (c_x, c_y) of every particle of one
+ * rollout at the current state: o = float(r_body) - half, c = floor((x - o) * inv), no FMA.
+ * cells host int32[n_fluid][2]; grid host float[4] = (o_x, o_y, inv, cell side). */
+sph_status sph_debug_cells(sph_ctx* ctx, int rollout, int32_t* cells, float* grid);
+
+/* Neighbour sets of one rollout at the current state, from the cell-list enumeration the
+ * kernels use: NF(i) (fluid, |r|^2 < (2h)^2, j != i), NG2(i) (ghosts within 2h), NG1(i)
+ * (ghosts within h); float32 predicates, no FMA.  CSR in canonical order with ascending ids:
+ * *_off host int64[n_fluid+1], *_idx host int32[cap].  Returns SPH_ENOMEM if cap too small. */
+sph_status sph_debug_neighbours(sph_ctx* ctx, int rollout, int64_t* nf_off, int32_t* nf_idx,
+                                int64_t nf_cap, int64_t* g2_off, int32_t* g2_idx,
+                                int64_t g2_cap, int64_t* g1_off, int32_t* g1_idx,
+                                int64_t g1_cap);
+
+/* Kernel timing (CUDA events on the context stream, no graph): runs n_substeps substeps with
+ * u held and writes the average device time per launch in ms of each kernel into
+ * ms[SPH_NUM_TIMERS] (order: see SPH_TIMER_* below). */
+enum {
+    SPH_TIMER_HASH = 0, SPH_TIMER_SCAN = 1, SPH_TIMER_SCATTER = 2, SPH_TIMER_CELLSORT = 3,
+    SPH_TIMER_GATHER = 4, SPH_TIMER_DENSITY = 5, SPH_TIMER_FORCE = 6, SPH_TIMER_BODY = 7,
+    SPH_TIMER_SUBSTEP = 8, SPH_NUM_TIMERS = 9
+};
+sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms);
+
+/* Number of our kernel launches one substep issues (for the bench's gpu_launches count). */
+int sph_launches_per_substep(const sph_ctx* ctx);
+
+/* Sizes of the context (any pointer may be NULL). */
+void sph_get_sizes(const sph_ctx* ctx, int* n_fluid, int* n_ghost, int* n_rollouts,
+                   int* n_cells);
+
+/* Last error message of this context (or of the last failed sph_init_tank when ctx == NULL). */
+const char* sph_last_error(const sph_ctx* ctx);
+
+/* Destroy the context (CUDA handles only; the workspace stays the caller's). */
+void sph_destroy(sph_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPH_H */

@@ -93,7 +93,14 @@ static void grid_build(grid_t* g, int n, const double* pts, double cs) {
     g->x0 = xmin;
     g->y0 = ymin;
     double fx = (xmax - xmin) / cs + 1.0, fy = (ymax - ymin) / cs + 1.0;
-    if (n == 0 || !(fx * fy < 4.0 * n + 1e6)) { /* degenerate / exploded: one cell */
+    /* sparse point sets (e.g. a ghost ring): coarser cells are still correct for a query
+       radius <= cell side (3 x 3 cells are scanned) */
+    for (int k = 0; k < 40 && fx * fy > 4.0 * n + 4e6; k++) {
+        g->cs *= 2.0;
+        fx = (xmax - xmin) / g->cs + 1.0;
+        fy = (ymax - ymin) / g->cs + 1.0;
+    }
+    if (n == 0 || !(fx * fy <= 4.0 * n + 4e6)) { /* degenerate / exploded: one cell */
         g->nx = 1;
         g->ny = 1;
         g->cs = INFINITY;

@@ -1,0 +1,291 @@
+"""Thin ctypes binding over libsphb200.so (include/sph.h).  Argument marshalling only:
+every step of the SPH path runs in the library's sm_100a kernels.  PyTorch provides the device
+workspace, the CUDA stream and device tensors for inputs / outputs.
+
+There is no CPU fallback: if the CUDA library is missing, ``lib()`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsphb200.so")
+
+SPH_OK, SPH_EINVAL, SPH_ENOMEM, SPH_ECUDA, SPH_EBLOWUP, SPH_ESTATE = 0, 1, 2, 3, 4, 6
+TIMER_NAMES = ["hash", "scan", "scatter", "cellsort", "gather", "density", "force", "body",
+               "substep"]
+
+
+class FluidParams(C.Structure):
+    _fields_ = [("rho0", C.c_double), ("k", C.c_double), ("alpha", C.c_double),
+                ("beta", C.c_double), ("gamma1", C.c_double), ("eps", C.c_double),
+                ("h", C.c_double), ("mass", C.c_double), ("w_cb_const", C.c_double),
+                ("ghost_pressure_sign", C.c_double), ("gravity", C.c_double * 2)]
+
+
+class BodyParams(C.Structure):
+    _fields_ = [("m", C.c_double), ("J", C.c_double), ("tank_radius", C.c_double)]
+
+
+class TimeParams(C.Structure):
+    _fields_ = [("dt", C.c_double), ("substeps_per_sample", C.c_int), ("rebin_every", C.c_int),
+                ("skin", C.c_double)]
+
+
+class PdAttitude(C.Structure):
+    _fields_ = [("Kp", C.c_double), ("Kd", C.c_double), ("theta_ref", C.c_void_p)]
+
+
+class SphError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load libsphb200.so (fails loudly when the CUDA extension was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SphError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, dbl = C.c_void_p, C.c_int, C.c_int64, C.c_double
+        sig = {
+            "sph_workspace_bytes": (C.c_size_t, [vp, vp, vp, i32, i32, i32]),
+            "sph_init_tank": (i32, [vp, vp, vp, i32, vp, i32, vp, i32, vp, vp, C.c_size_t, vp]),
+            "sph_set_state": (i32, [vp, i32, vp, vp]),
+            "sph_set_body_state": (i32, [vp, vp]),
+            "sph_get_particles": (i32, [vp, i32, vp, vp]),
+            "sph_get_ghosts": (i32, [vp, i32, vp]),
+            "sph_step": (i32, [vp, vp, i32, i32]),
+            "sph_rollout_batch": (i32, [vp, vp, i32, vp, vp, vp, i32]),
+            "sph_get_body_state": (i32, [vp, vp]),
+            "sph_settle": (i32, [vp, dbl, i32]),
+            "sph_get_status": (i32, [vp, vp, vp, vp]),
+            "sph_debug_cells": (i32, [vp, i32, vp, vp]),
+            "sph_debug_neighbours": (i32, [vp, i32, vp, vp, i64, vp, vp, i64, vp, vp, i64]),
+            "sph_profile_substeps": (i32, [vp, i32, vp]),
+            "sph_launches_per_substep": (i32, [vp]),
+            "sph_get_sizes": (None, [vp, vp, vp, vp, vp]),
+            "sph_last_error": (C.c_char_p, [vp]),
+            "sph_destroy": (None, [vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return ["sph_workspace_bytes", "sph_init_tank", "sph_set_state", "sph_set_body_state",
+            "sph_get_particles", "sph_get_ghosts", "sph_step", "sph_rollout_batch",
+            "sph_get_body_state", "sph_settle", "sph_get_status", "sph_debug_cells",
+            "sph_debug_neighbours", "sph_profile_substeps", "sph_launches_per_substep",
+            "sph_get_sizes", "sph_last_error", "sph_destroy"]
+
+
+def fluid_params(sp) -> FluidParams:
+    g = FluidParams(sp.rho0, sp.k, sp.alpha, sp.beta, sp.gamma1, sp.eps, sp.h, sp.mass,
+                    sp.w_cb_const, sp.ghost_pressure_sign)
+    g.gravity[0] = sp.gx
+    g.gravity[1] = sp.gy
+    return g
+
+
+def body_params(sp) -> BodyParams:
+    return BodyParams(sp.m_body, sp.J_body, sp.R)
+
+
+def time_params(sp, rebin_every: int = 1, skin: float = 0.0) -> TimeParams:
+    return TimeParams(sp.dt, int(sp.n_sub), int(rebin_every), float(skin))
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _host(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+class SphContext:
+    """One batched ensemble of B identical tanks on one GPU (sph_init_tank)."""
+
+    def __init__(self, sp, fluid_pv, ghost_b, n_rollouts: int = 1, rebin_every: int = 1,
+                 skin: float = 0.0, device: int = 0):
+        import torch
+        self.torch = torch
+        self.L = lib()
+        self.device = torch.device("cuda", device)
+        self.fp, self.bp = fluid_params(sp), body_params(sp)
+        self.tp = time_params(sp, rebin_every, skin)
+        pv = _host(fluid_pv, np.float32).reshape(-1, 4)
+        gb = _host(ghost_b, np.float64).reshape(-1, 2)
+        self.N, self.G, self.B = pv.shape[0], gb.shape[0], int(n_rollouts)
+        nbytes = self.L.sph_workspace_bytes(C.byref(self.fp), C.byref(self.bp), C.byref(self.tp),
+                                            self.N, self.G, self.B)
+        if nbytes == 0:
+            raise SphError("invalid parameters (sph_workspace_bytes returned 0)")
+        with torch.cuda.device(self.device):
+            self.stream = torch.cuda.Stream(self.device)
+            self.workspace = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        self.workspace_bytes = int(nbytes)
+        ctx = C.c_void_p()
+        st = self.L.sph_init_tank(C.byref(self.fp), C.byref(self.bp), C.byref(self.tp), self.N,
+                                  pv.ctypes.data, self.G, gb.ctypes.data, self.B,
+                                  self.stream.cuda_stream, self.workspace.data_ptr(), nbytes,
+                                  C.byref(ctx))
+        if st != SPH_OK:
+            raise SphError(f"sph_init_tank: {st}: {self.L.sph_last_error(None).decode()}")
+        self.ctx = ctx
+        self.n_sub = int(sp.n_sub)
+        nc = C.c_int()
+        self.L.sph_get_sizes(self.ctx, None, None, None, C.byref(nc))
+        self.n_cells = nc.value
+
+    # -- helpers ------------------------------------------------------------------------
+    def _check(self, st, what):
+        if st != SPH_OK:
+            msg = self.L.sph_last_error(self.ctx).decode()
+            raise SphError(f"{what}: status {st}: {msg}")
+
+    def _dev_in(self, t):
+        """Order the context stream after torch's current stream (device inputs)."""
+        self.stream.wait_stream(self.torch.cuda.current_stream(self.device))
+        return t
+
+    def _dev_out(self):
+        self.torch.cuda.current_stream(self.device).wait_stream(self.stream)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.L.sph_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- state ---------------------------------------------------------------------------
+    def set_state(self, fluid_pv, rollout: int = -1, body=None):
+        pv = _host(fluid_pv, np.float32).reshape(self.N, 4)
+        bd = None if body is None else _host(body, np.float64).reshape(6)
+        self._check(self.L.sph_set_state(self.ctx, rollout, pv.ctypes.data,
+                                         None if bd is None else bd.ctypes.data), "sph_set_state")
+
+    def set_body_state(self, body):
+        bd = _host(body, np.float64).reshape(self.B, 6)
+        self._check(self.L.sph_set_body_state(self.ctx, bd.ctypes.data), "sph_set_body_state")
+
+    def get_particles(self, rollout: int = 0, with_rho: bool = False):
+        pv = np.zeros((self.N, 4), np.float32)
+        rho = np.zeros(self.N, np.float32) if with_rho else None
+        self._check(self.L.sph_get_particles(self.ctx, rollout, pv.ctypes.data,
+                                             None if rho is None else rho.ctypes.data),
+                    "sph_get_particles")
+        return (pv, rho) if with_rho else pv
+
+    def get_ghosts(self, rollout: int = 0):
+        g = np.zeros((self.G, 4), np.float32)
+        self._check(self.L.sph_get_ghosts(self.ctx, rollout, g.ctypes.data), "sph_get_ghosts")
+        return g
+
+    def get_body_state(self):
+        out = np.zeros((self.B, 6), np.float64)
+        self._check(self.L.sph_get_body_state(self.ctx, out.ctypes.data), "sph_get_body_state")
+        return out
+
+    def get_status(self):
+        st = np.zeros(self.B, np.int32)
+        bs = np.zeros(self.B, np.int64)
+        bp = np.zeros(self.B, np.int32)
+        self._check(self.L.sph_get_status(self.ctx, st.ctypes.data, bs.ctypes.data, bp.ctypes.data),
+                    "sph_get_status")
+        return st, bs, bp
+
+    # -- dynamics ------------------------------------------------------------------------
+    def step(self, u, n_substeps: int = 1):
+        """u: [B,3] (numpy -> host path; cuda tensor -> device path)."""
+        if hasattr(u, "is_cuda") and u.is_cuda:
+            u = self._dev_in(u.contiguous().float())
+            self._check(self.L.sph_step(self.ctx, u.data_ptr(), int(n_substeps), 1), "sph_step")
+            self._dev_out()
+        else:
+            uu = _host(np.broadcast_to(np.asarray(u, np.float32), (self.B, 3)), np.float32)
+            self._check(self.L.sph_step(self.ctx, uu.ctypes.data, int(n_substeps), 0), "sph_step")
+
+    def settle(self, damping: float, n_steps: int):
+        self._check(self.L.sph_settle(self.ctx, float(damping), int(n_steps)), "sph_settle")
+
+    def rollout(self, u_seq, theta_ref=None, Kp: float = 0.0, Kd: float = 0.0, y_out=None,
+                u_applied=None):
+        """Multi-rate rollout.  Device tensors -> device path (outputs must be given or are
+        allocated as cuda tensors); numpy -> host path.  Returns (y, u_applied)."""
+        torch = self.torch
+        on_dev = hasattr(u_seq, "is_cuda") and u_seq.is_cuda
+        if on_dev:
+            K = int(u_seq.shape[1])
+            u_seq = self._dev_in(u_seq.contiguous())
+            if y_out is None:
+                y_out = torch.empty((self.B, K, 6), dtype=torch.float32, device=self.device)
+            if u_applied is None:
+                u_applied = torch.empty((self.B, K, 3), dtype=torch.float32, device=self.device)
+            th = None if theta_ref is None else theta_ref.contiguous()
+            pd = None if th is None else PdAttitude(Kp, Kd, th.data_ptr())
+            self._check(self.L.sph_rollout_batch(self.ctx, u_seq.data_ptr(), K,
+                                                 None if pd is None else C.byref(pd),
+                                                 y_out.data_ptr(), u_applied.data_ptr(), 1),
+                        "sph_rollout_batch")
+            self._dev_out()
+            return y_out, u_applied
+        u_seq = _host(u_seq, np.float32)
+        K = u_seq.shape[1]
+        y = y_out if y_out is not None else np.zeros((self.B, K, 6), np.float32)
+        ua = u_applied if u_applied is not None else np.zeros((self.B, K, 3), np.float32)
+        th = None if theta_ref is None else _host(theta_ref, np.float32)
+        pd = None if th is None else PdAttitude(Kp, Kd, _ptr(th))
+        self._check(self.L.sph_rollout_batch(self.ctx, _ptr(u_seq), K,
+                                             None if pd is None else C.byref(pd), _ptr(y),
+                                             _ptr(ua), 0), "sph_rollout_batch")
+        return y, ua
+
+    # -- parity / debug -----------------------------------------------------------------
+    def debug_cells(self, rollout: int = 0):
+        cells = np.zeros((self.N, 2), np.int32)
+        grid = np.zeros(4, np.float32)
+        self._check(self.L.sph_debug_cells(self.ctx, rollout, cells.ctypes.data, grid.ctypes.data),
+                    "sph_debug_cells")
+        return cells, grid
+
+    def debug_neighbours(self, rollout: int = 0, cap: int | None = None):
+        cap = cap or max(64, 40 * self.N)
+        arrs = []
+        args = []
+        for _ in range(3):
+            off = np.zeros(self.N + 1, np.int64)
+            idx = np.zeros(cap, np.int32)
+            arrs.append((off, idx))
+            args += [off.ctypes.data, idx.ctypes.data, cap]
+        self._check(self.L.sph_debug_neighbours(self.ctx, rollout, *args), "sph_debug_neighbours")
+        return [(off, idx[:off[-1]].copy()) for off, idx in arrs]
+
+    def profile(self, n_substeps: int = 10):
+        ms = np.zeros(len(TIMER_NAMES), np.float32)
+        self._check(self.L.sph_profile_substeps(self.ctx, int(n_substeps), ms.ctypes.data),
+                    "sph_profile_substeps")
+        return dict(zip(TIMER_NAMES, ms.tolist()))
+
+    def launches_per_substep(self):
+        return int(self.L.sph_launches_per_substep(self.ctx))

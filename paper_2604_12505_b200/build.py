@@ -1,0 +1,39 @@
+"""Build recipe of libsphb200.so (nvcc, sm_100a only)."""
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SRC = [os.path.join(HERE, "csrc", "sph_api.cu")]
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("sph_device.cuh", "sph_kernels.cuh")] + \
+    [os.path.join(ROOT, "include", "sph.h")]
+OUT = os.path.join(HERE, "libsphb200.so")
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
+              "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]
+
+
+def nvcc():
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.sep not in cand or os.path.exists(cand)):
+            return cand
+    return "nvcc"
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and os.path.exists(OUT) and \
+            os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in DEPS):
+        return OUT
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *SRC]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    with open(os.path.join(HERE, "csrc", "ptxas_info.txt"), "w") as f:
+        f.write(res.stderr)
+    os.replace(OUT + ".tmp", OUT)
+    if verbose:
+        print(res.stderr)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force=True))

@@ -1,0 +1,643 @@
+// sph_api.cu -- host side of libsphb200.so: the C ABI of include/sph.h.
+// Validation, workspace carve-up, launch sequencing, CUDA-graph capture of a slow tick,
+// canonical-order import/export and the parity/debug entry points.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sph.h"
+#include "sph_kernels.cuh"
+
+using namespace sph;
+
+struct sph_ctx {
+    DevParams P;
+    DevPtrs D;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    float ghost_angle0 = 0.f;
+    std::string err;
+    // graph of one slow tick's substeps (n_sub substeps, damping 1, body free)
+    cudaGraphExec_t tick_graph = nullptr;
+    // staging for host-pointer calls (ctx-owned)
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
+    int* dbg_buf = nullptr;
+    int n_sub = 1;
+};
+
+static std::string g_init_err;
+
+#define CK(expr)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (expr);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            ctx->err = std::string(#expr) + ": " + cudaGetErrorString(e_);             \
+            return SPH_ECUDA;                                                          \
+        }                                                                              \
+    } while (0)
+
+static sph_status fail(sph_ctx* ctx, sph_status s, const std::string& m) {
+    if (ctx) ctx->err = m;
+    else g_init_err = m;
+    return s;
+}
+
+// ---------------------------------------------------------------------------------------
+// Parameters and layout
+// ---------------------------------------------------------------------------------------
+static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
+                        const sph_time_params* tp, int N, int G, int B, DevParams* P,
+                        std::string* why) {
+    if (!fp || !bp || !tp) return *why = "null parameter struct", false;
+    if (N < 0 || G < 0 || B < 1) return *why = "n_fluid, n_ghost must be >= 0, n_rollouts >= 1", false;
+    if (!(fp->h > 0) || !(fp->rho0 > 0) || !(fp->mass > 0) || !(fp->k >= 0) ||
+        !(fp->gamma1 > 0 && fp->gamma1 <= 1) || !(fp->eps > 0) || !(fp->alpha >= 0) ||
+        !(fp->beta >= 0) || !(fp->w_cb_const > 0) || !std::isfinite(fp->gravity[0]) ||
+        !std::isfinite(fp->gravity[1]))
+        return *why = "invalid fluid parameters (h, rho0, mass > 0, k >= 0, gamma1 in (0,1], eps > 0, alpha, beta >= 0)", false;
+    if (!(bp->m > 0) || !(bp->J > 0) || !(bp->tank_radius > 0))
+        return *why = "invalid body parameters (m, J, tank_radius > 0)", false;
+    if (!(tp->dt > 0) || tp->substeps_per_sample < 1 || tp->rebin_every < 0 || tp->rebin_every > 1 ||
+        !(tp->skin >= 0))
+        return *why = "invalid time parameters (dt > 0, substeps_per_sample >= 1, rebin_every in {0,1}, skin >= 0)", false;
+    if (tp->rebin_every == 0 && !(tp->skin > 0))
+        return *why = "adaptive rebinning (rebin_every = 0) needs skin > 0", false;
+    const double h = fp->h, R = bp->tank_radius;
+    std::memset(P, 0, sizeof(*P));
+    P->N = N;
+    P->G = G;
+    P->B = B;
+    const double Cd = 2.0 * h + (tp->rebin_every ? 0.0 : tp->skin);
+    P->C = (float)Cd;
+    P->inv_C = 1.0f / P->C;
+    const int half_cells = (int)std::ceil(R / (double)P->C) + 2;
+    P->nx = 2 * half_cells;
+    if ((double)P->nx * P->nx > 2.0e9 / std::max(B, 1))
+        return *why = "cell grid too large", false;
+    P->ncell = P->nx * P->nx;
+    P->half = (float)half_cells * P->C;
+    P->ntile = std::max(1, (N + TILE - 1) / TILE);
+    P->nscan = (P->ncell + 1 + SCAN_TILE - 1) / SCAN_TILE;
+    if ((P->nscan + SCAN_T - 1) / SCAN_T > SCAN_V) return *why = "cell grid too large for the scan", false;
+    P->h = (float)h;
+    P->inv_h = (float)(1.0 / h);
+    const float H = (float)(2.0 * h);
+    P->H2 = H * H;                        // float32 (2h)^2 (reading A19)
+    P->h2 = P->h * P->h;
+    P->mass = (float)fp->mass;
+    P->m2 = (float)(fp->mass * fp->mass);
+    P->rho0 = (float)fp->rho0;
+    P->k = (float)fp->k;
+    P->gamma1 = (float)fp->gamma1;
+    P->alpha2h = (float)(2.0 * fp->alpha * h);
+    P->beta = (float)fp->beta;
+    P->eps_h2 = (float)(fp->eps * h * h);
+    P->wcb = (float)(fp->w_cb_const / (h * h));
+    P->dwcb = (float)(fp->w_cb_const / (h * h * h));
+    P->dws3 = (float)(-30.0 / (M_PI * std::pow(h, 5)));
+    P->gsign2m2 = (float)(fp->ghost_pressure_sign * 2.0 * fp->mass * fp->mass);
+    P->gx = (float)fp->gravity[0];
+    P->gy = (float)fp->gravity[1];
+    P->dt = (float)tp->dt;
+    P->dtd = tp->dt;
+    P->m_body = bp->m;
+    P->J_body = bp->J;
+    P->rebin_every = tp->rebin_every;
+    P->skin_half = (float)(0.5 * tp->skin);
+    // ghost-ring window (see for_ghost_candidates): only particles farther than d_min from the
+    // centre can have a ghost within 2h; their ghosts lie within +-dphi of their polar angle.
+    const double d_min = R - 2.0 * h - 1e-3 * h;
+    P->ghost_scale = (float)(G / (2.0 * M_PI));
+    P->ghost_full = 1;
+    P->wall_r2 = -1.0f;
+    if (G > 0 && d_min > 0) {
+        const double arg = h / std::sqrt(d_min * R);
+        if (arg < 1.0) {
+            const double dphi = 2.0 * std::asin(arg);
+            const int K = (int)std::ceil(dphi * G / (2.0 * M_PI)) + 2;
+            if (2 * K + 1 < G) {
+                P->ghost_full = 0;
+                P->ghost_K = K;
+                P->wall_r2 = std::nextafter((float)(d_min * d_min), 0.0f);
+            }
+        }
+    }
+    return true;
+}
+
+struct Layout {
+    size_t off[32];
+    size_t total;
+};
+
+static Layout layout(const DevParams& P) {
+    Layout L;
+    size_t o = 0;
+    int k = 0;
+    const size_t BN = (size_t)P.B * P.N, BG = (size_t)P.B * P.G;
+    auto put = [&](size_t bytes) {
+        L.off[k++] = o;
+        o += (bytes + 255) & ~(size_t)255;
+    };
+    put(BN * 8); put(BN * 8);           // pos[2]        0 1
+    put(BN * 8); put(BN * 8);           // vel[2]        2 3
+    put(BN * 4); put(BN * 4);           // id[2]         4 5
+    put(BN * 8);                        // aux           6
+    put(BN * 4); put(BN * 4);           // skey key      7 8
+    put(BN * 4); put(BN * 4);           // rank perm     9 10
+    put((size_t)P.B * P.ncell * 4);     // counts        11
+    put((size_t)P.B * (P.ncell + 1) * 4);  // cstart    12
+    put((size_t)P.B * P.nscan * 4);     // tsum          13
+    put(BG * 16);                       // gst           14
+    put(BG * 8);                        // garm          15
+    put((size_t)std::max(P.G, 1) * 16); // ghost_b       16
+    put((size_t)P.B * 48);              // body          17
+    put((size_t)P.B * 12);              // u_cur         18
+    put((size_t)P.B * P.ntile * 32);    // part          19
+    put((size_t)P.B * sizeof(RolloutState));  // rs     20
+    put((size_t)P.B * sizeof(Geom));    // geom          21
+    put((size_t)std::max(P.N, 1) * 16); // xfer          22
+    put((size_t)std::max(P.N, 1) * 4);  // xrho          23
+    L.total = o;
+    return L;
+}
+
+static void bind(DevPtrs* D, const Layout& L, char* base) {
+    auto p = [&](int k) { return (void*)(base + L.off[k]); };
+    D->pos[0] = (float2*)p(0);
+    D->pos[1] = (float2*)p(1);
+    D->vel[0] = (float2*)p(2);
+    D->vel[1] = (float2*)p(3);
+    D->id[0] = (uint32_t*)p(4);
+    D->id[1] = (uint32_t*)p(5);
+    D->aux = (float2*)p(6);
+    D->skey = (uint32_t*)p(7);
+    D->key = (uint32_t*)p(8);
+    D->rank = (uint32_t*)p(9);
+    D->perm = (uint32_t*)p(10);
+    D->counts = (uint32_t*)p(11);
+    D->cstart = (uint32_t*)p(12);
+    D->tsum = (uint32_t*)p(13);
+    D->gst = (float4*)p(14);
+    D->garm = (float2*)p(15);
+    D->ghost_b = (double2*)p(16);
+    D->body = (double*)p(17);
+    D->u_cur = (float*)p(18);
+    D->part = (double4*)p(19);
+    D->rs = (RolloutState*)p(20);
+    D->geom = (Geom*)p(21);
+    D->xfer = (float4*)p(22);
+    D->xrho = (float*)p(23);
+    D->dbg_cnt = nullptr;
+    D->dbg_idx = nullptr;
+}
+
+// ---------------------------------------------------------------------------------------
+// Launch sequencing
+// ---------------------------------------------------------------------------------------
+static void launch_rebin(sph_ctx* ctx) {
+    const DevParams& P = ctx->P;
+    cudaStream_t s = ctx->stream;
+    dim3 gp(P.ntile, P.B), gs(P.nscan, P.B), gc((P.ncell + TILE - 1) / TILE, P.B);
+    k_hash<<<gp, TILE, 0, s>>>(P, ctx->D);
+    k_scan_reduce<<<gs, SCAN_T, 0, s>>>(P, ctx->D);
+    k_scan_tiles<<<P.B, SCAN_T, 0, s>>>(P, ctx->D);
+    k_scan_down<<<gs, SCAN_T, 0, s>>>(P, ctx->D);
+    k_scatter<<<gp, TILE, 0, s>>>(P, ctx->D);
+    k_cellsort<<<gc, TILE, 0, s>>>(P, ctx->D);
+    k_gather<<<gp, TILE, 0, s>>>(P, ctx->D);
+}
+
+static void launch_substep(sph_ctx* ctx, float damping, int pin) {
+    const DevParams& P = ctx->P;
+    cudaStream_t s = ctx->stream;
+    dim3 gp(P.ntile, P.B);
+    launch_rebin(ctx);
+    k_density<<<gp, TILE, 0, s>>>(P, ctx->D);
+    k_force<<<gp, TILE, 0, s>>>(P, ctx->D, damping);
+    k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, pin, ctx->ghost_angle0);
+}
+
+static const int kLaunchesPerSubstep = 10;
+
+static sph_status check_launch(sph_ctx* ctx) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ctx, SPH_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    return SPH_OK;
+}
+
+static sph_status ensure_stage(sph_ctx* ctx, size_t bytes) {
+    if (ctx->stage_bytes >= bytes) return SPH_OK;
+    if (ctx->stage) cudaFree(ctx->stage);
+    ctx->stage = nullptr;
+    ctx->stage_bytes = 0;
+    CK(cudaMalloc(&ctx->stage, bytes));
+    ctx->stage_bytes = bytes;
+    return SPH_OK;
+}
+
+static sph_status all_failed(sph_ctx* ctx) {
+    std::vector<RolloutState> rs(ctx->P.B);
+    CK(cudaMemcpyAsync(rs.data(), ctx->D.rs, sizeof(RolloutState) * ctx->P.B, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (auto& r : rs)
+        if (!r.status) return SPH_OK;
+    return fail(ctx, SPH_EBLOWUP, "every rollout has a non-zero numerical status");
+}
+
+// ---------------------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------------------
+extern "C" {
+
+size_t sph_workspace_bytes(const sph_fluid_params* fp, const sph_body_params* bp,
+                           const sph_time_params* tp, int n_fluid, int n_ghost, int n_rollouts) {
+    DevParams P;
+    std::string why;
+    if (!make_params(fp, bp, tp, n_fluid, n_ghost, n_rollouts, &P, &why)) return 0;
+    return layout(P).total;
+}
+
+sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
+                         const sph_time_params* tp, int n_fluid, const float* fluid_pv,
+                         int n_ghost, const double* ghost_body_xy, int n_rollouts,
+                         void* cuda_stream, void* d_workspace, size_t workspace_bytes,
+                         sph_ctx** out) {
+    if (!out) return fail(nullptr, SPH_EINVAL, "out is NULL");
+    *out = nullptr;
+    DevParams P;
+    std::string why;
+    if (!make_params(fp, bp, tp, n_fluid, n_ghost, n_rollouts, &P, &why))
+        return fail(nullptr, SPH_EINVAL, why);
+    if ((n_fluid > 0 && !fluid_pv) || (n_ghost > 0 && !ghost_body_xy))
+        return fail(nullptr, SPH_EINVAL, "fluid_pv / ghost_body_xy is NULL");
+    const Layout L = layout(P);
+    if (!d_workspace || workspace_bytes < L.total)
+        return fail(nullptr, SPH_ENOMEM, "workspace too small: need " + std::to_string(L.total) + " bytes");
+    if (((uintptr_t)d_workspace) & 255) return fail(nullptr, SPH_EINVAL, "workspace must be 256-byte aligned");
+    for (int i = 0; i < 4 * n_fluid; ++i)
+        if (!std::isfinite(fluid_pv[i])) return fail(nullptr, SPH_EINVAL, "non-finite fluid state");
+    // the ghost-ring lookup needs ghosts uniformly spaced on the wall circle, angular order
+    const double R = bp->tank_radius;
+    double a0 = 0.0;
+    if (n_ghost > 0) {
+        a0 = std::atan2(ghost_body_xy[1], ghost_body_xy[0]);
+        for (int g = 0; g < n_ghost; ++g) {
+            const double a = a0 + 2.0 * M_PI * g / n_ghost;
+            const double ex = R * std::cos(a) - ghost_body_xy[2 * g];
+            const double ey = R * std::sin(a) - ghost_body_xy[2 * g + 1];
+            if (std::sqrt(ex * ex + ey * ey) > 1e-6 * R)
+                return fail(nullptr, SPH_EINVAL, "ghosts must lie uniformly spaced on the tank wall circle (radius tank_radius) in counter-clockwise order");
+        }
+    }
+    sph_ctx* ctx = new sph_ctx();
+    ctx->P = P;
+    ctx->n_sub = tp->substeps_per_sample;
+    ctx->ghost_angle0 = (float)a0;
+    bind(&ctx->D, L, (char*)d_workspace);
+    if (cuda_stream) {
+        ctx->stream = (cudaStream_t)cuda_stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete ctx;
+            return fail(nullptr, SPH_ECUDA, "cudaStreamCreate failed");
+        }
+        ctx->own_stream = true;
+    }
+    cudaStream_t s = ctx->stream;
+    auto bail = [&](const char* what, cudaError_t e) {
+        g_init_err = std::string(what) + ": " + cudaGetErrorString(e);
+        sph_destroy(ctx);
+        return SPH_ECUDA;
+    };
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(d_workspace, 0, L.total, s)) != cudaSuccess) return bail("memset", e);
+    std::vector<double2> gb(std::max(n_ghost, 1));
+    for (int g = 0; g < n_ghost; ++g) gb[g] = make_double2(ghost_body_xy[2 * g], ghost_body_xy[2 * g + 1]);
+    if (n_ghost > 0 && (e = cudaMemcpyAsync(ctx->D.ghost_b, gb.data(), sizeof(double2) * n_ghost, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return bail("ghost copy", e);
+    if (n_fluid > 0) {
+        if ((e = cudaMemcpyAsync(ctx->D.xfer, fluid_pv, sizeof(float4) * n_fluid, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+            return bail("state copy", e);
+        k_import<<<dim3((n_fluid + 255) / 256, P.B), 256, 0, s>>>(P, ctx->D, 0, ctx->D.xfer);
+    }
+    k_reset_rollout<<<P.B, BODY_T, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
+    if ((e = cudaGetLastError()) != cudaSuccess) return bail("init kernels", e);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail("init sync", e);
+    *out = ctx;
+    return SPH_OK;
+}
+
+sph_status sph_set_state(sph_ctx* ctx, int rollout, const float* fluid_pv, const double* body) {
+    if (!ctx) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    if (rollout < -1 || rollout >= P.B) return fail(ctx, SPH_EINVAL, "rollout out of range");
+    if (P.N > 0 && !fluid_pv) return fail(ctx, SPH_EINVAL, "fluid_pv is NULL");
+    for (int i = 0; i < 4 * P.N; ++i)
+        if (!std::isfinite(fluid_pv[i])) return fail(ctx, SPH_EINVAL, "non-finite fluid state");
+    const int b0 = rollout < 0 ? 0 : rollout, nb = rollout < 0 ? P.B : 1;
+    cudaStream_t s = ctx->stream;
+    if (P.N > 0) {
+        CK(cudaMemcpyAsync(ctx->D.xfer, fluid_pv, sizeof(float4) * P.N, cudaMemcpyHostToDevice, s));
+        k_import<<<dim3((P.N + 255) / 256, nb), 256, 0, s>>>(P, ctx->D, b0, ctx->D.xfer);
+    }
+    if (body) {
+        for (int b = b0; b < b0 + nb; ++b)
+            CK(cudaMemcpyAsync(ctx->D.body + (size_t)b * 6, body, 48, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaMemsetAsync(ctx->D.counts + (size_t)b0 * P.ncell, 0, sizeof(uint32_t) * P.ncell * nb, s));
+    k_reset_rollout<<<nb, BODY_T, 0, s>>>(P, ctx->D, b0, ctx->ghost_angle0);
+    sph_status st = check_launch(ctx);
+    if (st) return st;
+    CK(cudaStreamSynchronize(s));
+    return SPH_OK;
+}
+
+sph_status sph_set_body_state(sph_ctx* ctx, const double* body) {
+    if (!ctx || !body) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    for (int i = 0; i < 6 * P.B; ++i)
+        if (!std::isfinite(body[i])) return fail(ctx, SPH_EINVAL, "non-finite body state");
+    CK(cudaMemcpyAsync(ctx->D.body, body, 48 * (size_t)P.B, cudaMemcpyHostToDevice, ctx->stream));
+    // keep status / parity, refresh ghosts and the float pose
+    k_reset_rollout<<<P.B, BODY_T, 0, ctx->stream>>>(P, ctx->D, 0, ctx->ghost_angle0);
+    sph_status st = check_launch(ctx);
+    if (st) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SPH_OK;
+}
+
+sph_status sph_get_particles(sph_ctx* ctx, int rollout, float* fluid_pv, float* rho) {
+    if (!ctx || !fluid_pv) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    if (rollout < 0 || rollout >= P.B) return fail(ctx, SPH_EINVAL, "rollout out of range");
+    if (P.N == 0) return SPH_OK;
+    cudaStream_t s = ctx->stream;
+    k_export<<<(P.N + 255) / 256, 256, 0, s>>>(P, ctx->D, rollout, ctx->D.xfer, ctx->D.xrho);
+    sph_status st = check_launch(ctx);
+    if (st) return st;
+    CK(cudaMemcpyAsync(fluid_pv, ctx->D.xfer, sizeof(float4) * P.N, cudaMemcpyDeviceToHost, s));
+    if (rho) CK(cudaMemcpyAsync(rho, ctx->D.xrho, sizeof(float) * P.N, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return SPH_OK;
+}
+
+sph_status sph_get_ghosts(sph_ctx* ctx, int rollout, float* ghost_pv) {
+    if (!ctx || !ghost_pv) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    if (rollout < 0 || rollout >= P.B) return fail(ctx, SPH_EINVAL, "rollout out of range");
+    if (P.G == 0) return SPH_OK;
+    CK(cudaMemcpyAsync(ghost_pv, ctx->D.gst + (size_t)rollout * P.G, sizeof(float4) * P.G, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SPH_OK;
+}
+
+sph_status sph_step(sph_ctx* ctx, const float* u, int n_substeps, int ptr_on_device) {
+    if (!ctx || !u || n_substeps < 0) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    cudaStream_t s = ctx->stream;
+    const size_t ub = sizeof(float) * 3 * P.B;
+    if (!ptr_on_device)
+        for (int i = 0; i < 3 * P.B; ++i)
+            if (!std::isfinite(u[i])) return fail(ctx, SPH_EINVAL, "non-finite input u");
+    CK(cudaMemcpyAsync(ctx->D.u_cur, u, ub, ptr_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    for (int k = 0; k < n_substeps; ++k) launch_substep(ctx, 1.0f, 0);
+    sph_status st = check_launch(ctx);
+    if (st) return st;
+    if (!ptr_on_device) CK(cudaStreamSynchronize(s));
+    return SPH_OK;
+}
+
+static sph_status capture_tick_graph(sph_ctx* ctx) {
+    if (ctx->tick_graph) return SPH_OK;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < ctx->n_sub; ++k) launch_substep(ctx, 1.0f, 0);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    if (e != cudaSuccess) return fail(ctx, SPH_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&ctx->tick_graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        ctx->tick_graph = nullptr;
+        return fail(ctx, SPH_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+    return SPH_OK;
+}
+
+sph_status sph_rollout_batch(sph_ctx* ctx, const float* u_seq, int K, const sph_pd_attitude* pd,
+                             float* y_out, float* u_applied, int ptr_on_device) {
+    if (!ctx || !u_seq || !y_out || K < 0) return SPH_EINVAL;
+    if (pd && !pd->theta_ref) return fail(ctx, SPH_EINVAL, "pd->theta_ref is NULL");
+    const DevParams& P = ctx->P;
+    if (K == 0) return SPH_OK;
+    cudaStream_t s = ctx->stream;
+    const size_t nu = (size_t)P.B * K * 3, ny = (size_t)P.B * K * 6, nt = (size_t)P.B * K;
+    const float *du = u_seq, *dth = pd ? pd->theta_ref : nullptr;
+    float *dy = y_out, *dua = u_applied;
+    if (!ptr_on_device) {   // stage host buffers through ctx-owned device memory
+        for (size_t i = 0; i < nu; ++i)
+            if (!std::isfinite(u_seq[i])) return fail(ctx, SPH_EINVAL, "non-finite input u");
+        const size_t bytes = sizeof(float) * (nu + ny + nu + (pd ? nt : 0));
+        sph_status st = ensure_stage(ctx, bytes);
+        if (st) return st;
+        float* base = (float*)ctx->stage;
+        float* su = base;
+        dy = base + nu;
+        dua = u_applied ? base + nu + ny : nullptr;
+        float* sth = base + nu + ny + nu;
+        CK(cudaMemcpyAsync(su, u_seq, sizeof(float) * nu, cudaMemcpyHostToDevice, s));
+        if (pd) CK(cudaMemcpyAsync(sth, pd->theta_ref, sizeof(float) * nt, cudaMemcpyHostToDevice, s));
+        du = su;
+        dth = pd ? sth : nullptr;
+    }
+    sph_status st = capture_tick_graph(ctx);
+    if (st) return st;
+    const int tb = 128, tg = (P.B + tb - 1) / tb;
+    for (int k = 0; k < K; ++k) {
+        k_tick<<<tg, tb, 0, s>>>(P, ctx->D, du, dth, dy, dua, K, k, pd ? 1 : 0, pd ? pd->Kp : 0.0, pd ? pd->Kd : 0.0);
+        CK(cudaGraphLaunch(ctx->tick_graph, s));
+    }
+    st = check_launch(ctx);
+    if (st) return st;
+    if (!ptr_on_device) {
+        CK(cudaMemcpyAsync(y_out, dy, sizeof(float) * ny, cudaMemcpyDeviceToHost, s));
+        if (u_applied) CK(cudaMemcpyAsync(u_applied, dua, sizeof(float) * nu, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return all_failed(ctx);
+    }
+    return SPH_OK;
+}
+
+sph_status sph_get_body_state(sph_ctx* ctx, double* out) {
+    if (!ctx || !out) return SPH_EINVAL;
+    CK(cudaMemcpyAsync(out, ctx->D.body, 48 * (size_t)ctx->P.B, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SPH_OK;
+}
+
+sph_status sph_settle(sph_ctx* ctx, double damping, int n_steps) {
+    if (!ctx || n_steps < 0 || !(damping > 0 && damping <= 1)) return SPH_EINVAL;
+    CK(cudaMemsetAsync(ctx->D.u_cur, 0, sizeof(float) * 3 * ctx->P.B, ctx->stream));
+    for (int k = 0; k < n_steps; ++k) launch_substep(ctx, (float)damping, 1);
+    sph_status st = check_launch(ctx);
+    if (st) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SPH_OK;
+}
+
+sph_status sph_get_status(sph_ctx* ctx, int32_t* rollout_status, int64_t* bad_step,
+                          int32_t* bad_particle) {
+    if (!ctx || !rollout_status) return SPH_EINVAL;
+    std::vector<RolloutState> rs(ctx->P.B);
+    CK(cudaMemcpyAsync(rs.data(), ctx->D.rs, sizeof(RolloutState) * ctx->P.B, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int b = 0; b < ctx->P.B; ++b) {
+        rollout_status[b] = rs[b].status;
+        if (bad_step) bad_step[b] = rs[b].bad_step;
+        if (bad_particle) bad_particle[b] = rs[b].bad_particle;
+    }
+    return SPH_OK;
+}
+
+sph_status sph_debug_cells(sph_ctx* ctx, int rollout, int32_t* cells, float* grid) {
+    if (!ctx || !cells) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    if (rollout < 0 || rollout >= P.B) return fail(ctx, SPH_EINVAL, "rollout out of range");
+    sph_status st = ensure_stage(ctx, sizeof(int) * 2 * std::max(P.N, 1));
+    if (st) return st;
+    k_debug_cells<<<(P.N + 255) / 256, 256, 0, ctx->stream>>>(P, ctx->D, rollout, (int*)ctx->stage);
+    if ((st = check_launch(ctx))) return st;
+    CK(cudaMemcpyAsync(cells, ctx->stage, sizeof(int) * 2 * P.N, cudaMemcpyDeviceToHost, ctx->stream));
+    Geom gm;
+    CK(cudaMemcpyAsync(&gm, ctx->D.geom + rollout, sizeof(Geom), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (grid) {
+        volatile float rx = gm.rx, ry = gm.ry, hf = P.half;
+        grid[0] = rx - hf;
+        grid[1] = ry - hf;
+        grid[2] = P.inv_C;
+        grid[3] = P.C;
+    }
+    return SPH_OK;
+}
+
+__global__ void k_force_rebin(RolloutState* rs, int b) { rs[b].need_rebin = 1; }
+
+sph_status sph_debug_neighbours(sph_ctx* ctx, int rollout, int64_t* nf_off, int32_t* nf_idx,
+                                int64_t nf_cap, int64_t* g2_off, int32_t* g2_idx,
+                                int64_t g2_cap, int64_t* g1_off, int32_t* g1_idx,
+                                int64_t g1_cap) {
+    if (!ctx || !nf_off || !g2_off || !g1_off) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    if (rollout < 0 || rollout >= P.B) return fail(ctx, SPH_EINVAL, "rollout out of range");
+    cudaStream_t s = ctx->stream;
+    if (!ctx->dbg_buf) CK(cudaMalloc(&ctx->dbg_buf, sizeof(int) * 3 * (size_t)std::max(P.N, 1) * (DBG_CAP + 1)));
+    DevPtrs D = ctx->D;
+    D.dbg_cnt = ctx->dbg_buf;
+    D.dbg_idx = ctx->dbg_buf + 3 * (size_t)std::max(P.N, 1);
+    // rebuild the cell list of the current state into the other buffer (state untouched)
+    k_force_rebin<<<1, 1, 0, s>>>(ctx->D.rs, rollout);
+    launch_rebin(ctx);
+    if (P.N > 0) k_debug_neighbours<<<(P.N + 255) / 256, 256, 0, s>>>(P, D, rollout);
+    sph_status st = check_launch(ctx);
+    if (st) return st;
+    std::vector<int> cnt(3 * (size_t)P.N), idx(3 * (size_t)P.N * DBG_CAP);
+    if (P.N > 0) {
+        CK(cudaMemcpyAsync(cnt.data(), D.dbg_cnt, sizeof(int) * cnt.size(), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(idx.data(), D.dbg_idx, sizeof(int) * idx.size(), cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    int64_t* offs[3] = {nf_off, g2_off, g1_off};
+    int32_t* outs[3] = {nf_idx, g2_idx, g1_idx};
+    int64_t caps[3] = {nf_cap, g2_cap, g1_cap};
+    for (int t = 0; t < 3; ++t) {
+        int64_t tot = 0;
+        offs[t][0] = 0;
+        for (int i = 0; i < P.N; ++i) {
+            const int n = cnt[(size_t)t * P.N + i];
+            if (n > DBG_CAP) return fail(ctx, SPH_ENOMEM, "more than DBG_CAP neighbours");
+            if (tot + n > caps[t]) return fail(ctx, SPH_ENOMEM, "neighbour cap too small");
+            int* row = idx.data() + ((size_t)t * P.N + i) * DBG_CAP;
+            std::sort(row, row + n);
+            for (int q = 0; q < n; ++q) outs[t][tot + q] = row[q];
+            tot += n;
+            offs[t][i + 1] = tot;
+        }
+    }
+    return SPH_OK;
+}
+
+sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
+    if (!ctx || !ms || n_substeps < 1) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    cudaStream_t s = ctx->stream;
+    cudaEvent_t ev[10];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    double acc[SPH_NUM_TIMERS] = {0};
+    dim3 gp(P.ntile, P.B), gs(P.nscan, P.B), gc((P.ncell + TILE - 1) / TILE, P.B);
+    for (int it = 0; it < n_substeps; ++it) {
+        cudaEventRecord(ev[0], s);
+        k_hash<<<gp, TILE, 0, s>>>(P, ctx->D);
+        cudaEventRecord(ev[1], s);
+        k_scan_reduce<<<gs, SCAN_T, 0, s>>>(P, ctx->D);
+        k_scan_tiles<<<P.B, SCAN_T, 0, s>>>(P, ctx->D);
+        k_scan_down<<<gs, SCAN_T, 0, s>>>(P, ctx->D);
+        cudaEventRecord(ev[2], s);
+        k_scatter<<<gp, TILE, 0, s>>>(P, ctx->D);
+        cudaEventRecord(ev[3], s);
+        k_cellsort<<<gc, TILE, 0, s>>>(P, ctx->D);
+        cudaEventRecord(ev[4], s);
+        k_gather<<<gp, TILE, 0, s>>>(P, ctx->D);
+        cudaEventRecord(ev[5], s);
+        k_density<<<gp, TILE, 0, s>>>(P, ctx->D);
+        cudaEventRecord(ev[6], s);
+        k_force<<<gp, TILE, 0, s>>>(P, ctx->D, 1.0f);
+        cudaEventRecord(ev[7], s);
+        k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
+        cudaEventRecord(ev[8], s);
+        sph_status st = check_launch(ctx);
+        if (st) return st;
+        CK(cudaEventSynchronize(ev[8]));
+        for (int t = 0; t < 8; ++t) {
+            float m;
+            CK(cudaEventElapsedTime(&m, ev[t], ev[t + 1]));
+            acc[t] += m;
+        }
+        float m;
+        CK(cudaEventElapsedTime(&m, ev[0], ev[8]));
+        acc[SPH_TIMER_SUBSTEP] += m;
+    }
+    for (int t = 0; t < SPH_NUM_TIMERS; ++t) ms[t] = (float)(acc[t] / n_substeps);
+    for (auto& e : ev) cudaEventDestroy(e);
+    return SPH_OK;
+}
+
+int sph_launches_per_substep(const sph_ctx* ctx) { return ctx ? kLaunchesPerSubstep : 0; }
+
+void sph_get_sizes(const sph_ctx* ctx, int* n_fluid, int* n_ghost, int* n_rollouts, int* n_cells) {
+    if (!ctx) return;
+    if (n_fluid) *n_fluid = ctx->P.N;
+    if (n_ghost) *n_ghost = ctx->P.G;
+    if (n_rollouts) *n_rollouts = ctx->P.B;
+    if (n_cells) *n_cells = ctx->P.ncell;
+}
+
+const char* sph_last_error(const sph_ctx* ctx) { return ctx ? ctx->err.c_str() : g_init_err.c_str(); }
+
+void sph_destroy(sph_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->tick_graph) cudaGraphExecDestroy(ctx->tick_graph);
+    if (ctx->stage) cudaFree(ctx->stage);
+    if (ctx->dbg_buf) cudaFree(ctx->dbg_buf);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+}  // extern "C"

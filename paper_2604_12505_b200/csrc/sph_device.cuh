@@ -1,0 +1,168 @@
+// sph_device.cuh -- device-side data layout, parameters and the hot-path kernels of the
+// B200-native SPH fuel-sloshing step (sm_100a).  P:n = line n of the paper text.
+//
+// One substep of one rollout is (Algorithm 1, + symplectic Euler):
+//   [rebin]   k_hash -> k_scan_reduce -> k_scan_tiles -> k_scan_down -> k_scatter
+//             -> k_cellsort -> k_gather          (cell list by counting sort, row-major cells)
+//   k_density  Eq. density_update + Eq. EOS
+//   k_force    Eqs. momentum, viscous, pressure_b2f / viscous_b2f,
+//              Alg. 1 l.8, kick-then-drift of the fluid, per-CTA body partials
+//   k_body     Eq. tankdynamics fixed-order fp64 reduction, body kick-drift,
+//              Eq. kinematicghost for the next substep, status, rebin policy
+// Every rollout owns whole CTAs (blockIdx.y = rollout), so results never depend on the batch.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sph {
+
+constexpr int TILE = 256;        // particles (threads) per CTA in the particle kernels
+constexpr int SCAN_T = 256;      // threads per scan CTA
+constexpr int SCAN_V = 8;        // counts per scan thread
+constexpr int SCAN_TILE = SCAN_T * SCAN_V;
+constexpr int BODY_T = 128;      // threads of the per-rollout body kernel
+constexpr int SORT_LOCAL = 16;   // cells up to this size are sorted in registers
+
+struct DevParams {
+    int N, G, B;            // fluid particles / ghosts per rollout, rollouts
+    int nx, ncell;          // square cell grid: nx * nx cells per rollout
+    int ntile, nscan;       // CTAs per rollout (particle kernels, scan kernels)
+    int ghost_K, ghost_full;
+    float C, inv_C, half;   // cell side (2h [+ skin]), 1/C, half extent of the grid
+    float h, inv_h, H2, h2; // h, 1/h, (2h)^2, h^2 in float32 (predicates, reading A19)
+    float mass, m2, rho0, k, gamma1;
+    float alpha2h, beta, eps_h2;
+    float wcb, dwcb, dws3;  // C/h^2, C/h^3, -30/(pi h^5)
+    float gsign2m2;         // ghost_pressure_sign * 2 m^2
+    float gx, gy, dt;
+    float wall_r2;          // particles with |x - r|^2 <= wall_r2 see no ghost within 2h
+    float ghost_scale;      // G / (2 pi)
+    float skin_half;
+    int rebin_every;
+    double dtd, m_body, J_body;
+};
+
+struct RolloutState {
+    int sp;              // particle state buffer parity
+    int ip;              // id buffer parity
+    int need_rebin;      // rebuild the cell list at the start of the next substep
+    int status;          // 0 ok, 1 non-finite, 2 |x| > 1e9, 3 left the grid (sticky)
+    int frozen;          // set by k_body at the end of the substep in which status became
+                         // non-zero; kernels skip frozen rollouts (the failing substep is
+                         // committed whole, so the exported state stays consistent)
+    long long step;      // substeps taken
+    long long bad_step;
+    int bad_particle;
+    float disp;          // displacement bound since the last rebuild (adaptive mode)
+};
+
+struct Geom {            // float copy of the body pose used by the particle kernels
+    float rx, ry, th;    // th = theta + angle of ghost 0 (ghost-ring lookup)
+    float pad;
+};
+
+struct DevPtrs {
+    float2* pos[2];      // [B][N] sorted-by-cell particle positions (double buffered)
+    float2* vel[2];      // [B][N] velocities
+    uint32_t* id[2];     // [B][N] canonical id of each slot
+    float2* aux;         // [B][N] (rho, P / rho^2)
+    uint32_t* skey;      // [B][N] cell of each slot at the last rebuild
+    uint32_t* key;       // [B][N] rebin scratch: cell of each (unsorted) slot
+    uint32_t* rank;      // [B][N] rebin scratch: rank inside the cell
+    uint32_t* perm;      // [B][N] rebin scratch: new slot -> old slot
+    uint32_t* counts;    // [B][ncell] cell populations (kept zero between rebuilds)
+    uint32_t* cstart;    // [B][ncell + 1] exclusive prefix of counts (cell start table)
+    uint32_t* tsum;      // [B][nscan] scan tile sums
+    float4* gst;         // [B][G] ghost world state (x, y, vx, vy)
+    float2* garm;        // [B][G] ghost arm r_g - r (world frame)
+    double2* ghost_b;    // [G] body-frame ghost positions
+    double* body;        // [B][6] r_x r_y theta rd_x rd_y thd
+    float* u_cur;        // [B][3] current ZOH input
+    double4* part;       // [B][ntile] per-CTA (F_x, F_y, T, vmax) partials
+    RolloutState* rs;    // [B]
+    Geom* geom;          // [B]
+    float4* xfer;        // [N] canonical-order export / import staging
+    float* xrho;         // [N]
+    int* dbg_cnt;        // [3][N] debug neighbour counts
+    int* dbg_idx;        // [3][N][DBG_CAP] debug neighbour ids
+};
+
+constexpr int DBG_CAP = 64;
+
+// ---------------------------------------------------------------------------------------
+// Small device helpers
+// ---------------------------------------------------------------------------------------
+// Canonical float32 cell coordinate (reading A19): floor((x - o) * inv), IEEE RN, no FMA.
+__device__ __forceinline__ int cell_coord(float x, float o, float inv) {
+    return __float2int_rd(__fmul_rn(__fsub_rn(x, o), inv));
+}
+
+// Canonical float32 squared distance (reading A19): dx*dx + dy*dy, no contraction.
+__device__ __forceinline__ float dist2(float dx, float dy) {
+    return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+}
+
+// Cubic spline (Eq. cubicspline) without its constant C/h^2; q = r/h < 2.
+__device__ __forceinline__ float wcb_poly(float q) {
+    float a = 2.0f - q, b = 1.0f - q;
+    float w = a * a * a;
+    if (q < 1.0f) w -= 4.0f * b * b * b;
+    return w;
+}
+
+// dW/dq of the cubic spline without C/h^3.
+__device__ __forceinline__ float dwcb_poly(float q) {
+    float a = 2.0f - q, b = 1.0f - q;
+    float d = -3.0f * a * a;
+    if (q < 1.0f) d += 12.0f * b * b;
+    return d;
+}
+
+__device__ __forceinline__ void set_status(RolloutState* rs, int code, int particle) {
+    if (atomicCAS(&rs->status, 0, code) == 0) {
+        rs->bad_step = rs->step;
+        rs->bad_particle = particle;
+    }
+}
+
+// Enumerate the fluid candidates of a particle whose (rebuild-time) cell is c: the three cell
+// rows cy-1..cy+1, each a contiguous slot range [start(cx-1), start(cx+2)) because cells are
+// numbered row-major and slots are sorted by cell.
+template <class F>
+__device__ __forceinline__ void for_fluid_candidates(const DevParams& P, const uint32_t* cs,
+                                                     uint32_t c, F&& f) {
+    int cy = (int)c / P.nx;
+    int cx = (int)c - cy * P.nx;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+        int c0 = (cy + dy) * P.nx + cx - 1;
+        uint32_t j0 = __ldg(cs + c0), j1 = __ldg(cs + c0 + 3);
+        for (uint32_t j = j0; j < j1; ++j) f(j);
+    }
+}
+
+// Enumerate the candidate ghosts of a particle (ghost-ring lookup).  The ghosts sit uniformly
+// on the wall circle, so those within 2h of x lie in an angular window around
+// the particle's polar angle; the window half-width ghost_K is derived on the host from
+// |x - g|^2 >= 4 d R sin^2(dphi / 2) with d >= sqrt(wall_r2).  Exact predicates follow.
+template <class F>
+__device__ __forceinline__ void for_ghost_candidates(const DevParams& P, const Geom& gm,
+                                                     float2 x, F&& f) {
+    float rx = x.x - gm.rx, ry = x.y - gm.ry;
+    if (rx * rx + ry * ry <= P.wall_r2) return;
+    if (P.ghost_full) {
+        for (int g = 0; g < P.G; ++g) f(g);
+        return;
+    }
+    float phi = atan2f(ry, rx) - gm.th;
+    int j0 = __float2int_rn(phi * P.ghost_scale) % P.G;
+    if (j0 < 0) j0 += P.G;
+    int g = j0 - P.ghost_K;
+    if (g < 0) g += P.G;
+    for (int t = 0; t < 2 * P.ghost_K + 1; ++t) {
+        f(g);
+        if (++g == P.G) g = 0;
+    }
+}
+
+}  // namespace sph

@@ -1,0 +1,556 @@
+// sph_kernels.cuh -- the sm_100a kernels of one substep (see sph_device.cuh for the pipeline).
+// Included once by sph_api.cu.  P:n = line n of the paper text.
+#pragma once
+#include "sph_device.cuh"
+
+namespace sph {
+
+// ---------------------------------------------------------------------------------------
+// Rebin 1/7: cell key + rank inside the cell (north star: "cell-hash build").
+// Grid origin o = float(r_body) - half (reading A19), cells row-major.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TILE) k_hash(DevParams P, DevPtrs D) {
+    const int b = blockIdx.y;
+    RolloutState* rs = D.rs + b;
+    if (rs->frozen || !rs->need_rebin) return;
+    const int i = blockIdx.x * TILE + threadIdx.x;
+    if (i >= P.N) return;
+    const size_t o = (size_t)b * P.N;
+    const float2 x = D.pos[rs->sp][o + i];
+    const Geom gm = D.geom[b];
+    const float ox = __fsub_rn(gm.rx, P.half), oy = __fsub_rn(gm.ry, P.half);
+    int cx = cell_coord(x.x, ox, P.inv_C), cy = cell_coord(x.y, oy, P.inv_C);
+    if (cx < 1 || cx > P.nx - 2 || cy < 1 || cy > P.nx - 2) {   // tunnelled out of the tank
+        set_status(rs, 3, (int)D.id[rs->ip][o + i]);
+        cx = min(max(cx, 1), P.nx - 2);
+        cy = min(max(cy, 1), P.nx - 2);
+    }
+    const uint32_t c = (uint32_t)(cy * P.nx + cx);
+    D.key[o + i] = c;
+    D.rank[o + i] = atomicAdd(D.counts + (size_t)b * P.ncell + c, 1u);
+}
+
+// ---------------------------------------------------------------------------------------
+// Rebin 2-4/7: segmented exclusive scan of the cell counts of each rollout
+//   cstart[b][c] = sum_{c' < c} counts[b][c'],  c = 0..ncell  (cstart[b][ncell] = N).
+// Three phases (tile sums, scan of tile sums, down-sweep); the down-sweep re-zeroes counts.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total) {
+    __shared__ uint32_t warp_tot[SCAN_T / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t t = lane < SCAN_T / 32 ? warp_tot[lane] : 0u;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, t, d);
+            if (lane >= d) t += y;
+        }
+        if (lane < SCAN_T / 32) warp_tot[lane] = t;   // inclusive warp prefix
+    }
+    __syncthreads();
+    uint32_t base = w ? warp_tot[w - 1] : 0u;
+    if (total) *total = warp_tot[SCAN_T / 32 - 1];
+    return base + x - v;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_reduce(DevParams P, DevPtrs D) {
+    const int b = blockIdx.y;
+    if (D.rs[b].frozen || !D.rs[b].need_rebin) return;
+    const uint32_t* cnt = D.counts + (size_t)b * P.ncell;
+    const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_V;
+    uint32_t s = 0;
+#pragma unroll
+    for (int v = 0; v < SCAN_V; ++v) {
+        int c = base + v;
+        if (c < P.ncell) s += cnt[c];
+    }
+    uint32_t tot;
+    block_excl_scan(s, &tot);
+    if (threadIdx.x == 0) D.tsum[(size_t)b * P.nscan + blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(DevParams P, DevPtrs D) {
+    const int b = blockIdx.x;
+    if (D.rs[b].frozen || !D.rs[b].need_rebin) return;
+    uint32_t* ts = D.tsum + (size_t)b * P.nscan;
+    const int per = (P.nscan + SCAN_T - 1) / SCAN_T;   // host guarantees per <= SCAN_V
+    uint32_t v[SCAN_V];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_V; ++k) {
+        int t = threadIdx.x * per + k;
+        v[k] = (k < per && t < P.nscan) ? ts[t] : 0u;
+        s += v[k];
+    }
+    uint32_t run = block_excl_scan(s, nullptr);
+#pragma unroll
+    for (int k = 0; k < SCAN_V; ++k) {
+        int t = threadIdx.x * per + k;
+        if (k < per && t < P.nscan) ts[t] = run;
+        run += v[k];
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_down(DevParams P, DevPtrs D) {
+    const int b = blockIdx.y;
+    if (D.rs[b].frozen || !D.rs[b].need_rebin) return;
+    uint32_t* cnt = D.counts + (size_t)b * P.ncell;
+    uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
+    const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_V;
+    uint32_t v[SCAN_V];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_V; ++k) {
+        int c = base + k;
+        v[k] = c < P.ncell ? cnt[c] : 0u;
+        s += v[k];
+    }
+    uint32_t run = block_excl_scan(s, nullptr) + D.tsum[(size_t)b * P.nscan + blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < SCAN_V; ++k) {
+        int c = base + k;
+        if (c <= P.ncell) cs[c] = run;
+        if (c < P.ncell) cnt[c] = 0u;          // counts stay zero between rebuilds
+        run += v[k];
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Rebin 5/7: scatter old slot -> new slot (cell start + rank).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TILE) k_scatter(DevParams P, DevPtrs D) {
+    const int b = blockIdx.y;
+    if (D.rs[b].frozen || !D.rs[b].need_rebin) return;
+    const int i = blockIdx.x * TILE + threadIdx.x;
+    if (i >= P.N) return;
+    const size_t o = (size_t)b * P.N;
+    const uint32_t c = D.key[o + i];
+    D.perm[o + D.cstart[(size_t)b * (P.ncell + 1) + c] + D.rank[o + i]] = (uint32_t)i;
+}
+
+// ---------------------------------------------------------------------------------------
+// Rebin 6/7: make the order inside every cell ascending in canonical id (the atomic ranks are
+// not deterministic; this makes the whole sort deterministic and history independent,
+// reading A20).  One thread per cell.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TILE) k_cellsort(DevParams P, DevPtrs D) {
+    const int b = blockIdx.y;
+    const RolloutState* rs = D.rs + b;
+    if (rs->frozen || !rs->need_rebin) return;
+    const int c = blockIdx.x * TILE + threadIdx.x;
+    if (c >= P.ncell) return;
+    const uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
+    const uint32_t s = cs[c], e = cs[c + 1];
+    const int n = (int)(e - s);
+    if (n <= 1) return;
+    const size_t o = (size_t)b * P.N;
+    uint32_t* pm = D.perm + o + s;
+    const uint32_t* id = D.id[rs->ip] + o;
+    if (n <= SORT_LOCAL) {
+        uint32_t src[SORT_LOCAL], key[SORT_LOCAL];
+        for (int t = 0; t < n; ++t) {
+            src[t] = pm[t];
+            key[t] = id[src[t]];
+        }
+        for (int t = 1; t < n; ++t) {
+            uint32_t ks = key[t], ss = src[t];
+            int u = t - 1;
+            while (u >= 0 && key[u] > ks) {
+                key[u + 1] = key[u];
+                src[u + 1] = src[u];
+                --u;
+            }
+            key[u + 1] = ks;
+            src[u + 1] = ss;
+        }
+        for (int t = 0; t < n; ++t) pm[t] = src[t];
+    } else {   // crowded cell (compressed flow): in-place insertion sort in global memory
+        for (int t = 1; t < n; ++t) {
+            uint32_t ss = pm[t], ks = id[ss];
+            int u = t - 1;
+            while (u >= 0 && id[pm[u]] > ks) {
+                pm[u + 1] = pm[u];
+                --u;
+            }
+            pm[u + 1] = ss;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Rebin 7/7: gather the state into cell order (coalesced writes; reads are nearly sequential
+// because particles move little between rebuilds).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) {
+    const int b = blockIdx.y;
+    const RolloutState* rs = D.rs + b;
+    if (rs->frozen || !rs->need_rebin) return;
+    const int d = blockIdx.x * TILE + threadIdx.x;
+    if (d >= P.N) return;
+    const size_t o = (size_t)b * P.N;
+    const int sp = rs->sp, ip = rs->ip;
+    const uint32_t src = D.perm[o + d];
+    D.pos[sp ^ 1][o + d] = D.pos[sp][o + src];
+    D.vel[sp ^ 1][o + d] = D.vel[sp][o + src];
+    D.id[ip ^ 1][o + d] = D.id[ip][o + src];
+    D.skey[o + d] = D.key[o + src];
+}
+
+// ---------------------------------------------------------------------------------------
+// Density + EOS (Eq. density_update, Eq. EOS, cubic kernel P:268-271):
+//   rho_i = m ( sum_{j : r_ij < 2h} W_cb(r_ij)  [self included]  + gamma1 sum_g W_cb(r_ig) )
+//   P_i = k (rho_i - rho0);  stores (rho_i, P_i / rho_i^2).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D) {
+    const int b = blockIdx.y;
+    const RolloutState* rs = D.rs + b;
+    if (rs->frozen) return;
+    const int i = blockIdx.x * TILE + threadIdx.x;
+    if (i >= P.N) return;
+    const size_t o = (size_t)b * P.N;
+    const float2* __restrict__ pos = D.pos[rs->sp ^ rs->need_rebin] + o;
+    const uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
+    const float2 xi = pos[i];
+    float wf = 0.0f;
+    for_fluid_candidates(P, cs, D.skey[o + i], [&](uint32_t j) {
+        const float2 xj = __ldg(pos + j);
+        const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+        if (r2 < P.H2) wf += wcb_poly(sqrtf(r2) * P.inv_h);
+    });
+    float wg = 0.0f;
+    const Geom gm = D.geom[b];
+    const float4* gst = D.gst + (size_t)b * P.G;
+    for_ghost_candidates(P, gm, xi, [&](int g) {
+        const float4 xg = __ldg(gst + g);
+        const float r2 = dist2(__fsub_rn(xi.x, xg.x), __fsub_rn(xi.y, xg.y));
+        if (r2 < P.H2) wg += wcb_poly(sqrtf(r2) * P.inv_h);
+    });
+    const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
+    const float pr = P.k * (rho - P.rho0);
+    D.aux[o + i] = make_float2(rho, pr / (rho * rho));
+}
+
+// ---------------------------------------------------------------------------------------
+// Forces + wall + fluid integration + body partials.
+//   F^p_i = m sum m (P_i/rho_i^2 + P_j/rho_j^2) grad W_ij            (Eq. momentum)
+//   F^v_i = m sum m 2 alpha h/(rho_i+rho_j) (v_ij.r_ij)/(r^2 + eps h^2) grad W_ij
+//   G_ig  = s 2 m^2 (P_i/rho_i^2) grad W_s3 + m^2 beta/rho_i min(v.r,0)/(r^2+eps h^2) grad W_s3
+//           (Eqs. pressure_b2f, viscous_b2f P:188-200; s = ghost_pressure_sign, reading A4)
+//   a_i = (-F^p + F^v + sum_g G_ig) / m + g        (Algorithm 1 l.8)
+//   v_i += dt a_i ; x_i += dt v_i                   (symplectic Euler, kick then drift)
+// The reaction -G_ig on the body (Eqs. pressure_f2b, viscous_f2b) and its torque about r are
+// reduced per CTA (warp shuffle -> fp64 per warp -> fixed order) into D.part.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float damping) {
+    const int b = blockIdx.y;
+    RolloutState* rs = D.rs + b;
+    if (rs->frozen) return;   // CTA-uniform
+    const int i = blockIdx.x * TILE + threadIdx.x;
+    const size_t o = (size_t)b * P.N;
+    const int cur = rs->sp ^ rs->need_rebin;
+    const float2* __restrict__ pos = D.pos[cur] + o;
+    const float2* __restrict__ vel = D.vel[cur] + o;
+    const float2* __restrict__ aux = D.aux + o;
+    float fbx = 0.0f, fby = 0.0f, tq = 0.0f, vmax = 0.0f;
+    if (i < P.N) {
+        const float2 xi = pos[i], vi = vel[i], ai = aux[i];
+        const uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
+        float sx = 0.0f, sy = 0.0f;   // sum of (-pressure + viscous) * grad W / m^2
+        for_fluid_candidates(P, cs, D.skey[o + i], [&](uint32_t j) {
+            const float2 xj = __ldg(pos + j);
+            const float dx = __fsub_rn(xi.x, xj.x), dy = __fsub_rn(xi.y, xj.y);
+            const float r2 = dist2(dx, dy);
+            if (r2 < P.H2 && r2 > 0.0f) {
+                const float2 vj = __ldg(vel + j), aj = __ldg(aux + j);
+                const float r = sqrtf(r2);
+                const float gw = P.dwcb * dwcb_poly(r * P.inv_h) / r;   // |grad W| / r
+                const float vr = (vi.x - vj.x) * dx + (vi.y - vj.y) * dy;
+                const float visc = P.alpha2h / (ai.x + aj.x) * vr / (r2 + P.eps_h2);
+                const float s = (visc - (ai.y + aj.y)) * gw;
+                sx += s * dx;
+                sy += s * dy;
+            }
+        });
+        float gxs = 0.0f, gys = 0.0f;   // sum_g G_ig
+        const Geom gm = D.geom[b];
+        const float4* gst = D.gst + (size_t)b * P.G;
+        const float2* garm = D.garm + (size_t)b * P.G;
+        for_ghost_candidates(P, gm, xi, [&](int g) {
+            const float4 xg = __ldg(gst + g);
+            const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
+            const float r2 = dist2(dx, dy);
+            if (r2 < P.h2 && r2 > 0.0f) {
+                const float r = sqrtf(r2);
+                const float hr = P.h - r;
+                const float gw = P.dws3 * hr * hr / r;
+                const float vr = (vi.x - xg.z) * dx + (vi.y - xg.w) * dy;
+                const float cp = P.gsign2m2 * ai.y;
+                const float cv = P.m2 * P.beta / ai.x * fminf(vr, 0.0f) / (r2 + P.eps_h2);
+                const float c = (cp + cv) * gw;
+                const float Gx = c * dx, Gy = c * dy;
+                gxs += Gx;
+                gys += Gy;
+                const float2 a = __ldg(garm + g);
+                tq -= a.x * Gy - a.y * Gx;     // (r_g - r) x (-G_ig)
+            }
+        });
+        fbx = -gxs;
+        fby = -gys;
+        const float ax = P.mass * sx + gxs / P.mass + P.gx;
+        const float ay = P.mass * sy + gys / P.mass + P.gy;
+        float2 vn = make_float2(vi.x + P.dt * ax, vi.y + P.dt * ay);
+        const float2 xn = make_float2(xi.x + P.dt * vn.x, xi.y + P.dt * vn.y);
+        vn.x *= damping;
+        vn.y *= damping;
+        D.pos[cur ^ 1][o + i] = xn;
+        D.vel[cur ^ 1][o + i] = vn;
+        vmax = sqrtf(vn.x * vn.x + vn.y * vn.y);
+        const bool finite = isfinite(xn.x) && isfinite(xn.y) && isfinite(vn.x) && isfinite(vn.y);
+        if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || vmax > 1e9f)
+            set_status(rs, finite ? 2 : 1, (int)D.id[rs->ip ^ rs->need_rebin][o + i]);
+    }
+    // body partials: warp butterfly (deterministic), then warps in fixed order in fp64
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        fbx += __shfl_xor_sync(0xffffffffu, fbx, d);
+        fby += __shfl_xor_sync(0xffffffffu, fby, d);
+        tq += __shfl_xor_sync(0xffffffffu, tq, d);
+        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
+    }
+    __shared__ double4 wsum[TILE / 32];
+    if ((threadIdx.x & 31) == 0)
+        wsum[threadIdx.x >> 5] = make_double4(fbx, fby, tq, vmax);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double4 s = wsum[0];
+        for (int w = 1; w < TILE / 32; ++w) {
+            s.x += wsum[w].x;
+            s.y += wsum[w].y;
+            s.z += wsum[w].z;
+            s.w = fmax(s.w, wsum[w].w);
+        }
+        D.part[(size_t)b * P.ntile + blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Ghost kinematics, Eq. kinematicghost, in fp64 from the fp64 body state.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void ghost_update(const DevParams& P, const DevPtrs& D, int b,
+                                             const double* body, int tid, int nthr) {
+    const double c = cos(body[2]), s = sin(body[2]);
+    for (int g = tid; g < P.G; g += nthr) {
+        const double2 q = D.ghost_b[g];
+        const double ax = c * q.x - s * q.y, ay = s * q.x + c * q.y;
+        const double wx = ax + body[0], wy = ay + body[1];
+        const double vx = body[3] - body[5] * (wy - body[1]);
+        const double vy = body[4] + body[5] * (wx - body[0]);
+        D.gst[(size_t)b * P.G + g] = make_float4((float)wx, (float)wy, (float)vx, (float)vy);
+        D.garm[(size_t)b * P.G + g] = make_float2((float)(wx - body[0]), (float)(wy - body[1]));
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Body: fixed-order fp64 reduction of the CTA partials, Eq. tankdynamics
+//   m rddot = -sum G + (u_x, u_y),  J thddot = sum (r_g - r) x (-G) + tau,
+// symplectic Euler, status, rebin policy, then ghosts for the next substep.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(BODY_T) k_body(DevParams P, DevPtrs D, int pin,
+                                                 float ghost_angle0) {
+    const int b = blockIdx.x;
+    RolloutState* rs = D.rs + b;
+    __shared__ double4 red[BODY_T];
+    __shared__ double sbody[6];
+    __shared__ int sdead;
+    if (threadIdx.x == 0) sdead = rs->frozen;
+    __syncthreads();
+    if (sdead) return;
+    double4 s = make_double4(0, 0, 0, 0);
+    for (int t = threadIdx.x; t < P.ntile; t += BODY_T) {
+        const double4 q = D.part[(size_t)b * P.ntile + t];
+        s.x += q.x;
+        s.y += q.y;
+        s.z += q.z;
+        s.w = fmax(s.w, q.w);
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = BODY_T / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            double4 a = red[threadIdx.x], c = red[threadIdx.x + w];
+            red[threadIdx.x] = make_double4(a.x + c.x, a.y + c.y, a.z + c.z, fmax(a.w, c.w));
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double* body = D.body + (size_t)b * 6;
+        const float* u = D.u_cur + (size_t)b * 3;
+        const double4 f = red[0];
+        if (!pin) {
+            const double ax = (f.x + (double)u[0]) / P.m_body;
+            const double ay = (f.y + (double)u[1]) / P.m_body;
+            const double ath = (f.z + (double)u[2]) / P.J_body;
+            body[3] += P.dtd * ax;
+            body[4] += P.dtd * ay;
+            body[5] += P.dtd * ath;
+            body[0] += P.dtd * body[3];
+            body[1] += P.dtd * body[4];
+            body[2] += P.dtd * body[5];
+        }
+        bool fin = true, big = false;
+        for (int c = 0; c < 6; ++c) {
+            sbody[c] = body[c];
+            fin = fin && isfinite(body[c]);
+            big = big || fabs(body[c]) > 1e9;
+        }
+        if (!fin || big) set_status(rs, fin ? 2 : 1, -1);
+        D.geom[b] = Geom{(float)body[0], (float)body[1], (float)((double)body[2] + ghost_angle0), 0.f};
+        const int nr = rs->need_rebin;
+        rs->sp = rs->sp ^ nr ^ 1;
+        rs->ip ^= nr;
+        const float d = P.dt * (float)f.w;
+        rs->disp = nr ? d : rs->disp + d;
+        rs->need_rebin = P.rebin_every ? 1 : (rs->disp >= P.skin_half ? 1 : 0);
+        rs->step += 1;
+        if (rs->status) rs->frozen = 1;
+    }
+    __syncthreads();
+    ghost_update(P, D, b, sbody, threadIdx.x, BODY_T);
+}
+
+// ---------------------------------------------------------------------------------------
+// Slow tick (multi-rate loop): sample y_k before u_k, set the ZOH
+// input u_k from the table, tau from the PD law when pd != 0.
+// ---------------------------------------------------------------------------------------
+__global__ void k_tick(DevParams P, DevPtrs D, const float* __restrict__ u_seq,
+                       const float* __restrict__ theta_ref, float* y, float* u_applied, int K,
+                       int k, int pd, double Kp, double Kd) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= P.B) return;
+    const double* body = D.body + (size_t)b * 6;
+    const size_t bk = (size_t)b * K + k;
+    for (int c = 0; c < 6; ++c) y[bk * 6 + c] = (float)body[c];
+    float u0 = u_seq[bk * 3], u1 = u_seq[bk * 3 + 1], u2 = u_seq[bk * 3 + 2];
+    if (pd) u2 = (float)(Kp * ((double)theta_ref[bk] - body[2]) - Kd * body[5]);
+    D.u_cur[(size_t)b * 3] = u0;
+    D.u_cur[(size_t)b * 3 + 1] = u1;
+    D.u_cur[(size_t)b * 3 + 2] = u2;
+    if (u_applied) {
+        u_applied[bk * 3] = u0;
+        u_applied[bk * 3 + 1] = u1;
+        u_applied[bk * 3 + 2] = u2;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Host-boundary helpers: canonical-order import/export and ghost initialisation.
+// ---------------------------------------------------------------------------------------
+__global__ void k_import(DevParams P, DevPtrs D, int b0, const float4* __restrict__ in) {
+    const int b = b0 + blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.N) return;
+    const RolloutState* rs = D.rs + b;
+    const size_t o = (size_t)b * P.N;
+    const float4 v = in[i];
+    D.pos[rs->sp][o + i] = make_float2(v.x, v.y);
+    D.vel[rs->sp][o + i] = make_float2(v.z, v.w);
+    D.id[rs->ip][o + i] = (uint32_t)i;
+    D.aux[o + i] = make_float2(0.f, 0.f);
+}
+
+__global__ void k_export(DevParams P, DevPtrs D, int b, float4* out, float* rho) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.N) return;
+    const RolloutState* rs = D.rs + b;
+    const size_t o = (size_t)b * P.N;
+    const uint32_t id = D.id[rs->ip][o + i];
+    const float2 x = D.pos[rs->sp][o + i], v = D.vel[rs->sp][o + i];
+    out[id] = make_float4(x.x, x.y, v.x, v.y);
+    if (rho) rho[id] = D.aux[o + i].x;
+}
+
+__global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angle0) {
+    const int b = b0 + blockIdx.x;
+    RolloutState* rs = D.rs + b;
+    __shared__ double sbody[6];
+    if (threadIdx.x == 0) {
+        rs->need_rebin = 1;
+        rs->status = 0;
+        rs->frozen = 0;
+        rs->bad_step = -1;
+        rs->bad_particle = -1;
+        rs->disp = 0.f;
+        const double* body = D.body + (size_t)b * 6;
+        for (int c = 0; c < 6; ++c) sbody[c] = body[c];
+        D.geom[b] = Geom{(float)body[0], (float)body[1], (float)(body[2] + ghost_angle0), 0.f};
+    }
+    __syncthreads();
+    ghost_update(P, D, b, sbody, threadIdx.x, blockDim.x);
+}
+
+// Canonical cells of the current state (debug / parity, reading A19).
+__global__ void k_debug_cells(DevParams P, DevPtrs D, int b, int* cells) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.N) return;
+    const RolloutState* rs = D.rs + b;
+    const size_t o = (size_t)b * P.N;
+    const float2 x = D.pos[rs->sp][o + i];
+    const Geom gm = D.geom[b];
+    const float ox = __fsub_rn(gm.rx, P.half), oy = __fsub_rn(gm.ry, P.half);
+    const uint32_t id = D.id[rs->ip][o + i];
+    cells[2 * id] = cell_coord(x.x, ox, P.inv_C);
+    cells[2 * id + 1] = cell_coord(x.y, oy, P.inv_C);
+}
+
+// Neighbour sets through the kernels' own enumeration (after a forced rebuild into the
+// other buffer: reads pos[sp ^ 1], id[ip ^ 1]).
+__global__ void k_debug_neighbours(DevParams P, DevPtrs D, int b) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.N) return;
+    const RolloutState* rs = D.rs + b;
+    const size_t o = (size_t)b * P.N;
+    const int cur = rs->sp ^ 1, ic = rs->ip ^ 1;
+    const float2* pos = D.pos[cur] + o;
+    const uint32_t* id = D.id[ic] + o;
+    const uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
+    const float2 xi = pos[i];
+    const uint32_t me = id[i];
+    int* cnt = D.dbg_cnt;
+    int* idx = D.dbg_idx;
+    int n0 = 0, n1 = 0, n2 = 0;
+    for_fluid_candidates(P, cs, D.skey[o + i], [&](uint32_t j) {
+        const float2 xj = pos[j];
+        const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+        if (j != (uint32_t)i && r2 < P.H2) {
+            if (n0 < DBG_CAP) idx[(size_t)me * DBG_CAP + n0] = (int)id[j];
+            ++n0;
+        }
+    });
+    const Geom gm = D.geom[b];
+    const float4* gst = D.gst + (size_t)b * P.G;
+    for_ghost_candidates(P, gm, xi, [&](int g) {
+        const float4 xg = gst[g];
+        const float r2 = dist2(__fsub_rn(xi.x, xg.x), __fsub_rn(xi.y, xg.y));
+        if (r2 < P.H2) {
+            if (n1 < DBG_CAP) idx[((size_t)P.N + me) * DBG_CAP + n1] = g;
+            ++n1;
+        }
+        if (r2 < P.h2) {
+            if (n2 < DBG_CAP) idx[((size_t)2 * P.N + me) * DBG_CAP + n2] = g;
+            ++n2;
+        }
+    });
+    cnt[me] = n0;
+    cnt[P.N + me] = n1;
+    cnt[2 * P.N + me] = n2;
+}
+
+}  // namespace sph

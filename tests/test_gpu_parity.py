@@ -1,0 +1,299 @@
+"""GPU <-> oracle parity through the C ABI (SURVEY 8(c) protocol; tolerances from the north star:
+bit-exact cells and neighbour sets, 1e-5 one-step, 1e-3 body trajectories over 200 steps).
+
+Every input is seeded and synthetic (sph_inputs); the oracle computes every expected value."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import sph_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(t, B=1, **kw):
+    from paper_2604_12505_b200 import SphContext
+    return SphContext(t.params, t.pv32(), t.ghost_b, n_rollouts=B, **kw)
+
+
+def _csr_sets(off, idx):
+    return [tuple(idx[off[i]:off[i + 1]].tolist()) for i in range(len(off) - 1)]
+
+
+def _moving_tank(ell=1.0, seed=1, jitter=0.05, vel=0.01, body=None):
+    """Jittered lattice with random velocities (unsettled: one-step parity)."""
+    t = si.make_tank(ell, jitter=jitter, seed=seed)
+    t.vel = np.random.Generator(np.random.Philox(seed + 100)).normal(0, vel, t.pos.shape)
+    if body is not None:
+        th = body[2]
+        c, s = math.cos(th), math.sin(th)
+        p = t.pos.copy()
+        t.pos = np.stack([c * p[:, 0] - s * p[:, 1] + body[0], s * p[:, 0] + c * p[:, 1] + body[1]], 1)
+        t.body = np.asarray(body, np.float64)
+    return t.snapped()
+
+
+def _rel(a, b, floor=0.0):
+    return np.abs(a - b).max() / max(np.abs(b).max(), floor)
+
+
+# ---------------------------------------------------------------------------------------
+# Cells and neighbour sets: bit-exact (reading A19)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("case", ["rest", "moved_rotated", "after_200_steps", "adaptive_grid"])
+def test_cells_and_neighbour_sets_bit_exact(case):
+    body = [0.3, -0.2, 0.7, 0.01, -0.02, 0.05] if case == "moved_rotated" else None
+    t = _moving_tank(body=body)
+    kw = dict(rebin_every=0, skin=0.2 * t.params.h) if case == "adaptive_grid" else {}
+    ctx = _ctx(t, **kw)
+    if body is not None:
+        ctx.set_body_state(np.array([body]))
+    if case in ("after_200_steps", "adaptive_grid"):
+        ctx.step(np.array([[5.0, 2.0, 1.0]], np.float32), 200)
+    pv = ctx.get_particles(0)
+    p32 = np.ascontiguousarray(pv[:, :2])
+    g32 = np.ascontiguousarray(ctx.get_ghosts(0)[:, :2])
+    cells, grid = ctx.debug_cells(0)
+    ref = O.cells_f32(p32, grid[0], grid[1], grid[2])
+    assert np.array_equal(cells, ref)
+    assert grid[3] == np.float32(2 * t.params.h + kw.get("skin", 0.0))
+    nf, g2, g1 = ctx.debug_neighbours(0)
+    H = np.float32(2 * t.params.h)
+    h = np.float32(t.params.h)
+    assert _csr_sets(*nf) == _csr_sets(*O.neighbours_f32(p32, H * H))
+    assert _csr_sets(*g2) == _csr_sets(*O.ghost_neighbours_f32(p32, g32, H * H))
+    assert _csr_sets(*g1) == _csr_sets(*O.ghost_neighbours_f32(p32, g32, h * h))
+    # sanity: R1 lattice has ~8 fluid neighbours per particle and the wall is wetted
+    assert 5 < np.diff(nf[0]).mean() < 10
+    assert g1[0][-1] > 0
+    ctx.close()
+
+
+def test_ghost_world_state_matches_oracle():
+    """Eq. kinematicghost at a translated, rotated, moving pose."""
+    body = np.array([0.3, -0.2, 0.7, 0.01, -0.02, 0.05])
+    t = _moving_tank()
+    ctx = _ctx(t)
+    ctx.set_body_state(body[None])
+    g = ctx.get_ghosts(0).astype(np.float64)
+    gp, gv = O.ghosts(t.ghost_b, body)
+    assert np.abs(g[:, :2] - gp).max() <= 4e-8      # float32 rounding of ~0.5 m coordinates
+    assert np.abs(g[:, 2:] - gv).max() <= 1e-9
+    ctx.close()
+
+
+# ---------------------------------------------------------------------------------------
+# One-step parity (1e-5, SURVEY 8(c) normalisation)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("ell,body", [(1.0, None), (1.0, [0.3, -0.2, 0.7, 0.01, -0.02, 0.05]),
+                                      (4.0, None)])
+def test_one_step_parity(ell, body):
+    t = _moving_tank(ell=ell, body=body)
+    u = (5.0, 2.0, 1.0)
+    ctx = _ctx(t)
+    if body is not None:
+        ctx.set_body_state(np.array([body]))
+    ctx.step(np.array([u], np.float32), 1)
+    pv, rho = ctx.get_particles(0, with_rho=True)
+    bg = ctx.get_body_state()[0]
+    ref = O.State.from_tank(t)
+    rho_ref = ref.step(u, want_rho=True)
+    sp = t.params
+    vfloor = sp.dt * sp.k / sp.h
+    assert _rel(pv[:, :2], ref.pos) <= 1e-5
+    assert _rel(pv[:, 2:], ref.vel, vfloor) <= 1e-5
+    assert _rel(rho, rho_ref) <= 1e-5
+    # body: position, angle, rates (actuated case)
+    for sl in (slice(0, 2), slice(2, 3), slice(3, 5), slice(5, 6)):
+        assert _rel(bg[sl], ref.body[sl], 1e-12) <= 1e-5, (sl, bg, ref.body)
+    assert ctx.get_status()[0][0] == 0
+    ctx.close()
+
+
+# ---------------------------------------------------------------------------------------
+# 200-step body trajectory from a settled snapshot (1e-3)
+# ---------------------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def settled_c1():
+    t = si.make_tank(1.0)
+    s = O.settle(t, seconds=4.0)
+    t2 = si.Tank(t.params, s.pos, s.vel, t.ghost_b)
+    return t2.snapped()
+
+
+@pytest.mark.parametrize("rebin_every", [1, 0])
+def test_200_step_body_trajectory(settled_c1, rebin_every):
+    t = settled_c1
+    u = (5.0, 2.0, 1.0)
+    kw = {} if rebin_every else dict(rebin_every=0, skin=0.2 * t.params.h)
+    ctx = _ctx(t, **kw)
+    ref = O.State.from_tank(t)
+    yg, yo = [], []
+    for _ in range(200):
+        ctx.step(np.array([u], np.float32), 1)
+        ref.step(u)
+        yg.append(ctx.get_body_state()[0])
+        yo.append(ref.body.copy())
+    yg, yo = np.array(yg), np.array(yo)
+    for c in range(6):
+        assert _rel(yg[:, c], yo[:, c]) <= 1e-3, (c, _rel(yg[:, c], yo[:, c]))
+    pv = ctx.get_particles(0)
+    assert _rel(pv[:, :2], ref.pos) <= 1e-5
+    ctx.close()
+
+
+def test_rollout_pd_closed_loop_matches_oracle(settled_c1):
+    """Multi-rate loop + PD law on profile 1 over 1 s (20 ticks x 50)."""
+    t = settled_c1
+    sp = t.params
+    K = 20
+    u, th = si.profile(1, K)
+    th[:] = 0.1
+    ctx = _ctx(t)
+    y, ua = ctx.rollout(u[None].astype(np.float32), theta_ref=th[None].astype(np.float32),
+                        Kp=sp.Kp, Kd=sp.Kd)
+    ref = O.State.from_tank(t)
+    yo, uo = ref.rollout(u, sp.n_sub, theta_ref=th, Kp=sp.Kp, Kd=sp.Kd)
+    assert np.all(y[0, 0] == 0)
+    for c in range(6):
+        assert _rel(y[0, :, c], yo[:, c], 1e-12) <= 1e-3, c
+    assert _rel(ua[0], uo) <= 1e-3
+    ctx.close()
+
+
+# ---------------------------------------------------------------------------------------
+# Ensemble layout, determinism, graph == direct launches, failure isolation
+# ---------------------------------------------------------------------------------------
+def test_ensemble_invariance_and_determinism(settled_c1):
+    """A rollout in a batch of B is bitwise identical to the same rollout run alone,
+    and two identical runs are bitwise identical."""
+    t = settled_c1
+    K, B = 6, 5
+    u = si.ensemble_inputs(range(B), K)[0]
+    ctx = _ctx(t, B=B)
+    y, _ = ctx.rollout(u)
+    pv3 = ctx.get_particles(3)
+    ctx.close()
+    one = _ctx(t, B=1)
+    y1, _ = one.rollout(u[3:4])
+    assert np.array_equal(y1[0], y[3])
+    assert np.array_equal(one.get_particles(0), pv3)
+    one.close()
+    again = _ctx(t, B=B)
+    y2, _ = again.rollout(u)
+    assert np.array_equal(y2, y)
+    again.close()
+
+
+def test_graph_rollout_equals_direct_steps(settled_c1):
+    t = settled_c1
+    K = 3
+    u = si.ensemble_inputs([7], K)[0]
+    a = _ctx(t)
+    ya, _ = a.rollout(u)
+    b = _ctx(t)
+    for k in range(K):
+        b.step(u[:, k], t.params.n_sub)
+    assert np.array_equal(a.get_particles(0), b.get_particles(0))
+    assert np.array_equal(a.get_body_state(), b.get_body_state())
+    a.close()
+    b.close()
+
+
+def test_device_pointer_rollout_equals_host_pointer(settled_c1):
+    import torch
+    t = settled_c1
+    u = si.ensemble_inputs([1, 2], 4)[0]
+    a = _ctx(t, B=2)
+    ya, _ = a.rollout(u)
+    b = _ctx(t, B=2)
+    yb, _ = b.rollout(torch.from_numpy(u).cuda())
+    assert np.array_equal(ya, yb.cpu().numpy())
+    a.close()
+    b.close()
+
+
+def test_failure_freezes_only_the_bad_rollout(settled_c1):
+    t = settled_c1
+    ctx = _ctx(t, B=3)
+    bad = t.pv32().copy()
+    bad[10, 0] = 5.0            # a particle far outside the tank -> status 3 (left the grid)
+    ctx.set_state(bad, rollout=1)
+    ctx.step(np.array([[1.0, 0, 0]] * 3, np.float32), 5)
+    st, bs, bp = ctx.get_status()
+    assert st.tolist() == [0, 3, 0] and bs[1] == 0 and bp[1] == 10
+    ref = _ctx(t, B=1)
+    ref.step(np.array([[1.0, 0, 0]], np.float32), 5)
+    assert np.array_equal(ref.get_particles(0), ctx.get_particles(2))
+    ctx.close()
+    ref.close()
+
+
+def test_rigid_only_and_single_particle_edge_cases():
+    """N_f = 0 reproduces the closed form x_n = dt^2 (u/m) n(n+1)/2; a single particle
+    far from the wall has rho = m W(0) and stays at rest."""
+    from paper_2604_12505_b200 import SphContext
+    sp = si.preset(1.0)
+    ctx = SphContext(sp, np.zeros((0, 4), np.float32), si.ghost_ring(236), n_rollouts=2)
+    u = np.array([[5.0, -2.0, 0.7], [1.0, 1.0, 0.0]], np.float32)
+    ctx.step(u, 100)
+    body = ctx.get_body_state()
+    n = 100
+    for b in range(2):
+        acc = np.array([u[b, 0] / sp.m_body, u[b, 1] / sp.m_body, u[b, 2] / sp.J_body])
+        assert body[b, 3:6] == pytest.approx(n * sp.dt * acc, rel=1e-6, abs=1e-15)
+        assert body[b, 0:3] == pytest.approx(sp.dt ** 2 * acc * n * (n + 1) / 2, rel=1e-6, abs=1e-15)
+    ctx.close()
+    one = SphContext(sp, np.zeros((1, 4), np.float32), si.ghost_ring(236), n_rollouts=1)
+    one.step(np.zeros((1, 3), np.float32), 3)
+    pv, rho = one.get_particles(0, with_rho=True)
+    assert rho[0] == pytest.approx(sp.mass * O.W_cb(sp, 0.0), rel=1e-6)
+    assert np.all(pv == 0)
+    one.close()
+
+
+# ---------------------------------------------------------------------------------------
+# Full sizes in the bench launch configuration: sampled rollouts / particles
+# ---------------------------------------------------------------------------------------
+def test_c3_full_batch_sampled_rollouts():
+    """C3 layout: 1024 rollouts of the C2 tank (9,261 + 944) in one batch.  Rollouts get
+    different body poses; sampled rollouts are checked one step against the oracle."""
+    t = _moving_tank(ell=4.0, seed=3)
+    B = 1024
+    ctx = _ctx(t, B=B)
+    rng = np.random.Generator(np.random.Philox(9))
+    bodies = np.zeros((B, 6))
+    bodies[:, 2] = rng.uniform(-1, 1, B)
+    bodies[:, 5] = rng.uniform(-0.05, 0.05, B)
+    ctx.set_body_state(bodies)
+    u = rng.uniform(-5, 5, (B, 3)).astype(np.float32)
+    ctx.step(u, 1)
+    sp = t.params
+    for b in (0, 517, 1023):
+        pv = ctx.get_particles(b)
+        ref = O.State(sp, t.pos, t.vel, t.ghost_b, bodies[b])
+        ref.step(u[b].astype(np.float64))
+        # same world-frame fluid in every rollout; the wall ring is rotated by theta_b
+        assert _rel(pv[:, :2], ref.pos) <= 1e-5
+        assert _rel(pv[:, 2:], ref.vel, sp.dt * sp.k / sp.h) <= 1e-5
+    assert ctx.get_status()[0].max() == 0
+    ctx.close()
+
+
+def test_c4_million_particles_one_step():
+    """C4: 1,025,788 fluid + 9,912 ghosts (ell = 42), one substep vs the oracle on all particles."""
+    t = _moving_tank(ell=42.0, seed=4, jitter=0.02, vel=0.001)
+    assert t.n_fluid == 1025788
+    u = (5.0, 0.0, 0.0)
+    ctx = _ctx(t)
+    ctx.step(np.array([u], np.float32), 1)
+    pv, rho = ctx.get_particles(0, with_rho=True)
+    ref = O.State.from_tank(t)
+    rho_ref = ref.step(u, want_rho=True)
+    sp = t.params
+    assert _rel(pv[:, :2], ref.pos) <= 1e-5
+    assert _rel(pv[:, 2:], ref.vel, sp.dt * sp.k / sp.h) <= 1e-5
+    assert _rel(rho, rho_ref) <= 1e-5
+    ctx.close()
