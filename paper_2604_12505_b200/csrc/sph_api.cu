@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/sph.h"
@@ -131,71 +132,45 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     return true;
 }
 
-struct Layout {
-    size_t off[32];
-    size_t total;
-};
-
-static Layout layout(const DevParams& P) {
-    Layout L;
+// Workspace carve-up: one pass computes the offsets (base == nullptr) or binds the pointers.
+static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     size_t o = 0;
-    int k = 0;
     const size_t BN = (size_t)P.B * P.N, BG = (size_t)P.B * P.G;
-    auto put = [&](size_t bytes) {
-        L.off[k++] = o;
+    auto put = [&](auto*& ptr, size_t bytes) {
+        using T = std::remove_reference_t<decltype(*ptr)>;
+        ptr = base ? reinterpret_cast<T*>(base + o) : nullptr;
         o += (bytes + 255) & ~(size_t)255;
     };
-    put(BN * 8); put(BN * 8);           // pos[2]        0 1
-    put(BN * 8); put(BN * 8);           // vel[2]        2 3
-    put(BN * 4); put(BN * 4);           // id[2]         4 5
-    put(BN * 8);                        // aux           6
-    put(BN * 4); put(BN * 4);           // skey key      7 8
-    put(BN * 4); put(BN * 4);           // rank perm     9 10
-    put((size_t)P.B * P.ncell * 4);     // counts        11
-    put((size_t)P.B * (P.ncell + 1) * 4);  // cstart    12
-    put((size_t)P.B * P.nscan * 4);     // tsum          13
-    put(BG * 16);                       // gst           14
-    put(BG * 8);                        // garm          15
-    put((size_t)std::max(P.G, 1) * 16); // ghost_b       16
-    put((size_t)P.B * 48);              // body          17
-    put((size_t)P.B * 12);              // u_cur         18
-    put((size_t)P.B * P.ntile * 32);    // part          19
-    put((size_t)P.B * sizeof(RolloutState));  // rs     20
-    put((size_t)P.B * sizeof(Geom));    // geom          21
-    put((size_t)std::max(P.N, 1) * 16); // xfer          22
-    put((size_t)std::max(P.N, 1) * 4);  // xrho          23
-    L.total = o;
-    return L;
-}
-
-static void bind(DevPtrs* D, const Layout& L, char* base) {
-    auto p = [&](int k) { return (void*)(base + L.off[k]); };
-    D->pos[0] = (float2*)p(0);
-    D->pos[1] = (float2*)p(1);
-    D->vel[0] = (float2*)p(2);
-    D->vel[1] = (float2*)p(3);
-    D->id[0] = (uint32_t*)p(4);
-    D->id[1] = (uint32_t*)p(5);
-    D->aux = (float2*)p(6);
-    D->skey = (uint32_t*)p(7);
-    D->key = (uint32_t*)p(8);
-    D->rank = (uint32_t*)p(9);
-    D->perm = (uint32_t*)p(10);
-    D->counts = (uint32_t*)p(11);
-    D->cstart = (uint32_t*)p(12);
-    D->tsum = (uint32_t*)p(13);
-    D->gst = (float4*)p(14);
-    D->garm = (float2*)p(15);
-    D->ghost_b = (double2*)p(16);
-    D->body = (double*)p(17);
-    D->u_cur = (float*)p(18);
-    D->part = (double4*)p(19);
-    D->rs = (RolloutState*)p(20);
-    D->geom = (Geom*)p(21);
-    D->xfer = (float4*)p(22);
-    D->xrho = (float*)p(23);
-    D->dbg_cnt = nullptr;
-    D->dbg_idx = nullptr;
+    DevPtrs d{};
+    put(d.pos[0], BN * 8);
+    put(d.pos[1], BN * 8);
+    put(d.vel[0], BN * 8);
+    put(d.vel[1], BN * 8);
+    put(d.id[0], BN * 4);
+    put(d.id[1], BN * 4);
+    put(d.aux, BN * 8);
+    put(d.skey, BN * 4);
+    put(d.key, BN * 4);
+    put(d.rank, BN * 4);
+    put(d.perm, BN * 4);
+    put(d.counts, (size_t)P.B * P.ncell * 4);
+    put(d.cstart, (size_t)P.B * (P.ncell + 1) * 4);
+    put(d.tsum, (size_t)P.B * P.nscan * 4);
+    put(d.gst, BG * 16);
+    put(d.glo, BG * 8);
+    put(d.garm, BG * 8);
+    put(d.ghost_b, (size_t)std::max(P.G, 1) * 16);
+    put(d.body, (size_t)P.B * 48);
+    put(d.u_cur, (size_t)P.B * 12);
+    put(d.part, (size_t)P.B * P.ntile * 32);
+    put(d.rs, (size_t)P.B * sizeof(RolloutState));
+    put(d.geom, (size_t)P.B * sizeof(Geom));
+    put(d.xfer, (size_t)std::max(P.N, 1) * 16);
+    put(d.xrho, (size_t)std::max(P.N, 1) * 4);
+    d.dbg_cnt = nullptr;
+    d.dbg_idx = nullptr;
+    if (D) *D = d;
+    return o;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -261,7 +236,7 @@ size_t sph_workspace_bytes(const sph_fluid_params* fp, const sph_body_params* bp
     DevParams P;
     std::string why;
     if (!make_params(fp, bp, tp, n_fluid, n_ghost, n_rollouts, &P, &why)) return 0;
-    return layout(P).total;
+    return carve(P, nullptr, nullptr);
 }
 
 sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
@@ -277,9 +252,9 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
         return fail(nullptr, SPH_EINVAL, why);
     if ((n_fluid > 0 && !fluid_pv) || (n_ghost > 0 && !ghost_body_xy))
         return fail(nullptr, SPH_EINVAL, "fluid_pv / ghost_body_xy is NULL");
-    const Layout L = layout(P);
-    if (!d_workspace || workspace_bytes < L.total)
-        return fail(nullptr, SPH_ENOMEM, "workspace too small: need " + std::to_string(L.total) + " bytes");
+    const size_t total = carve(P, nullptr, nullptr);
+    if (!d_workspace || workspace_bytes < total)
+        return fail(nullptr, SPH_ENOMEM, "workspace too small: need " + std::to_string(total) + " bytes");
     if (((uintptr_t)d_workspace) & 255) return fail(nullptr, SPH_EINVAL, "workspace must be 256-byte aligned");
     for (int i = 0; i < 4 * n_fluid; ++i)
         if (!std::isfinite(fluid_pv[i])) return fail(nullptr, SPH_EINVAL, "non-finite fluid state");
@@ -300,7 +275,7 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
     ctx->P = P;
     ctx->n_sub = tp->substeps_per_sample;
     ctx->ghost_angle0 = (float)a0;
-    bind(&ctx->D, L, (char*)d_workspace);
+    carve(P, (char*)d_workspace, &ctx->D);
     if (cuda_stream) {
         ctx->stream = (cudaStream_t)cuda_stream;
     } else {
@@ -317,7 +292,7 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
         return SPH_ECUDA;
     };
     cudaError_t e;
-    if ((e = cudaMemsetAsync(d_workspace, 0, L.total, s)) != cudaSuccess) return bail("memset", e);
+    if ((e = cudaMemsetAsync(d_workspace, 0, total, s)) != cudaSuccess) return bail("memset", e);
     std::vector<double2> gb(std::max(n_ghost, 1));
     for (int g = 0; g < n_ghost; ++g) gb[g] = make_double2(ghost_body_xy[2 * g], ghost_body_xy[2 * g + 1]);
     if (n_ghost > 0 && (e = cudaMemcpyAsync(ctx->D.ghost_b, gb.data(), sizeof(double2) * n_ghost, cudaMemcpyHostToDevice, s)) != cudaSuccess)

@@ -73,7 +73,9 @@ struct DevPtrs {
     uint32_t* counts;    // [B][ncell] cell populations (kept zero between rebuilds)
     uint32_t* cstart;    // [B][ncell + 1] exclusive prefix of counts (cell start table)
     uint32_t* tsum;      // [B][nscan] scan tile sums
-    float4* gst;         // [B][G] ghost world state (x, y, vx, vy)
+    float4* gst;         // [B][G] ghost world state (x_hi, y_hi, vx, vy); x_hi = float(x)
+    float2* glo;         // [B][G] x - x_hi, y - y_hi (hi/lo pair: the hi part defines the
+                         // float32 neighbour predicate, hi + lo feeds the wall force)
     float2* garm;        // [B][G] ghost arm r_g - r (world frame)
     double2* ghost_b;    // [G] body-frame ghost positions
     double* body;        // [B][6] r_x r_y theta rd_x rd_y thd

@@ -223,15 +223,21 @@ __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D) {
     for_fluid_candidates(P, cs, D.skey[o + i], [&](uint32_t j) {
         const float2 xj = __ldg(pos + j);
         const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-        if (r2 < P.H2) wf += wcb_poly(sqrtf(r2) * P.inv_h);
+        if (r2 < P.H2) wf += wcb_poly(r2 > 0.0f ? r2 * rsqrtf(r2) * P.inv_h : 0.0f);
     });
     float wg = 0.0f;
     const Geom gm = D.geom[b];
     const float4* gst = D.gst + (size_t)b * P.G;
+    const float2* glo = D.glo + (size_t)b * P.G;
     for_ghost_candidates(P, gm, xi, [&](int g) {
         const float4 xg = __ldg(gst + g);
-        const float r2 = dist2(__fsub_rn(xi.x, xg.x), __fsub_rn(xi.y, xg.y));
-        if (r2 < P.H2) wg += wcb_poly(sqrtf(r2) * P.inv_h);
+        const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
+        if (dist2(dx, dy) < P.H2) {
+            const float2 lo = __ldg(glo + g);
+            const float ex = dx - lo.x, ey = dy - lo.y;
+            const float r2 = ex * ex + ey * ey;
+            wg += wcb_poly(r2 > 0.0f ? r2 * rsqrtf(r2) * P.inv_h : 0.0f);
+        }
     });
     const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
     const float pr = P.k * (rho - P.rho0);
@@ -270,10 +276,10 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
             const float r2 = dist2(dx, dy);
             if (r2 < P.H2 && r2 > 0.0f) {
                 const float2 vj = __ldg(vel + j), aj = __ldg(aux + j);
-                const float r = sqrtf(r2);
-                const float gw = P.dwcb * dwcb_poly(r * P.inv_h) / r;   // |grad W| / r
+                const float rs = rsqrtf(r2);                              // 1 / r
+                const float gw = P.dwcb * dwcb_poly(r2 * rs * P.inv_h) * rs;   // W'(r) / r
                 const float vr = (vi.x - vj.x) * dx + (vi.y - vj.y) * dy;
-                const float visc = P.alpha2h / (ai.x + aj.x) * vr / (r2 + P.eps_h2);
+                const float visc = __fdividef(P.alpha2h * vr, (ai.x + aj.x) * (r2 + P.eps_h2));
                 const float s = (visc - (ai.y + aj.y)) * gw;
                 sx += s * dx;
                 sy += s * dy;
@@ -282,12 +288,17 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
         float gxs = 0.0f, gys = 0.0f;   // sum_g G_ig
         const Geom gm = D.geom[b];
         const float4* gst = D.gst + (size_t)b * P.G;
+        const float2* glo = D.glo + (size_t)b * P.G;
         const float2* garm = D.garm + (size_t)b * P.G;
         for_ghost_candidates(P, gm, xi, [&](int g) {
             const float4 xg = __ldg(gst + g);
-            const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
-            const float r2 = dist2(dx, dy);
-            if (r2 < P.h2 && r2 > 0.0f) {
+            float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
+            if (dist2(dx, dy) < P.h2) {
+                const float2 lo = __ldg(glo + g);
+                dx -= lo.x;
+                dy -= lo.y;
+                const float r2 = dx * dx + dy * dy;
+                if (!(r2 > 0.0f)) return;
                 const float r = sqrtf(r2);
                 const float hr = P.h - r;
                 const float gw = P.dws3 * hr * hr / r;
@@ -353,7 +364,9 @@ __device__ __forceinline__ void ghost_update(const DevParams& P, const DevPtrs& 
         const double wx = ax + body[0], wy = ay + body[1];
         const double vx = body[3] - body[5] * (wy - body[1]);
         const double vy = body[4] + body[5] * (wx - body[0]);
-        D.gst[(size_t)b * P.G + g] = make_float4((float)wx, (float)wy, (float)vx, (float)vy);
+        const float hx = (float)wx, hy = (float)wy;
+        D.gst[(size_t)b * P.G + g] = make_float4(hx, hy, (float)vx, (float)vy);
+        D.glo[(size_t)b * P.G + g] = make_float2((float)(wx - (double)hx), (float)(wy - (double)hy));
         D.garm[(size_t)b * P.G + g] = make_float2((float)(wx - body[0]), (float)(wy - body[1]));
     }
 }
