@@ -70,9 +70,11 @@ typedef struct {
     double tank_radius;  /* inner wall radius R > 0  */
 } sph_body_params;
 
-/* Time stepping.  rebin_every = 1 rebuilds the cell list every substep; 0 rebuilds
- * adaptively when a particle may have moved more than skin/2 since the last rebuild (cells
- * are then 2h + skin wide, neighbour sets stay exact). */
+/* Time stepping.  rebin_every = 1 rebuilds the cell list and the neighbour lists every
+ * substep; 0 rebuilds them only when a particle may have moved (relative to the body
+ * translation) by 0.45 skin since the last rebuild.  Cells and lists are then 2h + skin wide
+ * (Verlet skin); the float32 predicate |x_i - x_j|^2 < (2h)^2 is re-applied to the current
+ * positions every substep, so the neighbour sets are exact in both modes. */
 typedef struct {
     double dt;                /* fast step > 0                                 */
     int substeps_per_sample;  /* n_sub = T_s / dt >= 1 (multi-rate)    */
@@ -159,10 +161,15 @@ sph_status sph_debug_neighbours(sph_ctx* ctx, int rollout, int64_t* nf_off, int3
  * ms[SPH_NUM_TIMERS] (order: see SPH_TIMER_* below). */
 enum {
     SPH_TIMER_HASH = 0, SPH_TIMER_SCAN = 1, SPH_TIMER_SCATTER = 2, SPH_TIMER_CELLSORT = 3,
-    SPH_TIMER_GATHER = 4, SPH_TIMER_DENSITY = 5, SPH_TIMER_FORCE = 6, SPH_TIMER_BODY = 7,
-    SPH_TIMER_SUBSTEP = 8, SPH_NUM_TIMERS = 9
+    SPH_TIMER_GATHER = 4, SPH_TIMER_NLIST = 5, SPH_TIMER_DENSITY = 6, SPH_TIMER_FORCE = 7,
+    SPH_TIMER_BODY = 8, SPH_TIMER_SUBSTEP = 9, SPH_NUM_TIMERS = 10
 };
 sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms);
+
+/* Per-rollout counters (host arrays of B, nullable): substeps taken and cell-list / neighbour-
+ * list rebuilds performed (with rebin_every = 0 rebuilds happen only when the displacement
+ * bound requires them). */
+sph_status sph_get_counters(sph_ctx* ctx, int64_t* steps, int32_t* rebuilds);
 
 /* Number of our kernel launches one substep issues (for the bench's gpu_launches count). */
 int sph_launches_per_substep(const sph_ctx* ctx);

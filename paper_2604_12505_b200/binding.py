@@ -15,8 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsphb200.so")
 
 SPH_OK, SPH_EINVAL, SPH_ENOMEM, SPH_ECUDA, SPH_EBLOWUP, SPH_ESTATE = 0, 1, 2, 3, 4, 6
-TIMER_NAMES = ["hash", "scan", "scatter", "cellsort", "gather", "density", "force", "body",
-               "substep"]
+TIMER_NAMES = ["hash", "scan", "scatter", "cellsort", "gather", "nlist", "density", "force",
+               "body", "substep"]
 
 
 class FluidParams(C.Structure):
@@ -70,6 +70,7 @@ def lib():
             "sph_debug_neighbours": (i32, [vp, i32, vp, vp, i64, vp, vp, i64, vp, vp, i64]),
             "sph_profile_substeps": (i32, [vp, i32, vp]),
             "sph_launches_per_substep": (i32, [vp]),
+            "sph_get_counters": (i32, [vp, vp, vp]),
             "sph_get_sizes": (None, [vp, vp, vp, vp, vp]),
             "sph_last_error": (C.c_char_p, [vp]),
             "sph_destroy": (None, [vp]),
@@ -86,7 +87,7 @@ def exported_symbols():
     return ["sph_workspace_bytes", "sph_init_tank", "sph_set_state", "sph_set_body_state",
             "sph_get_particles", "sph_get_ghosts", "sph_step", "sph_rollout_batch",
             "sph_get_body_state", "sph_settle", "sph_get_status", "sph_debug_cells",
-            "sph_debug_neighbours", "sph_profile_substeps", "sph_launches_per_substep",
+            "sph_debug_neighbours", "sph_profile_substeps", "sph_launches_per_substep", "sph_get_counters",
             "sph_get_sizes", "sph_last_error", "sph_destroy"]
 
 
@@ -286,6 +287,13 @@ class SphContext:
         self._check(self.L.sph_profile_substeps(self.ctx, int(n_substeps), ms.ctypes.data),
                     "sph_profile_substeps")
         return dict(zip(TIMER_NAMES, ms.tolist()))
+
+    def counters(self):
+        steps = np.zeros(self.B, np.int64)
+        reb = np.zeros(self.B, np.int32)
+        self._check(self.L.sph_get_counters(self.ctx, steps.ctypes.data, reb.ctypes.data),
+                    "sph_get_counters")
+        return steps, reb
 
     def launches_per_substep(self):
         return int(self.L.sph_launches_per_substep(self.ctx))

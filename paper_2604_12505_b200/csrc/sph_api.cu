@@ -110,7 +110,9 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->m_body = bp->m;
     P->J_body = bp->J;
     P->rebin_every = tp->rebin_every;
-    P->skin_half = (float)(0.5 * tp->skin);
+    const float RL = (float)(2.0 * h + (tp->rebin_every ? 0.0 : tp->skin));
+    P->RL2 = tp->rebin_every ? P->H2 : RL * RL;      // list radius (2h + skin)^2
+    P->rebuild_disp = (float)(0.45 * tp->skin);      // < skin / 2 with margin for rounding
     // ghost-ring window (see for_ghost_candidates): only particles farther than d_min from the
     // centre can have a ghost within 2h; their ghosts lie within +-dphi of their polar angle.
     const double d_min = R - 2.0 * h - 1e-3 * h;
@@ -150,6 +152,8 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     put(d.id[1], BN * 4);
     put(d.aux, BN * 8);
     put(d.skey, BN * 4);
+    put(d.nbr, BN * KMAX * 2);
+    put(d.ncnt, BN);
     put(d.key, BN * 4);
     put(d.rank, BN * 4);
     put(d.perm, BN * 4);
@@ -187,6 +191,7 @@ static void launch_rebin(sph_ctx* ctx) {
     k_scatter<<<gp, TILE, 0, s>>>(P, ctx->D);
     k_cellsort<<<gc, TILE, 0, s>>>(P, ctx->D);
     k_gather<<<gp, TILE, 0, s>>>(P, ctx->D);
+    k_nlist<<<gp, TILE, 0, s>>>(P, ctx->D);
 }
 
 static void launch_substep(sph_ctx* ctx, float damping, int pin) {
@@ -199,7 +204,7 @@ static void launch_substep(sph_ctx* ctx, float damping, int pin) {
     k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, pin, ctx->ghost_angle0);
 }
 
-static const int kLaunchesPerSubstep = 10;
+static const int kLaunchesPerSubstep = 11;
 
 static sph_status check_launch(sph_ctx* ctx) {
     cudaError_t e = cudaGetLastError();
@@ -552,7 +557,7 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
     if (!ctx || !ms || n_substeps < 1) return SPH_EINVAL;
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
-    cudaEvent_t ev[10];
+    cudaEvent_t ev[11];
     for (auto& e : ev) CK(cudaEventCreate(&e));
     double acc[SPH_NUM_TIMERS] = {0};
     dim3 gp(P.ntile, P.B), gs(P.nscan, P.B), gc((P.ncell + TILE - 1) / TILE, P.B);
@@ -570,22 +575,24 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
         cudaEventRecord(ev[4], s);
         k_gather<<<gp, TILE, 0, s>>>(P, ctx->D);
         cudaEventRecord(ev[5], s);
-        k_density<<<gp, TILE, 0, s>>>(P, ctx->D);
+        k_nlist<<<gp, TILE, 0, s>>>(P, ctx->D);
         cudaEventRecord(ev[6], s);
-        k_force<<<gp, TILE, 0, s>>>(P, ctx->D, 1.0f);
+        k_density<<<gp, TILE, 0, s>>>(P, ctx->D);
         cudaEventRecord(ev[7], s);
-        k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
+        k_force<<<gp, TILE, 0, s>>>(P, ctx->D, 1.0f);
         cudaEventRecord(ev[8], s);
+        k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
+        cudaEventRecord(ev[9], s);
         sph_status st = check_launch(ctx);
         if (st) return st;
-        CK(cudaEventSynchronize(ev[8]));
-        for (int t = 0; t < 8; ++t) {
+        CK(cudaEventSynchronize(ev[9]));
+        for (int t = 0; t < 9; ++t) {
             float m;
             CK(cudaEventElapsedTime(&m, ev[t], ev[t + 1]));
             acc[t] += m;
         }
         float m;
-        CK(cudaEventElapsedTime(&m, ev[0], ev[8]));
+        CK(cudaEventElapsedTime(&m, ev[0], ev[9]));
         acc[SPH_TIMER_SUBSTEP] += m;
     }
     for (int t = 0; t < SPH_NUM_TIMERS; ++t) ms[t] = (float)(acc[t] / n_substeps);
@@ -594,6 +601,18 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
 }
 
 int sph_launches_per_substep(const sph_ctx* ctx) { return ctx ? kLaunchesPerSubstep : 0; }
+
+sph_status sph_get_counters(sph_ctx* ctx, int64_t* steps, int32_t* rebuilds) {
+    if (!ctx) return SPH_EINVAL;
+    std::vector<RolloutState> rs(ctx->P.B);
+    CK(cudaMemcpyAsync(rs.data(), ctx->D.rs, sizeof(RolloutState) * ctx->P.B, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int b = 0; b < ctx->P.B; ++b) {
+        if (steps) steps[b] = rs[b].step;
+        if (rebuilds) rebuilds[b] = rs[b].rebuilds;
+    }
+    return SPH_OK;
+}
 
 void sph_get_sizes(const sph_ctx* ctx, int* n_fluid, int* n_ghost, int* n_rollouts, int* n_cells) {
     if (!ctx) return;

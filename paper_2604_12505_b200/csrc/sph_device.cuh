@@ -1,15 +1,20 @@
-// sph_device.cuh -- device-side data layout, parameters and the hot-path kernels of the
-// B200-native SPH fuel-sloshing step (sm_100a).  P:n = line n of the paper text.
+// sph_device.cuh -- device-side data layout, parameters and helpers of the B200-native SPH
+// fuel-sloshing step (sm_100a).  P:n = line n of the paper text.
 //
 // One substep of one rollout is (Algorithm 1, + symplectic Euler):
-//   [rebin]   k_hash -> k_scan_reduce -> k_scan_tiles -> k_scan_down -> k_scatter
-//             -> k_cellsort -> k_gather          (cell list by counting sort, row-major cells)
-//   k_density  Eq. density_update + Eq. EOS
+//   [rebuild, only when needed]
+//     k_hash -> k_scan_reduce -> k_scan_tiles -> k_scan_down -> k_scatter -> k_cellsort
+//     -> k_gather  (counting sort of the particles by cell, row-major cells of side 2h+skin)
+//     -> k_nlist   (per-particle candidate list within 2h+skin from the 3x3 cell block)
+//   k_density  Eq. density_update + Eq. EOS over the list
 //   k_force    Eqs. momentum, viscous, pressure_b2f / viscous_b2f,
 //              Alg. 1 l.8, kick-then-drift of the fluid, per-CTA body partials
 //   k_body     Eq. tankdynamics fixed-order fp64 reduction, body kick-drift,
-//              Eq. kinematicghost for the next substep, status, rebin policy
-// Every rollout owns whole CTAs (blockIdx.y = rollout), so results never depend on the batch.
+//              Eq. kinematicghost for the next substep, status, rebuild policy
+// The exact float32 neighbour predicate |x_i - x_j|^2 < (2h)^2 (reading A19) is applied to the
+// CURRENT positions inside k_density / k_force; the list is only a superset (Verlet skin), so
+// the neighbour sets are identical to a fresh all-pairs search every substep.
+// Every rollout owns whole CTAs (blockIdx.y = rollout): results never depend on the batch.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,14 +27,18 @@ constexpr int SCAN_V = 8;        // counts per scan thread
 constexpr int SCAN_TILE = SCAN_T * SCAN_V;
 constexpr int BODY_T = 128;      // threads of the per-rollout body kernel
 constexpr int SORT_LOCAL = 16;   // cells up to this size are sorted in registers
+constexpr int KMAX = 24;         // neighbour-list capacity; more -> cell-scan fallback
+constexpr int NL_OVERFLOW = 255; // ncnt value marking a particle that uses the fallback
+constexpr int DBG_CAP = 64;
 
 struct DevParams {
     int N, G, B;            // fluid particles / ghosts per rollout, rollouts
     int nx, ncell;          // square cell grid: nx * nx cells per rollout
     int ntile, nscan;       // CTAs per rollout (particle kernels, scan kernels)
     int ghost_K, ghost_full;
-    float C, inv_C, half;   // cell side (2h [+ skin]), 1/C, half extent of the grid
+    float C, inv_C, half;   // cell side (2h + skin), 1/C, half extent of the grid
     float h, inv_h, H2, h2; // h, 1/h, (2h)^2, h^2 in float32 (predicates, reading A19)
+    float RL2;              // list radius^2 = (2h + skin)^2
     float mass, m2, rho0, k, gamma1;
     float alpha2h, beta, eps_h2;
     float wcb, dwcb, dws3;  // C/h^2, C/h^3, -30/(pi h^5)
@@ -37,7 +46,7 @@ struct DevParams {
     float gx, gy, dt;
     float wall_r2;          // particles with |x - r|^2 <= wall_r2 see no ghost within 2h
     float ghost_scale;      // G / (2 pi)
-    float skin_half;
+    float rebuild_disp;     // rebuild when the displacement bound reaches this (< skin / 2)
     int rebin_every;
     double dtd, m_body, J_body;
 };
@@ -45,20 +54,23 @@ struct DevParams {
 struct RolloutState {
     int sp;              // particle state buffer parity
     int ip;              // id buffer parity
-    int need_rebin;      // rebuild the cell list at the start of the next substep
+    int need_rebin;      // rebuild cell list + neighbour lists at the start of the next substep
     int status;          // 0 ok, 1 non-finite, 2 |x| > 1e9, 3 left the grid (sticky)
     int frozen;          // set by k_body at the end of the substep in which status became
                          // non-zero; kernels skip frozen rollouts (the failing substep is
                          // committed whole, so the exported state stays consistent)
+    int rebuilds;        // number of rebuilds (diagnostics)
     long long step;      // substeps taken
     long long bad_step;
     int bad_particle;
-    float disp;          // displacement bound since the last rebuild (adaptive mode)
+    float disp;          // bound on any particle's displacement relative to the body
+                         // translation since the last rebuild
 };
 
-struct Geom {            // float copy of the body pose used by the particle kernels
+struct Geom {            // float copy of the body state used by the particle kernels
     float rx, ry, th;    // th = theta + angle of ghost 0 (ghost-ring lookup)
-    float pad;
+    float vx, vy;        // body velocity (relative-displacement bound)
+    float pad[3];
 };
 
 struct DevPtrs {
@@ -67,9 +79,11 @@ struct DevPtrs {
     uint32_t* id[2];     // [B][N] canonical id of each slot
     float2* aux;         // [B][N] (rho, P / rho^2)
     uint32_t* skey;      // [B][N] cell of each slot at the last rebuild
-    uint32_t* key;       // [B][N] rebin scratch: cell of each (unsorted) slot
-    uint32_t* rank;      // [B][N] rebin scratch: rank inside the cell
-    uint32_t* perm;      // [B][N] rebin scratch: new slot -> old slot
+    int16_t* nbr;        // [B][KMAX][N] neighbour candidates as slot offsets j - i
+    uint8_t* ncnt;       // [B][N] list length (NL_OVERFLOW: scan the cells instead)
+    uint32_t* key;       // [B][N] rebuild scratch: cell of each (unsorted) slot
+    uint32_t* rank;      // [B][N] rebuild scratch: rank inside the cell
+    uint32_t* perm;      // [B][N] rebuild scratch: new slot -> old slot
     uint32_t* counts;    // [B][ncell] cell populations (kept zero between rebuilds)
     uint32_t* cstart;    // [B][ncell + 1] exclusive prefix of counts (cell start table)
     uint32_t* tsum;      // [B][nscan] scan tile sums
@@ -80,7 +94,7 @@ struct DevPtrs {
     double2* ghost_b;    // [G] body-frame ghost positions
     double* body;        // [B][6] r_x r_y theta rd_x rd_y thd
     float* u_cur;        // [B][3] current ZOH input
-    double4* part;       // [B][ntile] per-CTA (F_x, F_y, T, vmax) partials
+    double4* part;       // [B][ntile] per-CTA (F_x, F_y, T, max relative speed) partials
     RolloutState* rs;    // [B]
     Geom* geom;          // [B]
     float4* xfer;        // [N] canonical-order export / import staging
@@ -88,8 +102,6 @@ struct DevPtrs {
     int* dbg_cnt;        // [3][N] debug neighbour counts
     int* dbg_idx;        // [3][N][DBG_CAP] debug neighbour ids
 };
-
-constexpr int DBG_CAP = 64;
 
 // ---------------------------------------------------------------------------------------
 // Small device helpers
@@ -131,8 +143,8 @@ __device__ __forceinline__ void set_status(RolloutState* rs, int code, int parti
 // rows cy-1..cy+1, each a contiguous slot range [start(cx-1), start(cx+2)) because cells are
 // numbered row-major and slots are sorted by cell.
 template <class F>
-__device__ __forceinline__ void for_fluid_candidates(const DevParams& P, const uint32_t* cs,
-                                                     uint32_t c, F&& f) {
+__device__ __forceinline__ void for_cell_candidates(const DevParams& P, const uint32_t* cs,
+                                                    uint32_t c, F&& f) {
     int cy = (int)c / P.nx;
     int cx = (int)c - cy * P.nx;
 #pragma unroll
@@ -140,6 +152,25 @@ __device__ __forceinline__ void for_fluid_candidates(const DevParams& P, const u
         int c0 = (cy + dy) * P.nx + cx - 1;
         uint32_t j0 = __ldg(cs + c0), j1 = __ldg(cs + c0 + 3);
         for (uint32_t j = j0; j < j1; ++j) f(j);
+    }
+}
+
+// Enumerate the fluid candidates of slot i (local index in its rollout): the neighbour list,
+// or the rebuild-time cell block when the list overflowed.  f(j) gets local slot indices
+// j != i.
+template <class F>
+__device__ __forceinline__ void for_fluid_candidates(const DevParams& P, const DevPtrs& D,
+                                                     int b, int i, F&& f) {
+    const size_t o = (size_t)b * P.N;
+    const int n = D.ncnt[o + i];
+    if (n != NL_OVERFLOW) {
+        const int16_t* nb = D.nbr + (size_t)b * KMAX * P.N + i;
+        for (int k = 0; k < n; ++k) f((uint32_t)(i + (int)__ldg(nb + (size_t)k * P.N)));
+    } else {
+        for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i],
+                            [&](uint32_t j) {
+                                if (j != (uint32_t)i) f(j);
+                            });
     }
 }
 

@@ -205,6 +205,36 @@ __global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Rebuild 8/8: neighbour candidate list of every slot: all j != i of the 3x3 rebuild-time cell
+// block with |x_i - x_j|^2 < (2h + skin)^2 (float32), stored as int16 slot offsets in a
+// [KMAX][N] interleaved layout (coalesced reads).  Lists that would exceed KMAX, or offsets
+// outside int16, mark the particle for the cell-scan fallback.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
+    const int b = blockIdx.y;
+    const RolloutState* rs = D.rs + b;
+    if (rs->frozen || !rs->need_rebin) return;
+    const int i = blockIdx.x * TILE + threadIdx.x;
+    if (i >= P.N) return;
+    const size_t o = (size_t)b * P.N;
+    const float2* __restrict__ pos = D.pos[rs->sp ^ 1] + o;   // the freshly gathered buffer
+    const float2 xi = pos[i];
+    int16_t* nb = D.nbr + (size_t)b * KMAX * P.N + i;
+    int n = 0;
+    for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
+        const float2 xj = __ldg(pos + j);
+        const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+        if (j != (uint32_t)i && r2 < P.RL2) {
+            const int off = (int)j - i;
+            if (n < KMAX && off >= -32768 && off <= 32767) nb[(size_t)n * P.N] = (int16_t)off;
+            else n = NL_OVERFLOW;
+            if (n != NL_OVERFLOW) ++n;
+        }
+    });
+    D.ncnt[o + i] = (uint8_t)n;
+}
+
+// ---------------------------------------------------------------------------------------
 // Density + EOS (Eq. density_update, Eq. EOS, cubic kernel P:268-271):
 //   rho_i = m ( sum_{j : r_ij < 2h} W_cb(r_ij)  [self included]  + gamma1 sum_g W_cb(r_ig) )
 //   P_i = k (rho_i - rho0);  stores (rho_i, P_i / rho_i^2).
@@ -217,10 +247,9 @@ __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D) {
     if (i >= P.N) return;
     const size_t o = (size_t)b * P.N;
     const float2* __restrict__ pos = D.pos[rs->sp ^ rs->need_rebin] + o;
-    const uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
     const float2 xi = pos[i];
-    float wf = 0.0f;
-    for_fluid_candidates(P, cs, D.skey[o + i], [&](uint32_t j) {
+    float wf = 4.0f;   // self term W_cb(0) ("all particles"): (2-0)^3 - 4 (1-0)^3 = 4
+    for_fluid_candidates(P, D, b, i, [&](uint32_t j) {
         const float2 xj = __ldg(pos + j);
         const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
         if (r2 < P.H2) wf += wcb_poly(r2 > 0.0f ? r2 * rsqrtf(r2) * P.inv_h : 0.0f);
@@ -266,11 +295,11 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
     const float2* __restrict__ vel = D.vel[cur] + o;
     const float2* __restrict__ aux = D.aux + o;
     float fbx = 0.0f, fby = 0.0f, tq = 0.0f, vmax = 0.0f;
+    const Geom gm = D.geom[b];
     if (i < P.N) {
         const float2 xi = pos[i], vi = vel[i], ai = aux[i];
-        const uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
         float sx = 0.0f, sy = 0.0f;   // sum of (-pressure + viscous) * grad W / m^2
-        for_fluid_candidates(P, cs, D.skey[o + i], [&](uint32_t j) {
+        for_fluid_candidates(P, D, b, i, [&](uint32_t j) {
             const float2 xj = __ldg(pos + j);
             const float dx = __fsub_rn(xi.x, xj.x), dy = __fsub_rn(xi.y, xj.y);
             const float r2 = dist2(dx, dy);
@@ -286,7 +315,6 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
             }
         });
         float gxs = 0.0f, gys = 0.0f;   // sum_g G_ig
-        const Geom gm = D.geom[b];
         const float4* gst = D.gst + (size_t)b * P.G;
         const float2* glo = D.glo + (size_t)b * P.G;
         const float2* garm = D.garm + (size_t)b * P.G;
@@ -323,9 +351,12 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
         vn.y *= damping;
         D.pos[cur ^ 1][o + i] = xn;
         D.vel[cur ^ 1][o + i] = vn;
-        vmax = sqrtf(vn.x * vn.x + vn.y * vn.y);
+        // speed relative to the body translation (bounds the drift of inter-particle vectors)
+        const float rvx = vn.x - gm.vx, rvy = vn.y - gm.vy;
+        vmax = sqrtf(rvx * rvx + rvy * rvy);
         const bool finite = isfinite(xn.x) && isfinite(xn.y) && isfinite(vn.x) && isfinite(vn.y);
-        if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || vmax > 1e9f)
+        if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || fabsf(vn.x) > 1e9f ||
+            fabsf(vn.y) > 1e9f)
             set_status(rs, finite ? 2 : 1, (int)D.id[rs->ip ^ rs->need_rebin][o + i]);
     }
     // body partials: warp butterfly (deterministic), then warps in fixed order in fp64
@@ -407,9 +438,10 @@ __global__ void __launch_bounds__(BODY_T) k_body(DevParams P, DevPtrs D, int pin
         double* body = D.body + (size_t)b * 6;
         const float* u = D.u_cur + (size_t)b * 3;
         const double4 f = red[0];
+        double ax = 0.0, ay = 0.0;
         if (!pin) {
-            const double ax = (f.x + (double)u[0]) / P.m_body;
-            const double ay = (f.y + (double)u[1]) / P.m_body;
+            ax = (f.x + (double)u[0]) / P.m_body;
+            ay = (f.y + (double)u[1]) / P.m_body;
             const double ath = (f.z + (double)u[2]) / P.J_body;
             body[3] += P.dtd * ax;
             body[4] += P.dtd * ay;
@@ -425,13 +457,17 @@ __global__ void __launch_bounds__(BODY_T) k_body(DevParams P, DevPtrs D, int pin
             big = big || fabs(body[c]) > 1e9;
         }
         if (!fin || big) set_status(rs, fin ? 2 : 1, -1);
-        D.geom[b] = Geom{(float)body[0], (float)body[1], (float)((double)body[2] + ghost_angle0), 0.f};
+        D.geom[b] = Geom{(float)body[0], (float)body[1], (float)((double)body[2] + ghost_angle0),
+                         (float)body[3], (float)body[4], {0.f, 0.f, 0.f}};
         const int nr = rs->need_rebin;
         rs->sp = rs->sp ^ nr ^ 1;
         rs->ip ^= nr;
-        const float d = P.dt * (float)f.w;
-        rs->disp = nr ? d : rs->disp + d;
-        rs->need_rebin = P.rebin_every ? 1 : (rs->disp >= P.skin_half ? 1 : 0);
+        rs->rebuilds += nr;
+        // drift of any particle relative to the body translation in this substep:
+        // dt |v_i' - rdot_n'| <= dt (|v_i' - rdot_n| + dt |rddot|)
+        const double d = P.dtd * (f.w + P.dtd * sqrt(ax * ax + ay * ay));
+        rs->disp = (float)(nr ? d : (double)rs->disp + d);
+        rs->need_rebin = P.rebin_every ? 1 : (rs->disp >= P.rebuild_disp ? 1 : 0);
         rs->step += 1;
         if (rs->status) rs->frozen = 1;
     }
@@ -503,7 +539,8 @@ __global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angl
         rs->disp = 0.f;
         const double* body = D.body + (size_t)b * 6;
         for (int c = 0; c < 6; ++c) sbody[c] = body[c];
-        D.geom[b] = Geom{(float)body[0], (float)body[1], (float)(body[2] + ghost_angle0), 0.f};
+        D.geom[b] = Geom{(float)body[0], (float)body[1], (float)(body[2] + ghost_angle0),
+                         (float)body[3], (float)body[4], {0.f, 0.f, 0.f}};
     }
     __syncthreads();
     ghost_update(P, D, b, sbody, threadIdx.x, blockDim.x);
@@ -533,16 +570,15 @@ __global__ void k_debug_neighbours(DevParams P, DevPtrs D, int b) {
     const int cur = rs->sp ^ 1, ic = rs->ip ^ 1;
     const float2* pos = D.pos[cur] + o;
     const uint32_t* id = D.id[ic] + o;
-    const uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
     const float2 xi = pos[i];
     const uint32_t me = id[i];
     int* cnt = D.dbg_cnt;
     int* idx = D.dbg_idx;
     int n0 = 0, n1 = 0, n2 = 0;
-    for_fluid_candidates(P, cs, D.skey[o + i], [&](uint32_t j) {
+    for_fluid_candidates(P, D, b, i, [&](uint32_t j) {
         const float2 xj = pos[j];
         const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-        if (j != (uint32_t)i && r2 < P.H2) {
+        if (r2 < P.H2) {
             if (n0 < DBG_CAP) idx[(size_t)me * DBG_CAP + n0] = (int)id[j];
             ++n0;
         }

@@ -18,8 +18,8 @@ ap.add_argument("--workload", default="C3")
 ap.add_argument("--rollouts", type=int, default=0)
 ap.add_argument("--substeps", type=int, default=6)
 ap.add_argument("--settle-steps", type=int, default=400)
-ap.add_argument("--rebin-every", type=int, default=1)
-ap.add_argument("--skin", type=float, default=0.0)
+ap.add_argument("--rebin-every", type=int, default=0)
+ap.add_argument("--skin", type=float, default=0.3)
 a = ap.parse_args()
 
 import torch  # noqa: E402
