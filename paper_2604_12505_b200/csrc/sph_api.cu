@@ -144,15 +144,13 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
         o += (bytes + 255) & ~(size_t)255;
     };
     DevPtrs d{};
-    put(d.pos[0], BN * 8);
-    put(d.pos[1], BN * 8);
-    put(d.vel[0], BN * 8);
-    put(d.vel[1], BN * 8);
+    put(d.pv[0], BN * 16);
+    put(d.pv[1], BN * 16);
     put(d.id[0], BN * 4);
     put(d.id[1], BN * 4);
     put(d.aux, BN * 8);
     put(d.skey, BN * 4);
-    put(d.nbr, BN * KMAX * 2);
+    put(d.nbr, BN * KQ * 8);
     put(d.ncnt, BN);
     put(d.key, BN * 4);
     put(d.rank, BN * 4);

@@ -28,6 +28,7 @@ constexpr int SCAN_TILE = SCAN_T * SCAN_V;
 constexpr int BODY_T = 128;      // threads of the per-rollout body kernel
 constexpr int SORT_LOCAL = 16;   // cells up to this size are sorted in registers
 constexpr int KMAX = 24;         // neighbour-list capacity; more -> cell-scan fallback
+constexpr int KQ = KMAX / 4;     // the list is stored as quads of int16 offsets (8 B loads)
 constexpr int NL_OVERFLOW = 255; // ncnt value marking a particle that uses the fallback
 constexpr int DBG_CAP = 64;
 
@@ -74,12 +75,11 @@ struct Geom {            // float copy of the body state used by the particle ke
 };
 
 struct DevPtrs {
-    float2* pos[2];      // [B][N] sorted-by-cell particle positions (double buffered)
-    float2* vel[2];      // [B][N] velocities
+    float4* pv[2];       // [B][N] sorted-by-cell particle state (x, y, vx, vy), double buffered
     uint32_t* id[2];     // [B][N] canonical id of each slot
     float2* aux;         // [B][N] (rho, P / rho^2)
     uint32_t* skey;      // [B][N] cell of each slot at the last rebuild
-    int16_t* nbr;        // [B][KMAX][N] neighbour candidates as slot offsets j - i
+    uint2* nbr;          // [B][KQ][N] neighbour candidates: 4 int16 slot offsets j - i per uint2
     uint8_t* ncnt;       // [B][N] list length (NL_OVERFLOW: scan the cells instead)
     uint32_t* key;       // [B][N] rebuild scratch: cell of each (unsorted) slot
     uint32_t* rank;      // [B][N] rebuild scratch: rank inside the cell
@@ -132,6 +132,12 @@ __device__ __forceinline__ float dwcb_poly(float q) {
     return d;
 }
 
+// t-th int16 offset (sign-extended) of a neighbour quad.
+__device__ __forceinline__ int quad_offset(uint2 w, int t) {
+    const uint32_t h = (t & 2) ? w.y : w.x;
+    return (t & 1) ? ((int)h >> 16) : (int)(int16_t)(h & 0xffffu);
+}
+
 __device__ __forceinline__ void set_status(RolloutState* rs, int code, int particle) {
     if (atomicCAS(&rs->status, 0, code) == 0) {
         rs->bad_step = rs->step;
@@ -164,8 +170,8 @@ __device__ __forceinline__ void for_fluid_candidates(const DevParams& P, const D
     const size_t o = (size_t)b * P.N;
     const int n = D.ncnt[o + i];
     if (n != NL_OVERFLOW) {
-        const int16_t* nb = D.nbr + (size_t)b * KMAX * P.N + i;
-        for (int k = 0; k < n; ++k) f((uint32_t)(i + (int)__ldg(nb + (size_t)k * P.N)));
+        const uint2* nq = D.nbr + (size_t)b * KQ * P.N + i;
+        for (int k = 0; k < n; ++k) f((uint32_t)(i + quad_offset(__ldg(nq + (k >> 2) * P.N), k & 3)));
     } else {
         for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i],
                             [&](uint32_t j) {

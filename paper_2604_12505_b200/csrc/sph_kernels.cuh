@@ -6,7 +6,7 @@
 namespace sph {
 
 // ---------------------------------------------------------------------------------------
-// Rebin 1/7: cell key + rank inside the cell (north star: "cell-hash build").
+// Rebuild 1/8: cell key + rank inside the cell (north star: "cell-hash build").
 // Grid origin o = float(r_body) - half (reading A19), cells row-major.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TILE) k_hash(DevParams P, DevPtrs D) {
@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(TILE) k_hash(DevParams P, DevPtrs D) {
     const int i = blockIdx.x * TILE + threadIdx.x;
     if (i >= P.N) return;
     const size_t o = (size_t)b * P.N;
-    const float2 x = D.pos[rs->sp][o + i];
+    const float4 x = D.pv[rs->sp][o + i];
     const Geom gm = D.geom[b];
     const float ox = __fsub_rn(gm.rx, P.half), oy = __fsub_rn(gm.ry, P.half);
     int cx = cell_coord(x.x, ox, P.inv_C), cy = cell_coord(x.y, oy, P.inv_C);
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(TILE) k_hash(DevParams P, DevPtrs D) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Rebin 2-4/7: segmented exclusive scan of the cell counts of each rollout
+// Rebuild 2-4/8: segmented exclusive scan of the cell counts of each rollout
 //   cstart[b][c] = sum_{c' < c} counts[b][c'],  c = 0..ncell  (cstart[b][ncell] = N).
 // Three phases (tile sums, scan of tile sums, down-sweep); the down-sweep re-zeroes counts.
 // ---------------------------------------------------------------------------------------
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_down(DevParams P, DevPtrs D) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Rebin 5/7: scatter old slot -> new slot (cell start + rank).
+// Rebuild 5/8: scatter old slot -> new slot (cell start + rank).
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TILE) k_scatter(DevParams P, DevPtrs D) {
     const int b = blockIdx.y;
@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(TILE) k_scatter(DevParams P, DevPtrs D) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Rebin 6/7: make the order inside every cell ascending in canonical id (the atomic ranks are
-// not deterministic; this makes the whole sort deterministic and history independent,
+// Rebuild 6/8: make the order inside every cell ascending in canonical id (the atomic ranks
+// are not deterministic; this makes the whole sort deterministic and history independent,
 // reading A20).  One thread per cell.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TILE) k_cellsort(DevParams P, DevPtrs D) {
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(TILE) k_cellsort(DevParams P, DevPtrs D) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Rebin 7/7: gather the state into cell order (coalesced writes; reads are nearly sequential
+// Rebuild 7/8: gather the state into cell order (coalesced writes; reads are nearly sequential
 // because particles move little between rebuilds).
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) {
@@ -198,16 +198,16 @@ __global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) {
     const size_t o = (size_t)b * P.N;
     const int sp = rs->sp, ip = rs->ip;
     const uint32_t src = D.perm[o + d];
-    D.pos[sp ^ 1][o + d] = D.pos[sp][o + src];
-    D.vel[sp ^ 1][o + d] = D.vel[sp][o + src];
+    D.pv[sp ^ 1][o + d] = D.pv[sp][o + src];
     D.id[ip ^ 1][o + d] = D.id[ip][o + src];
     D.skey[o + d] = D.key[o + src];
 }
 
 // ---------------------------------------------------------------------------------------
-// Rebuild 8/8: neighbour candidate list of every slot: all j != i of the 3x3 rebuild-time cell
-// block with |x_i - x_j|^2 < (2h + skin)^2 (float32), stored as int16 slot offsets in a
-// [KMAX][N] interleaved layout (coalesced reads).  Lists that would exceed KMAX, or offsets
+// Rebuild 8/8: neighbour candidate list of every slot: all j != i of the 3x3 rebuild-time
+// cell block with |x_i - x_j|^2 < (2h + skin)^2 (float32), stored as int16 slot offsets,
+// four per uint2, in a [KQ][N] interleaved layout (one coalesced 8-byte load per four
+// candidates).  Unused entries of the last quad are 0.  Lists longer than KMAX, or offsets
 // outside int16, mark the particle for the cell-scan fallback.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
@@ -217,20 +217,31 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
     const int i = blockIdx.x * TILE + threadIdx.x;
     if (i >= P.N) return;
     const size_t o = (size_t)b * P.N;
-    const float2* __restrict__ pos = D.pos[rs->sp ^ 1] + o;   // the freshly gathered buffer
-    const float2 xi = pos[i];
-    int16_t* nb = D.nbr + (size_t)b * KMAX * P.N + i;
+    const float4* __restrict__ pv = D.pv[rs->sp ^ 1] + o;   // the freshly gathered buffer
+    const float4 xi = pv[i];
+    uint2* nq = D.nbr + (size_t)b * KQ * P.N + i;
     int n = 0;
+    uint32_t acc0 = 0u, acc1 = 0u;
     for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
-        const float2 xj = __ldg(pos + j);
+        const float4 xj = __ldg(pv + j);
         const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-        if (j != (uint32_t)i && r2 < P.RL2) {
+        if (j != (uint32_t)i && r2 < P.RL2 && n != NL_OVERFLOW) {
             const int off = (int)j - i;
-            if (n < KMAX && off >= -32768 && off <= 32767) nb[(size_t)n * P.N] = (int16_t)off;
-            else n = NL_OVERFLOW;
-            if (n != NL_OVERFLOW) ++n;
+            if (n >= KMAX || off < -32768 || off > 32767) {
+                n = NL_OVERFLOW;
+                return;
+            }
+            const uint32_t bits = (uint32_t)(uint16_t)(int16_t)off << (16 * (n & 1));
+            if (n & 2) acc1 |= bits;
+            else acc0 |= bits;
+            ++n;
+            if ((n & 3) == 0) {
+                nq[(size_t)((n >> 2) - 1) * P.N] = make_uint2(acc0, acc1);
+                acc0 = acc1 = 0u;
+            }
         }
     });
+    if (n != NL_OVERFLOW && (n & 3)) nq[(size_t)(n >> 2) * P.N] = make_uint2(acc0, acc1);
     D.ncnt[o + i] = (uint8_t)n;
 }
 
@@ -238,7 +249,16 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
 // Density + EOS (Eq. density_update, Eq. EOS, cubic kernel P:268-271):
 //   rho_i = m ( sum_{j : r_ij < 2h} W_cb(r_ij)  [self included]  + gamma1 sum_g W_cb(r_ig) )
 //   P_i = k (rho_i - rho0);  stores (rho_i, P_i / rho_i^2).
+// The list is walked four candidates at a time: one 8-byte offset load, four independent
+// 16-byte state loads, then branch-free masked arithmetic.
 // ---------------------------------------------------------------------------------------
+__device__ __forceinline__ float w_masked(const DevParams& P, float4 xi, float4 xj, bool valid) {
+    const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+    const float r = r2 > 0.0f ? r2 * rsqrtf(r2) : 0.0f;
+    const float w = wcb_poly(r * P.inv_h);
+    return (valid && r2 < P.H2) ? w : 0.0f;
+}
+
 __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D) {
     const int b = blockIdx.y;
     const RolloutState* rs = D.rs + b;
@@ -246,19 +266,32 @@ __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D) {
     const int i = blockIdx.x * TILE + threadIdx.x;
     if (i >= P.N) return;
     const size_t o = (size_t)b * P.N;
-    const float2* __restrict__ pos = D.pos[rs->sp ^ rs->need_rebin] + o;
-    const float2 xi = pos[i];
+    const float4* __restrict__ pv = D.pv[rs->sp ^ rs->need_rebin] + o;
+    const float4 xi = pv[i];
     float wf = 4.0f;   // self term W_cb(0) ("all particles"): (2-0)^3 - 4 (1-0)^3 = 4
-    for_fluid_candidates(P, D, b, i, [&](uint32_t j) {
-        const float2 xj = __ldg(pos + j);
-        const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-        if (r2 < P.H2) wf += wcb_poly(r2 > 0.0f ? r2 * rsqrtf(r2) * P.inv_h : 0.0f);
-    });
+    const int n = D.ncnt[o + i];
+    if (n != NL_OVERFLOW) {
+        const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
+        for (int k = 0; k < n; k += 4) {
+            const uint2 w = __ldg(nq);
+            nq += P.N;
+            const float4 x0 = __ldg(pv + i + quad_offset(w, 0));
+            const float4 x1 = __ldg(pv + i + quad_offset(w, 1));
+            const float4 x2 = __ldg(pv + i + quad_offset(w, 2));
+            const float4 x3 = __ldg(pv + i + quad_offset(w, 3));
+            wf += w_masked(P, xi, x0, k < n) + w_masked(P, xi, x1, k + 1 < n) +
+                  w_masked(P, xi, x2, k + 2 < n) + w_masked(P, xi, x3, k + 3 < n);
+        }
+    } else {
+        for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
+            wf += w_masked(P, xi, __ldg(pv + j), j != (uint32_t)i);
+        });
+    }
     float wg = 0.0f;
     const Geom gm = D.geom[b];
     const float4* gst = D.gst + (size_t)b * P.G;
     const float2* glo = D.glo + (size_t)b * P.G;
-    for_ghost_candidates(P, gm, xi, [&](int g) {
+    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), [&](int g) {
         const float4 xg = __ldg(gst + g);
         const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
         if (dist2(dx, dy) < P.H2) {
@@ -270,7 +303,7 @@ __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D) {
     });
     const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
     const float pr = P.k * (rho - P.rho0);
-    D.aux[o + i] = make_float2(rho, pr / (rho * rho));
+    D.aux[o + i] = make_float2(rho, __fdividef(pr, rho * rho));
 }
 
 // ---------------------------------------------------------------------------------------
@@ -284,6 +317,21 @@ __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D) {
 // The reaction -G_ig on the body (Eqs. pressure_f2b, viscous_f2b) and its torque about r are
 // reduced per CTA (warp shuffle -> fp64 per warp -> fixed order) into D.part.
 // ---------------------------------------------------------------------------------------
+// (-pressure + viscous) pair term per m^2, times r_ij, accumulated into (sx, sy).
+__device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2 ai, float4 xj,
+                                           float2 aj, bool valid, float& sx, float& sy) {
+    const float dx = __fsub_rn(xi.x, xj.x), dy = __fsub_rn(xi.y, xj.y);
+    const float r2 = dist2(dx, dy);
+    const float rs = rsqrtf(r2);                                   // 1 / r (inf at r = 0)
+    const float gw = P.dwcb * dwcb_poly(r2 * rs * P.inv_h) * rs;   // W'(r) / r
+    const float vr = (xi.z - xj.z) * dx + (xi.w - xj.w) * dy;
+    const float visc = __fdividef(P.alpha2h * vr, (ai.x + aj.x) * (r2 + P.eps_h2));
+    float s = (visc - (ai.y + aj.y)) * gw;
+    s = (valid && r2 < P.H2 && r2 > 0.0f) ? s : 0.0f;              // exact predicate (A19)
+    sx += s * dx;
+    sy += s * dy;
+}
+
 __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float damping) {
     const int b = blockIdx.y;
     RolloutState* rs = D.rs + b;
@@ -291,34 +339,41 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
     const int i = blockIdx.x * TILE + threadIdx.x;
     const size_t o = (size_t)b * P.N;
     const int cur = rs->sp ^ rs->need_rebin;
-    const float2* __restrict__ pos = D.pos[cur] + o;
-    const float2* __restrict__ vel = D.vel[cur] + o;
+    const float4* __restrict__ pv = D.pv[cur] + o;
     const float2* __restrict__ aux = D.aux + o;
     float fbx = 0.0f, fby = 0.0f, tq = 0.0f, vmax = 0.0f;
     const Geom gm = D.geom[b];
     if (i < P.N) {
-        const float2 xi = pos[i], vi = vel[i], ai = aux[i];
+        const float4 xi = pv[i];
+        const float2 ai = aux[i];
         float sx = 0.0f, sy = 0.0f;   // sum of (-pressure + viscous) * grad W / m^2
-        for_fluid_candidates(P, D, b, i, [&](uint32_t j) {
-            const float2 xj = __ldg(pos + j);
-            const float dx = __fsub_rn(xi.x, xj.x), dy = __fsub_rn(xi.y, xj.y);
-            const float r2 = dist2(dx, dy);
-            if (r2 < P.H2 && r2 > 0.0f) {
-                const float2 vj = __ldg(vel + j), aj = __ldg(aux + j);
-                const float rs = rsqrtf(r2);                              // 1 / r
-                const float gw = P.dwcb * dwcb_poly(r2 * rs * P.inv_h) * rs;   // W'(r) / r
-                const float vr = (vi.x - vj.x) * dx + (vi.y - vj.y) * dy;
-                const float visc = __fdividef(P.alpha2h * vr, (ai.x + aj.x) * (r2 + P.eps_h2));
-                const float s = (visc - (ai.y + aj.y)) * gw;
-                sx += s * dx;
-                sy += s * dy;
+        const int n = D.ncnt[o + i];
+        if (n != NL_OVERFLOW) {
+            const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
+            for (int k = 0; k < n; k += 4) {
+                const uint2 w = __ldg(nq);
+                nq += P.N;
+                const int j0 = i + quad_offset(w, 0), j1 = i + quad_offset(w, 1);
+                const int j2 = i + quad_offset(w, 2), j3 = i + quad_offset(w, 3);
+                const float4 x0 = __ldg(pv + j0), x1 = __ldg(pv + j1);
+                const float4 x2 = __ldg(pv + j2), x3 = __ldg(pv + j3);
+                const float2 a0 = __ldg(aux + j0), a1 = __ldg(aux + j1);
+                const float2 a2 = __ldg(aux + j2), a3 = __ldg(aux + j3);
+                pair_force(P, xi, ai, x0, a0, k < n, sx, sy);
+                pair_force(P, xi, ai, x1, a1, k + 1 < n, sx, sy);
+                pair_force(P, xi, ai, x2, a2, k + 2 < n, sx, sy);
+                pair_force(P, xi, ai, x3, a3, k + 3 < n, sx, sy);
             }
-        });
+        } else {
+            for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
+                pair_force(P, xi, ai, __ldg(pv + j), __ldg(aux + j), j != (uint32_t)i, sx, sy);
+            });
+        }
         float gxs = 0.0f, gys = 0.0f;   // sum_g G_ig
         const float4* gst = D.gst + (size_t)b * P.G;
         const float2* glo = D.glo + (size_t)b * P.G;
         const float2* garm = D.garm + (size_t)b * P.G;
-        for_ghost_candidates(P, gm, xi, [&](int g) {
+        for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), [&](int g) {
             const float4 xg = __ldg(gst + g);
             float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
             if (dist2(dx, dy) < P.h2) {
@@ -330,7 +385,7 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
                 const float r = sqrtf(r2);
                 const float hr = P.h - r;
                 const float gw = P.dws3 * hr * hr / r;
-                const float vr = (vi.x - xg.z) * dx + (vi.y - xg.w) * dy;
+                const float vr = (xi.z - xg.z) * dx + (xi.w - xg.w) * dy;
                 const float cp = P.gsign2m2 * ai.y;
                 const float cv = P.m2 * P.beta / ai.x * fminf(vr, 0.0f) / (r2 + P.eps_h2);
                 const float c = (cp + cv) * gw;
@@ -345,18 +400,20 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
         fby = -gys;
         const float ax = P.mass * sx + gxs / P.mass + P.gx;
         const float ay = P.mass * sy + gys / P.mass + P.gy;
-        float2 vn = make_float2(vi.x + P.dt * ax, vi.y + P.dt * ay);
-        const float2 xn = make_float2(xi.x + P.dt * vn.x, xi.y + P.dt * vn.y);
-        vn.x *= damping;
-        vn.y *= damping;
-        D.pos[cur ^ 1][o + i] = xn;
-        D.vel[cur ^ 1][o + i] = vn;
+        float4 xn;
+        xn.z = xi.z + P.dt * ax;
+        xn.w = xi.w + P.dt * ay;
+        xn.x = xi.x + P.dt * xn.z;
+        xn.y = xi.y + P.dt * xn.w;
+        xn.z *= damping;
+        xn.w *= damping;
+        D.pv[cur ^ 1][o + i] = xn;
         // speed relative to the body translation (bounds the drift of inter-particle vectors)
-        const float rvx = vn.x - gm.vx, rvy = vn.y - gm.vy;
+        const float rvx = xn.z - gm.vx, rvy = xn.w - gm.vy;
         vmax = sqrtf(rvx * rvx + rvy * rvy);
-        const bool finite = isfinite(xn.x) && isfinite(xn.y) && isfinite(vn.x) && isfinite(vn.y);
-        if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || fabsf(vn.x) > 1e9f ||
-            fabsf(vn.y) > 1e9f)
+        const bool finite = isfinite(xn.x) && isfinite(xn.y) && isfinite(xn.z) && isfinite(xn.w);
+        if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || fabsf(xn.z) > 1e9f ||
+            fabsf(xn.w) > 1e9f)
             set_status(rs, finite ? 2 : 1, (int)D.id[rs->ip ^ rs->need_rebin][o + i]);
     }
     // body partials: warp butterfly (deterministic), then warps in fixed order in fp64
@@ -405,7 +462,7 @@ __device__ __forceinline__ void ghost_update(const DevParams& P, const DevPtrs& 
 // ---------------------------------------------------------------------------------------
 // Body: fixed-order fp64 reduction of the CTA partials, Eq. tankdynamics
 //   m rddot = -sum G + (u_x, u_y),  J thddot = sum (r_g - r) x (-G) + tau,
-// symplectic Euler, status, rebin policy, then ghosts for the next substep.
+// symplectic Euler, status, rebuild policy, then ghosts for the next substep.
 // ---------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(BODY_T) k_body(DevParams P, DevPtrs D, int pin,
                                                  float ghost_angle0) {
@@ -508,9 +565,7 @@ __global__ void k_import(DevParams P, DevPtrs D, int b0, const float4* __restric
     if (i >= P.N) return;
     const RolloutState* rs = D.rs + b;
     const size_t o = (size_t)b * P.N;
-    const float4 v = in[i];
-    D.pos[rs->sp][o + i] = make_float2(v.x, v.y);
-    D.vel[rs->sp][o + i] = make_float2(v.z, v.w);
+    D.pv[rs->sp][o + i] = in[i];
     D.id[rs->ip][o + i] = (uint32_t)i;
     D.aux[o + i] = make_float2(0.f, 0.f);
 }
@@ -521,8 +576,7 @@ __global__ void k_export(DevParams P, DevPtrs D, int b, float4* out, float* rho)
     const RolloutState* rs = D.rs + b;
     const size_t o = (size_t)b * P.N;
     const uint32_t id = D.id[rs->ip][o + i];
-    const float2 x = D.pos[rs->sp][o + i], v = D.vel[rs->sp][o + i];
-    out[id] = make_float4(x.x, x.y, v.x, v.y);
+    out[id] = D.pv[rs->sp][o + i];
     if (rho) rho[id] = D.aux[o + i].x;
 }
 
@@ -552,7 +606,7 @@ __global__ void k_debug_cells(DevParams P, DevPtrs D, int b, int* cells) {
     if (i >= P.N) return;
     const RolloutState* rs = D.rs + b;
     const size_t o = (size_t)b * P.N;
-    const float2 x = D.pos[rs->sp][o + i];
+    const float4 x = D.pv[rs->sp][o + i];
     const Geom gm = D.geom[b];
     const float ox = __fsub_rn(gm.rx, P.half), oy = __fsub_rn(gm.ry, P.half);
     const uint32_t id = D.id[rs->ip][o + i];
@@ -561,22 +615,22 @@ __global__ void k_debug_cells(DevParams P, DevPtrs D, int b, int* cells) {
 }
 
 // Neighbour sets through the kernels' own enumeration (after a forced rebuild into the
-// other buffer: reads pos[sp ^ 1], id[ip ^ 1]).
+// other buffer: reads pv[sp ^ 1], id[ip ^ 1]).
 __global__ void k_debug_neighbours(DevParams P, DevPtrs D, int b) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.N) return;
     const RolloutState* rs = D.rs + b;
     const size_t o = (size_t)b * P.N;
     const int cur = rs->sp ^ 1, ic = rs->ip ^ 1;
-    const float2* pos = D.pos[cur] + o;
+    const float4* pv = D.pv[cur] + o;
     const uint32_t* id = D.id[ic] + o;
-    const float2 xi = pos[i];
+    const float4 xi = pv[i];
     const uint32_t me = id[i];
     int* cnt = D.dbg_cnt;
     int* idx = D.dbg_idx;
     int n0 = 0, n1 = 0, n2 = 0;
     for_fluid_candidates(P, D, b, i, [&](uint32_t j) {
-        const float2 xj = pos[j];
+        const float4 xj = pv[j];
         const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
         if (r2 < P.H2) {
             if (n0 < DBG_CAP) idx[(size_t)me * DBG_CAP + n0] = (int)id[j];
@@ -585,7 +639,7 @@ __global__ void k_debug_neighbours(DevParams P, DevPtrs D, int b) {
     });
     const Geom gm = D.geom[b];
     const float4* gst = D.gst + (size_t)b * P.G;
-    for_ghost_candidates(P, gm, xi, [&](int g) {
+    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), [&](int g) {
         const float4 xg = gst[g];
         const float r2 = dist2(__fsub_rn(xi.x, xg.x), __fsub_rn(xi.y, xg.y));
         if (r2 < P.H2) {
