@@ -84,6 +84,7 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->ncell = P->nx * P->nx;
     P->half = (float)half_cells * P->C;
     P->ntile = std::max(1, (N + TILE - 1) / TILE);
+    P->npart = P->ntile * (TILE / 32);
     P->nscan = (P->ncell + 1 + SCAN_TILE - 1) / SCAN_TILE;
     if ((P->nscan + SCAN_T - 1) / SCAN_T > SCAN_V) return *why = "cell grid too large for the scan", false;
     P->h = (float)h;
@@ -115,22 +116,23 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->rebuild_disp = (float)(0.45 * tp->skin);      // < skin / 2 with margin for rounding
     // ghost-ring window (see for_ghost_candidates): only particles farther than d_min from the
     // centre can have a ghost within 2h; their ghosts lie within +-dphi of their polar angle.
-    const double d_min = R - 2.0 * h - 1e-3 * h;
+    // |x - g| < s with |x| = d, |g| = R  =>  d > R - s  and  sin(dphi/2) < s / (2 sqrt(d R)).
     P->ghost_scale = (float)(G / (2.0 * M_PI));
     P->ghost_full = 1;
     P->wall_r2 = -1.0f;
-    if (G > 0 && d_min > 0) {
-        const double arg = h / std::sqrt(d_min * R);
-        if (arg < 1.0) {
-            const double dphi = 2.0 * std::asin(arg);
-            const int K = (int)std::ceil(dphi * G / (2.0 * M_PI)) + 2;
-            if (2 * K + 1 < G) {
-                P->ghost_full = 0;
-                P->ghost_K = K;
-                P->wall_r2 = std::nextafter((float)(d_min * d_min), 0.0f);
-            }
-        }
-    }
+    P->wall1_r2 = -1.0f;
+    auto window = [&](double support, int* K, float* wall) {
+        const double d_min = R - support - 1e-3 * h;
+        if (!(G > 0 && d_min > 0)) return false;
+        const double arg = support / (2.0 * std::sqrt(d_min * R));
+        if (!(arg < 1.0)) return false;
+        const double dphi = 2.0 * std::asin(arg);
+        *K = (int)std::ceil(dphi * G / (2.0 * M_PI)) + 2;
+        *wall = std::nextafter((float)(d_min * d_min), 0.0f);
+        return 2 * *K + 1 < G;
+    };
+    if (window(2.0 * h, &P->ghost_K, &P->wall_r2) && window(h, &P->ghost_K1, &P->wall1_r2))
+        P->ghost_full = 0;
     return true;
 }
 
@@ -164,7 +166,7 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     put(d.ghost_b, (size_t)std::max(P.G, 1) * 16);
     put(d.body, (size_t)P.B * 48);
     put(d.u_cur, (size_t)P.B * 12);
-    put(d.part, (size_t)P.B * P.ntile * 32);
+    put(d.part, (size_t)P.B * P.npart * 32);
     put(d.rs, (size_t)P.B * sizeof(RolloutState));
     put(d.geom, (size_t)P.B * sizeof(Geom));
     put(d.xfer, (size_t)std::max(P.N, 1) * 16);

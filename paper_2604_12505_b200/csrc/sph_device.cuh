@@ -36,7 +36,8 @@ struct DevParams {
     int N, G, B;            // fluid particles / ghosts per rollout, rollouts
     int nx, ncell;          // square cell grid: nx * nx cells per rollout
     int ntile, nscan;       // CTAs per rollout (particle kernels, scan kernels)
-    int ghost_K, ghost_full;
+    int npart;              // per-warp body partials per rollout = ntile * TILE / 32
+    int ghost_K, ghost_K1, ghost_full;   // ghost windows for support 2h (density) and h (force)
     float C, inv_C, half;   // cell side (2h + skin), 1/C, half extent of the grid
     float h, inv_h, H2, h2; // h, 1/h, (2h)^2, h^2 in float32 (predicates, reading A19)
     float RL2;              // list radius^2 = (2h + skin)^2
@@ -46,6 +47,7 @@ struct DevParams {
     float gsign2m2;         // ghost_pressure_sign * 2 m^2
     float gx, gy, dt;
     float wall_r2;          // particles with |x - r|^2 <= wall_r2 see no ghost within 2h
+    float wall1_r2;         // ... no ghost within h
     float ghost_scale;      // G / (2 pi)
     float rebuild_disp;     // rebuild when the displacement bound reaches this (< skin / 2)
     int rebin_every;
@@ -94,7 +96,7 @@ struct DevPtrs {
     double2* ghost_b;    // [G] body-frame ghost positions
     double* body;        // [B][6] r_x r_y theta rd_x rd_y thd
     float* u_cur;        // [B][3] current ZOH input
-    double4* part;       // [B][ntile] per-CTA (F_x, F_y, T, max relative speed) partials
+    double4* part;       // [B][npart] per-warp (F_x, F_y, T, max relative speed) partials
     RolloutState* rs;    // [B]
     Geom* geom;          // [B]
     float4* xfer;        // [N] canonical-order export / import staging
@@ -182,13 +184,14 @@ __device__ __forceinline__ void for_fluid_candidates(const DevParams& P, const D
 
 // Enumerate the candidate ghosts of a particle (ghost-ring lookup).  The ghosts sit uniformly
 // on the wall circle, so those within 2h of x lie in an angular window around
-// the particle's polar angle; the window half-width ghost_K is derived on the host from
-// |x - g|^2 >= 4 d R sin^2(dphi / 2) with d >= sqrt(wall_r2).  Exact predicates follow.
+// the particle's polar angle; the window half-width K (ghost_K for support 2h, ghost_K1 for
+// support h) is derived on the host from |x - g|^2 >= 4 d R sin^2(dphi / 2) with
+// d >= sqrt(wall_r2).  Exact predicates follow.
 template <class F>
 __device__ __forceinline__ void for_ghost_candidates(const DevParams& P, const Geom& gm,
-                                                     float2 x, F&& f) {
+                                                     float2 x, int K, float wall_r2, F&& f) {
     float rx = x.x - gm.rx, ry = x.y - gm.ry;
-    if (rx * rx + ry * ry <= P.wall_r2) return;
+    if (rx * rx + ry * ry <= wall_r2) return;
     if (P.ghost_full) {
         for (int g = 0; g < P.G; ++g) f(g);
         return;
@@ -196,9 +199,9 @@ __device__ __forceinline__ void for_ghost_candidates(const DevParams& P, const G
     float phi = atan2f(ry, rx) - gm.th;
     int j0 = __float2int_rn(phi * P.ghost_scale) % P.G;
     if (j0 < 0) j0 += P.G;
-    int g = j0 - P.ghost_K;
+    int g = j0 - K;
     if (g < 0) g += P.G;
-    for (int t = 0; t < 2 * P.ghost_K + 1; ++t) {
+    for (int t = 0; t < 2 * K + 1; ++t) {
         f(g);
         if (++g == P.G) g = 0;
     }

@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D) {
     const Geom gm = D.geom[b];
     const float4* gst = D.gst + (size_t)b * P.G;
     const float2* glo = D.glo + (size_t)b * P.G;
-    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), [&](int g) {
+    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), P.ghost_K, P.wall_r2, [&](int g) {
         const float4 xg = __ldg(gst + g);
         const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
         if (dist2(dx, dy) < P.H2) {
@@ -332,10 +332,10 @@ __device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2
     sy += s * dy;
 }
 
-__global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float damping) {
+__global__ void __launch_bounds__(TILE, 5) k_force(DevParams P, DevPtrs D, float damping) {
     const int b = blockIdx.y;
     RolloutState* rs = D.rs + b;
-    if (rs->frozen) return;   // CTA-uniform
+    if (rs->frozen) return;   // CTA-uniform (before any warp-level collective)
     const int i = blockIdx.x * TILE + threadIdx.x;
     const size_t o = (size_t)b * P.N;
     const int cur = rs->sp ^ rs->need_rebin;
@@ -373,7 +373,9 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
         const float4* gst = D.gst + (size_t)b * P.G;
         const float2* glo = D.glo + (size_t)b * P.G;
         const float2* garm = D.garm + (size_t)b * P.G;
-        for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), [&](int g) {
+        const float cp = P.gsign2m2 * ai.y;                    // wall pressure coefficient
+        const float cvb = __fdividef(P.m2 * P.beta, ai.x);      // m^2 beta / rho_i
+        for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), P.ghost_K1, P.wall1_r2, [&](int g) {
             const float4 xg = __ldg(gst + g);
             float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
             if (dist2(dx, dy) < P.h2) {
@@ -382,12 +384,11 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
                 dy -= lo.y;
                 const float r2 = dx * dx + dy * dy;
                 if (!(r2 > 0.0f)) return;
-                const float r = sqrtf(r2);
-                const float hr = P.h - r;
-                const float gw = P.dws3 * hr * hr / r;
+                const float rs = rsqrtf(r2);
+                const float hr = P.h - r2 * rs;
+                const float gw = P.dws3 * hr * hr * rs;
                 const float vr = (xi.z - xg.z) * dx + (xi.w - xg.w) * dy;
-                const float cp = P.gsign2m2 * ai.y;
-                const float cv = P.m2 * P.beta / ai.x * fminf(vr, 0.0f) / (r2 + P.eps_h2);
+                const float cv = __fdividef(cvb * fminf(vr, 0.0f), r2 + P.eps_h2);
                 const float c = (cp + cv) * gw;
                 const float Gx = c * dx, Gy = c * dy;
                 gxs += Gx;
@@ -416,7 +417,8 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
             fabsf(xn.w) > 1e9f)
             set_status(rs, finite ? 2 : 1, (int)D.id[rs->ip ^ rs->need_rebin][o + i]);
     }
-    // body partials: warp butterfly (deterministic), then warps in fixed order in fp64
+    // body partials: warp butterfly (deterministic order), one fp64 partial per warp written
+    // straight to global memory (no CTA barrier: warps finish independently)
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         fbx += __shfl_xor_sync(0xffffffffu, fbx, d);
@@ -424,20 +426,9 @@ __global__ void __launch_bounds__(TILE) k_force(DevParams P, DevPtrs D, float da
         tq += __shfl_xor_sync(0xffffffffu, tq, d);
         vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
     }
-    __shared__ double4 wsum[TILE / 32];
     if ((threadIdx.x & 31) == 0)
-        wsum[threadIdx.x >> 5] = make_double4(fbx, fby, tq, vmax);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double4 s = wsum[0];
-        for (int w = 1; w < TILE / 32; ++w) {
-            s.x += wsum[w].x;
-            s.y += wsum[w].y;
-            s.z += wsum[w].z;
-            s.w = fmax(s.w, wsum[w].w);
-        }
-        D.part[(size_t)b * P.ntile + blockIdx.x] = s;
-    }
+        D.part[(size_t)b * P.npart + blockIdx.x * (TILE / 32) + (threadIdx.x >> 5)] =
+            make_double4(fbx, fby, tq, vmax);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -475,8 +466,8 @@ __global__ void __launch_bounds__(BODY_T) k_body(DevParams P, DevPtrs D, int pin
     __syncthreads();
     if (sdead) return;
     double4 s = make_double4(0, 0, 0, 0);
-    for (int t = threadIdx.x; t < P.ntile; t += BODY_T) {
-        const double4 q = D.part[(size_t)b * P.ntile + t];
+    for (int t = threadIdx.x; t < P.npart; t += BODY_T) {
+        const double4 q = D.part[(size_t)b * P.npart + t];
         s.x += q.x;
         s.y += q.y;
         s.z += q.z;
@@ -639,7 +630,7 @@ __global__ void k_debug_neighbours(DevParams P, DevPtrs D, int b) {
     });
     const Geom gm = D.geom[b];
     const float4* gst = D.gst + (size_t)b * P.G;
-    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), [&](int g) {
+    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), P.ghost_K, P.wall_r2, [&](int g) {
         const float4 xg = gst[g];
         const float r2 = dist2(__fsub_rn(xi.x, xg.x), __fsub_rn(xi.y, xg.y));
         if (r2 < P.H2) {
