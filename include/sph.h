@@ -80,6 +80,9 @@ typedef struct {
     int substeps_per_sample;  /* n_sub = T_s / dt >= 1 (multi-rate)    */
     int rebin_every;          /* 1 = every substep, 0 = adaptive with skin     */
     double skin;              /* >= 0, only used when rebin_every == 0         */
+    int rebuild_path;         /* 0 auto; 1 one CTA per rebuilding rollout in shared memory
+                                 (needs (n_cells+1)*4 + 10*n_fluid bytes <= 200 KB, else
+                                 SPH_EINVAL); 2 grid-wide multi-kernel counting sort        */
 } sph_time_params;
 
 /* PD attitude law tau_k = Kp (theta_ref_k - theta_k) - Kd thetadot_k, ZOH. */
@@ -160,9 +163,10 @@ sph_status sph_debug_neighbours(sph_ctx* ctx, int rollout, int64_t* nf_off, int3
  * u held and writes the average device time per launch in ms of each kernel into
  * ms[SPH_NUM_TIMERS] (order: see SPH_TIMER_* below). */
 enum {
-    SPH_TIMER_HASH = 0, SPH_TIMER_SCAN = 1, SPH_TIMER_SCATTER = 2, SPH_TIMER_CELLSORT = 3,
-    SPH_TIMER_GATHER = 4, SPH_TIMER_NLIST = 5, SPH_TIMER_DENSITY = 6, SPH_TIMER_FORCE = 7,
-    SPH_TIMER_BODY = 8, SPH_TIMER_SUBSTEP = 9, SPH_NUM_TIMERS = 10
+    SPH_TIMER_REBUILD = 0,  /* cell sort + neighbour lists of the rollouts that need it (small
+                               path: also their densities)                                 */
+    SPH_TIMER_DENSITY = 1, SPH_TIMER_FORCE = 2, SPH_TIMER_BODY = 3, SPH_TIMER_SUBSTEP = 4,
+    SPH_NUM_TIMERS = 5
 };
 sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms);
 

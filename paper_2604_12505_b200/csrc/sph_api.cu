@@ -30,6 +30,12 @@ struct sph_ctx {
     size_t stage_bytes = 0;
     int* dbg_buf = nullptr;
     int n_sub = 1;
+    // small-rollout rebuild path: k_rebuild_small on a forked branch (side stream + events)
+    bool small = false;
+    size_t small_smem = 0;
+    int small_grid = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 static std::string g_init_err;
@@ -67,6 +73,8 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     if (!(tp->dt > 0) || tp->substeps_per_sample < 1 || tp->rebin_every < 0 || tp->rebin_every > 1 ||
         !(tp->skin >= 0))
         return *why = "invalid time parameters (dt > 0, substeps_per_sample >= 1, rebin_every in {0,1}, skin >= 0)", false;
+    if (tp->rebuild_path < 0 || tp->rebuild_path > 2)
+        return *why = "rebuild_path must be 0 (auto), 1 (per-rollout CTA) or 2 (multi-kernel)", false;
     if (tp->rebin_every == 0 && !(tp->skin > 0))
         return *why = "adaptive rebinning (rebin_every = 0) needs skin > 0", false;
     const double h = fp->h, R = bp->tank_radius;
@@ -171,6 +179,8 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     put(d.geom, (size_t)P.B * sizeof(Geom));
     put(d.xfer, (size_t)std::max(P.N, 1) * 16);
     put(d.xrho, (size_t)std::max(P.N, 1) * 4);
+    put(d.rlist, (size_t)P.B * 4);
+    put(d.rcount, 4);
     d.dbg_cnt = nullptr;
     d.dbg_idx = nullptr;
     if (D) *D = d;
@@ -194,17 +204,38 @@ static void launch_rebin(sph_ctx* ctx) {
     k_nlist<<<gp, TILE, 0, s>>>(P, ctx->D);
 }
 
+// Rebuild (only rollouts that need it) + densities.  Small path: the plan kernel builds the
+// work list, then k_rebuild_small (one CTA per rebuilding rollout, side stream) runs
+// concurrently with k_density for every other rollout (fork/join via events; captured into
+// the tick graph as two parallel branches).
+static void launch_rebuild_and_density(sph_ctx* ctx) {
+    const DevParams& P = ctx->P;
+    cudaStream_t s = ctx->stream;
+    dim3 gp(P.ntile, P.B);
+    if (ctx->small) {
+        k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D);
+        cudaEventRecord(ctx->ev_fork, s);
+        cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+        k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
+        cudaEventRecord(ctx->ev_join, ctx->side);
+        k_density<<<gp, TILE, 0, s>>>(P, ctx->D, 1);
+        cudaStreamWaitEvent(s, ctx->ev_join, 0);
+    } else {
+        launch_rebin(ctx);
+        k_density<<<gp, TILE, 0, s>>>(P, ctx->D, 0);
+    }
+}
+
 static void launch_substep(sph_ctx* ctx, float damping, int pin) {
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
-    launch_rebin(ctx);
-    k_density<<<gp, TILE, 0, s>>>(P, ctx->D);
+    launch_rebuild_and_density(ctx);
     k_force<<<gp, TILE, 0, s>>>(P, ctx->D, damping);
     k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, pin, ctx->ghost_angle0);
 }
 
-static const int kLaunchesPerSubstep = 11;
+static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? 5 : 11; }
 
 static sph_status check_launch(sph_ctx* ctx) {
     cudaError_t e = cudaGetLastError();
@@ -297,6 +328,34 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
         return SPH_ECUDA;
     };
     cudaError_t e;
+    // rebuild path: one CTA per rebuilding rollout when its cell table and sort scratch fit in
+    // shared memory (rebuild_path 0 = auto, 1 = force per-rollout CTA, 2 = force multi-kernel)
+    {
+        const size_t smem = (size_t)(P.ncell + 1) * 4 + (size_t)P.N * 10 + 16;
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const bool fits = P.N > 0 && smem <= 200 * 1024;
+        bool want = tp->rebuild_path == 1 || (tp->rebuild_path == 0 && fits);
+        if (want && !fits) {
+            sph_destroy(ctx);
+            return fail(nullptr, SPH_EINVAL, "rebuild_path = 1 but the rollout does not fit in shared memory");
+        }
+        if (want && cudaFuncSetAttribute(k_rebuild_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem) != cudaSuccess) {
+            cudaGetLastError();
+            want = false;
+        }
+        if (want) {
+            ctx->small = true;
+            ctx->small_smem = smem;
+            ctx->small_grid = std::max(1, std::min(P.B, nsm));
+            if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+                (e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess)
+                return bail("side stream", e);
+        }
+    }
     if ((e = cudaMemsetAsync(d_workspace, 0, total, s)) != cudaSuccess) return bail("memset", e);
     std::vector<double2> gb(std::max(n_ghost, 1));
     for (int g = 0; g < n_ghost; ++g) gb[g] = make_double2(ghost_body_xy[2 * g], ghost_body_xy[2 * g + 1]);
@@ -557,42 +616,38 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
     if (!ctx || !ms || n_substeps < 1) return SPH_EINVAL;
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
-    cudaEvent_t ev[11];
+    cudaEvent_t ev[5];
     for (auto& e : ev) CK(cudaEventCreate(&e));
     double acc[SPH_NUM_TIMERS] = {0};
-    dim3 gp(P.ntile, P.B), gs(P.nscan, P.B), gc((P.ncell + TILE - 1) / TILE, P.B);
+    dim3 gp(P.ntile, P.B);
+    // Sequential on the context stream (no fork), so every kernel is timed alone.  The rebuild
+    // timer covers the plan + k_rebuild_small (small path; these also compute the rebuilt
+    // rollouts' densities) or the eight rebuild kernels (multi-kernel path).
     for (int it = 0; it < n_substeps; ++it) {
         cudaEventRecord(ev[0], s);
-        k_hash<<<gp, TILE, 0, s>>>(P, ctx->D);
+        if (ctx->small) {
+            k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D);
+            k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
+        } else {
+            launch_rebin(ctx);
+        }
         cudaEventRecord(ev[1], s);
-        k_scan_reduce<<<gs, SCAN_T, 0, s>>>(P, ctx->D);
-        k_scan_tiles<<<P.B, SCAN_T, 0, s>>>(P, ctx->D);
-        k_scan_down<<<gs, SCAN_T, 0, s>>>(P, ctx->D);
+        k_density<<<gp, TILE, 0, s>>>(P, ctx->D, ctx->small ? 1 : 0);
         cudaEventRecord(ev[2], s);
-        k_scatter<<<gp, TILE, 0, s>>>(P, ctx->D);
-        cudaEventRecord(ev[3], s);
-        k_cellsort<<<gc, TILE, 0, s>>>(P, ctx->D);
-        cudaEventRecord(ev[4], s);
-        k_gather<<<gp, TILE, 0, s>>>(P, ctx->D);
-        cudaEventRecord(ev[5], s);
-        k_nlist<<<gp, TILE, 0, s>>>(P, ctx->D);
-        cudaEventRecord(ev[6], s);
-        k_density<<<gp, TILE, 0, s>>>(P, ctx->D);
-        cudaEventRecord(ev[7], s);
         k_force<<<gp, TILE, 0, s>>>(P, ctx->D, 1.0f);
-        cudaEventRecord(ev[8], s);
+        cudaEventRecord(ev[3], s);
         k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
-        cudaEventRecord(ev[9], s);
+        cudaEventRecord(ev[4], s);
         sph_status st = check_launch(ctx);
         if (st) return st;
-        CK(cudaEventSynchronize(ev[9]));
-        for (int t = 0; t < 9; ++t) {
+        CK(cudaEventSynchronize(ev[4]));
+        for (int t = 0; t < 4; ++t) {
             float m;
             CK(cudaEventElapsedTime(&m, ev[t], ev[t + 1]));
             acc[t] += m;
         }
         float m;
-        CK(cudaEventElapsedTime(&m, ev[0], ev[9]));
+        CK(cudaEventElapsedTime(&m, ev[0], ev[4]));
         acc[SPH_TIMER_SUBSTEP] += m;
     }
     for (int t = 0; t < SPH_NUM_TIMERS; ++t) ms[t] = (float)(acc[t] / n_substeps);
@@ -600,7 +655,7 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
     return SPH_OK;
 }
 
-int sph_launches_per_substep(const sph_ctx* ctx) { return ctx ? kLaunchesPerSubstep : 0; }
+int sph_launches_per_substep(const sph_ctx* ctx) { return ctx ? launches_per_substep(ctx) : 0; }
 
 sph_status sph_get_counters(sph_ctx* ctx, int64_t* steps, int32_t* rebuilds) {
     if (!ctx) return SPH_EINVAL;
@@ -630,6 +685,9 @@ void sph_destroy(sph_ctx* ctx) {
     if (ctx->tick_graph) cudaGraphExecDestroy(ctx->tick_graph);
     if (ctx->stage) cudaFree(ctx->stage);
     if (ctx->dbg_buf) cudaFree(ctx->dbg_buf);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

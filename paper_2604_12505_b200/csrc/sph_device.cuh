@@ -101,6 +101,8 @@ struct DevPtrs {
     Geom* geom;          // [B]
     float4* xfer;        // [N] canonical-order export / import staging
     float* xrho;         // [N]
+    int* rlist;          // [B] rollouts that rebuild this substep (k_rebuild_plan)
+    int* rcount;         // [1] their number
     int* dbg_cnt;        // [3][N] debug neighbour counts
     int* dbg_idx;        // [3][N][DBG_CAP] debug neighbour ids
 };
@@ -158,7 +160,7 @@ __device__ __forceinline__ void for_cell_candidates(const DevParams& P, const ui
 #pragma unroll
     for (int dy = -1; dy <= 1; ++dy) {
         int c0 = (cy + dy) * P.nx + cx - 1;
-        uint32_t j0 = __ldg(cs + c0), j1 = __ldg(cs + c0 + 3);
+        uint32_t j0 = cs[c0], j1 = cs[c0 + 3];   // global or shared table
         for (uint32_t j = j0; j < j1; ++j) f(j);
     }
 }

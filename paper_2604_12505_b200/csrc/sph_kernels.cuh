@@ -210,20 +210,147 @@ __global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) {
 // candidates).  Unused entries of the last quad are 0.  Lists longer than KMAX, or offsets
 // outside int16, mark the particle for the cell-scan fallback.
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
+__global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D);
+// ---------------------------------------------------------------------------------------
+// Density + EOS (Eq. density_update P:180-182, Eq. EOS P:149-151, cubic kernel P:268-271):
+//   rho_i = m ( sum_{j : r_ij < 2h} W_cb(r_ij)  [self included]  + gamma1 sum_g W_cb(r_ig) )
+//   P_i = k (rho_i - rho0);  stores (rho_i, P_i / rho_i^2).
+// The list is walked four candidates at a time: one 8-byte offset load, four independent
+// 16-byte state loads, then branch-free masked arithmetic.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ float w_masked(const DevParams& P, float4 xi, float4 xj, bool valid) {
+    const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+    const float r = r2 > 0.0f ? r2 * rsqrtf(r2) : 0.0f;
+    const float w = wcb_poly(r * P.inv_h);
+    return (valid && r2 < P.H2) ? w : 0.0f;
+}
+
+// Load through the read-only path unless the data was written earlier in the same kernel.
+template <bool NC, class T>
+__device__ __forceinline__ T ld(const T* p) {
+    if constexpr (NC) return __ldg(p);
+    else return *p;
+}
+
+// Density + EOS of slot i of rollout b (state pv = the rollout's current buffer).
+template <bool NC>
+__device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D, int b, int i,
+                                           const float4* __restrict__ pv) {
+    const size_t o = (size_t)b * P.N;
+    const float4 xi = ld<NC>(pv + i);
+    float wf = 4.0f;   // self term W_cb(0) (P:135 "all particles"): (2-0)^3 - 4 (1-0)^3 = 4
+    const int n = ld<NC>(D.ncnt + o + i);
+    if (n != NL_OVERFLOW) {
+        const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
+        for (int k = 0; k < n; k += 4) {
+            const uint2 w = ld<NC>(nq);
+            nq += P.N;
+            const float4 x0 = ld<NC>(pv + i + quad_offset(w, 0));
+            const float4 x1 = ld<NC>(pv + i + quad_offset(w, 1));
+            const float4 x2 = ld<NC>(pv + i + quad_offset(w, 2));
+            const float4 x3 = ld<NC>(pv + i + quad_offset(w, 3));
+            wf += w_masked(P, xi, x0, k < n) + w_masked(P, xi, x1, k + 1 < n) +
+                  w_masked(P, xi, x2, k + 2 < n) + w_masked(P, xi, x3, k + 3 < n);
+        }
+    } else {
+        for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), ld<NC>(D.skey + o + i),
+                            [&](uint32_t j) { wf += w_masked(P, xi, ld<NC>(pv + j), j != (uint32_t)i); });
+    }
+    float wg = 0.0f;
+    const Geom gm = D.geom[b];
+    const float4* gst = D.gst + (size_t)b * P.G;
+    const float2* glo = D.glo + (size_t)b * P.G;
+    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), P.ghost_K, P.wall_r2, [&](int g) {
+        const float4 xg = __ldg(gst + g);
+        const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
+        if (dist2(dx, dy) < P.H2) {
+            const float2 lo = __ldg(glo + g);
+            const float ex = dx - lo.x, ey = dy - lo.y;
+            const float r2 = ex * ex + ey * ey;
+            wg += wcb_poly(r2 > 0.0f ? r2 * rsqrtf(r2) * P.inv_h : 0.0f);
+        }
+    });
+    const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
+    const float pr = P.k * (rho - P.rho0);
+    D.aux[o + i] = make_float2(rho, __fdividef(pr, rho * rho));
+}
+
+// skip_rebuilding = 1 when rollouts that rebuild this substep get their densities from
+// k_rebuild_small (which runs concurrently on another branch of the graph).
+__global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D, int skip_rebuilding) {
     const int b = blockIdx.y;
     const RolloutState* rs = D.rs + b;
-    if (rs->frozen || !rs->need_rebin) return;
+    if (rs->frozen || (skip_rebuilding && rs->need_rebin)) return;
     const int i = blockIdx.x * TILE + threadIdx.x;
     if (i >= P.N) return;
+    density_at<true>(P, D, b, i, D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N);
+}
+
+// ---------------------------------------------------------------------------------------
+// Small-rollout rebuild path (N and the cell grid fit in shared memory, e.g. C1, C2, C3):
+//   k_rebuild_plan   one CTA compacts the rollouts that need a rebuild into a work list;
+//   k_rebuild_small  persistent CTAs, ONE CTA PER LISTED ROLLOUT: counting sort by cell with
+//                    shared-memory atomics, block scan, per-cell canonical-id order, gather,
+//                    neighbour lists and the densities of the rollout -- all in shared memory,
+//                    no grid-wide phases.  It runs concurrently with k_density for the other
+//                    rollouts, so a rebuild costs one SM for tens of microseconds instead of
+//                    eight grid-wide launches.
+// ---------------------------------------------------------------------------------------
+constexpr int RB_T = 1024;
+
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t v, uint32_t* total,
+                                                      uint32_t* warp_tot /* [NT/32] smem */) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t t = lane < NT / 32 ? warp_tot[lane] : 0u;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, t, d);
+            if (lane >= d) t += y;
+        }
+        if (lane < NT / 32) warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const uint32_t base = w ? warp_tot[w - 1] : 0u;
+    if (total) *total = warp_tot[NT / 32 - 1];
+    __syncthreads();   // warp_tot may be reused by the caller's next scan
+    return base + x - v;
+}
+
+__global__ void __launch_bounds__(RB_T) k_rebuild_plan(DevParams P, DevPtrs D) {
+    __shared__ uint32_t wt[RB_T / 32];
+    uint32_t base = 0;
+    for (int b0 = 0; b0 < P.B; b0 += RB_T) {
+        const int b = b0 + threadIdx.x;
+        const uint32_t f = (b < P.B && D.rs[b].need_rebin && !D.rs[b].frozen) ? 1u : 0u;
+        uint32_t tot;
+        const uint32_t pos = base + block_excl_scan_t<RB_T>(f, &tot, wt);
+        if (f) D.rlist[pos] = b;
+        base += tot;
+    }
+    if (threadIdx.x == 0) *D.rcount = (int)base;
+}
+
+// neighbour candidate list of slot i (see k_nlist) from a given cell-start table
+template <bool NC>
+__device__ __forceinline__ void build_list(const DevParams& P, const DevPtrs& D, int b, int i,
+                                           const float4* pv, const uint32_t* cs, uint32_t cell) {
     const size_t o = (size_t)b * P.N;
-    const float4* __restrict__ pv = D.pv[rs->sp ^ 1] + o;   // the freshly gathered buffer
-    const float4 xi = pv[i];
+    const float4 xi = ld<NC>(pv + i);
     uint2* nq = D.nbr + (size_t)b * KQ * P.N + i;
     int n = 0;
     uint32_t acc0 = 0u, acc1 = 0u;
-    for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
-        const float4 xj = __ldg(pv + j);
+    for_cell_candidates(P, cs, cell, [&](uint32_t j) {
+        const float4 xj = ld<NC>(pv + j);
         const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
         if (j != (uint32_t)i && r2 < P.RL2 && n != NL_OVERFLOW) {
             const int off = (int)j - i;
@@ -245,65 +372,106 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
     D.ncnt[o + i] = (uint8_t)n;
 }
 
-// ---------------------------------------------------------------------------------------
-// Density + EOS (Eq. density_update P:180-182, Eq. EOS P:149-151, cubic kernel P:268-271):
-//   rho_i = m ( sum_{j : r_ij < 2h} W_cb(r_ij)  [self included]  + gamma1 sum_g W_cb(r_ig) )
-//   P_i = k (rho_i - rho0);  stores (rho_i, P_i / rho_i^2).
-// The list is walked four candidates at a time: one 8-byte offset load, four independent
-// 16-byte state loads, then branch-free masked arithmetic.
-// ---------------------------------------------------------------------------------------
-__device__ __forceinline__ float w_masked(const DevParams& P, float4 xi, float4 xj, bool valid) {
-    const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-    const float r = r2 > 0.0f ? r2 * rsqrtf(r2) : 0.0f;
-    const float w = wcb_poly(r * P.inv_h);
-    return (valid && r2 < P.H2) ? w : 0.0f;
-}
-
-__global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D) {
+__global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
     const int b = blockIdx.y;
     const RolloutState* rs = D.rs + b;
-    if (rs->frozen) return;
+    if (rs->frozen || !rs->need_rebin) return;
     const int i = blockIdx.x * TILE + threadIdx.x;
     if (i >= P.N) return;
     const size_t o = (size_t)b * P.N;
-    const float4* __restrict__ pv = D.pv[rs->sp ^ rs->need_rebin] + o;
-    const float4 xi = pv[i];
-    float wf = 4.0f;   // self term W_cb(0) (P:135 "all particles"): (2-0)^3 - 4 (1-0)^3 = 4
-    const int n = D.ncnt[o + i];
-    if (n != NL_OVERFLOW) {
-        const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
-        for (int k = 0; k < n; k += 4) {
-            const uint2 w = __ldg(nq);
-            nq += P.N;
-            const float4 x0 = __ldg(pv + i + quad_offset(w, 0));
-            const float4 x1 = __ldg(pv + i + quad_offset(w, 1));
-            const float4 x2 = __ldg(pv + i + quad_offset(w, 2));
-            const float4 x3 = __ldg(pv + i + quad_offset(w, 3));
-            wf += w_masked(P, xi, x0, k < n) + w_masked(P, xi, x1, k + 1 < n) +
-                  w_masked(P, xi, x2, k + 2 < n) + w_masked(P, xi, x3, k + 3 < n);
+    build_list<true>(P, D, b, i, D.pv[rs->sp ^ 1] + o, D.cstart + (size_t)b * (P.ncell + 1),
+                     D.skey[o + i]);
+}
+
+// dynamic shared memory: start[ncell + 1] u32 | key[N] u32 | perm[N] u32 | rank[N] u16
+__global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) {
+    extern __shared__ uint32_t smem[];
+    __shared__ uint32_t wt[RB_T / 32];
+    uint32_t* s_start = smem;
+    uint32_t* s_key = s_start + (P.ncell + 1);
+    uint32_t* s_perm = s_key + P.N;
+    uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_perm + P.N);
+    const int count = *D.rcount;
+    const int T = RB_T, tid = threadIdx.x;
+    for (int w = blockIdx.x; w < count; w += gridDim.x) {
+        const int b = D.rlist[w];
+        RolloutState* rs = D.rs + b;
+        const int sp = rs->sp, ip = rs->ip;
+        const size_t o = (size_t)b * P.N;
+        const float4* pv0 = D.pv[sp] + o;
+        float4* pv1 = D.pv[sp ^ 1] + o;
+        const uint32_t* id0 = D.id[ip] + o;
+        uint32_t* id1 = D.id[ip ^ 1] + o;
+        for (int c = tid; c <= P.ncell; c += T) s_start[c] = 0u;
+        __syncthreads();
+        // 1. cell key + rank (shared-memory atomics)
+        const Geom gm = D.geom[b];
+        const float ox = __fsub_rn(gm.rx, P.half), oy = __fsub_rn(gm.ry, P.half);
+        for (int i = tid; i < P.N; i += T) {
+            const float4 x = pv0[i];
+            int cx = cell_coord(x.x, ox, P.inv_C), cy = cell_coord(x.y, oy, P.inv_C);
+            if (cx < 1 || cx > P.nx - 2 || cy < 1 || cy > P.nx - 2) {
+                set_status(rs, 3, (int)id0[i]);
+                cx = min(max(cx, 1), P.nx - 2);
+                cy = min(max(cy, 1), P.nx - 2);
+            }
+            const uint32_t c = (uint32_t)(cy * P.nx + cx);
+            s_key[i] = c;
+            s_rank[i] = (uint16_t)atomicAdd(s_start + c, 1u);
         }
-    } else {
-        for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
-            wf += w_masked(P, xi, __ldg(pv + j), j != (uint32_t)i);
-        });
+        __syncthreads();
+        // 2. exclusive scan of the counts -> cell starts (smem and global table)
+        {
+            const int per = (P.ncell + 1 + T - 1) / T;
+            const int c0 = tid * per;
+            uint32_t s = 0;
+            for (int k = 0; k < per; ++k)
+                if (c0 + k <= P.ncell) s += s_start[c0 + k];
+            uint32_t run = block_excl_scan_t<RB_T>(s, nullptr, wt);
+            uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
+            for (int k = 0; k < per; ++k) {
+                const int c = c0 + k;
+                if (c <= P.ncell) {
+                    const uint32_t v = s_start[c];
+                    s_start[c] = run;
+                    cs[c] = run;
+                    run += v;
+                }
+            }
+        }
+        __syncthreads();
+        // 3. scatter
+        for (int i = tid; i < P.N; i += T) s_perm[s_start[s_key[i]] + s_rank[i]] = (uint32_t)i;
+        __syncthreads();
+        // 4. canonical-id order inside each cell (reading A20)
+        for (int c = tid; c < P.ncell; c += T) {
+            const int s = (int)s_start[c], e = (int)s_start[c + 1];
+            for (int t = s + 1; t < e; ++t) {
+                const uint32_t ss = s_perm[t], ks = id0[ss];
+                int u = t - 1;
+                while (u >= s && id0[s_perm[u]] > ks) {
+                    s_perm[u + 1] = s_perm[u];
+                    --u;
+                }
+                s_perm[u + 1] = ss;
+            }
+        }
+        __syncthreads();
+        // 5. gather into cell order
+        for (int d = tid; d < P.N; d += T) {
+            const uint32_t src = s_perm[d];
+            pv1[d] = pv0[src];
+            id1[d] = id0[src];
+            D.skey[o + d] = s_key[src];
+        }
+        __syncthreads();
+        // 6. neighbour lists (cell starts from shared memory, fresh state: coherent loads)
+        for (int i = tid; i < P.N; i += T) build_list<false>(P, D, b, i, pv1, s_start, s_key[s_perm[i]]);
+        __syncthreads();
+        // 7. densities of the rebuilt rollout
+        for (int i = tid; i < P.N; i += T) density_at<false>(P, D, b, i, pv1);
+        __syncthreads();
     }
-    float wg = 0.0f;
-    const Geom gm = D.geom[b];
-    const float4* gst = D.gst + (size_t)b * P.G;
-    const float2* glo = D.glo + (size_t)b * P.G;
-    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), P.ghost_K, P.wall_r2, [&](int g) {
-        const float4 xg = __ldg(gst + g);
-        const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
-        if (dist2(dx, dy) < P.H2) {
-            const float2 lo = __ldg(glo + g);
-            const float ex = dx - lo.x, ey = dy - lo.y;
-            const float r2 = ex * ex + ey * ey;
-            wg += wcb_poly(r2 > 0.0f ? r2 * rsqrtf(r2) * P.inv_h : 0.0f);
-        }
-    });
-    const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
-    const float pr = P.k * (rho - P.rho0);
-    D.aux[o + i] = make_float2(rho, __fdividef(pr, rho * rho));
 }
 
 // ---------------------------------------------------------------------------------------

@@ -42,15 +42,18 @@ def _rel(a, b, floor=0.0):
 # ---------------------------------------------------------------------------------------
 # Cells and neighbour sets: bit-exact (reading A19)
 # ---------------------------------------------------------------------------------------
-@pytest.mark.parametrize("case", ["rest", "moved_rotated", "after_200_steps", "adaptive_grid"])
+@pytest.mark.parametrize("case", ["rest", "moved_rotated", "after_200_steps", "adaptive_grid",
+                                  "after_200_steps_multikernel"])
 def test_cells_and_neighbour_sets_bit_exact(case):
     body = [0.3, -0.2, 0.7, 0.01, -0.02, 0.05] if case == "moved_rotated" else None
     t = _moving_tank(body=body)
     kw = dict(rebin_every=0, skin=0.2 * t.params.h) if case == "adaptive_grid" else {}
+    if case.endswith("multikernel"):
+        kw = dict(rebin_every=0, skin=0.3 * t.params.h, rebuild_path=2)
     ctx = _ctx(t, **kw)
     if body is not None:
         ctx.set_body_state(np.array([body]))
-    if case in ("after_200_steps", "adaptive_grid"):
+    if case.startswith("after_200_steps") or case == "adaptive_grid":
         ctx.step(np.array([[5.0, 2.0, 1.0]], np.float32), 200)
     pv = ctx.get_particles(0)
     p32 = np.ascontiguousarray(pv[:, :2])
@@ -87,12 +90,12 @@ def test_ghost_world_state_matches_oracle():
 # ---------------------------------------------------------------------------------------
 # One-step parity (1e-5, SURVEY 8(c) normalisation)
 # ---------------------------------------------------------------------------------------
-@pytest.mark.parametrize("ell,body", [(1.0, None), (1.0, [0.3, -0.2, 0.7, 0.01, -0.02, 0.05]),
-                                      (4.0, None)])
-def test_one_step_parity(ell, body):
+@pytest.mark.parametrize("ell,body,path", [(1.0, None, 0), (1.0, [0.3, -0.2, 0.7, 0.01, -0.02, 0.05], 0),
+                                           (4.0, None, 0), (4.0, None, 2)])
+def test_one_step_parity(ell, body, path):
     t = _moving_tank(ell=ell, body=body)
     u = (5.0, 2.0, 1.0)
-    ctx = _ctx(t)
+    ctx = _ctx(t, rebuild_path=path)
     if body is not None:
         ctx.set_body_state(np.array([body]))
     ctx.step(np.array([u], np.float32), 1)
@@ -123,11 +126,12 @@ def settled_c1():
     return t2.snapped()
 
 
-@pytest.mark.parametrize("rebin_every", [1, 0])
-def test_200_step_body_trajectory(settled_c1, rebin_every):
+@pytest.mark.parametrize("rebin_every,path", [(1, 0), (0, 0), (0, 2)])
+def test_200_step_body_trajectory(settled_c1, rebin_every, path):
     t = settled_c1
     u = (5.0, 2.0, 1.0)
-    kw = {} if rebin_every else dict(rebin_every=0, skin=0.2 * t.params.h)
+    kw = dict(rebuild_path=path) if rebin_every else dict(rebin_every=0, skin=0.2 * t.params.h,
+                                                         rebuild_path=path)
     ctx = _ctx(t, **kw)
     ref = O.State.from_tank(t)
     yg, yo = [], []
@@ -340,6 +344,10 @@ def test_adaptive_rebuilds_are_rare_and_results_match_every_step_mode(settled_c1
     u = si.ensemble_inputs([3, 4], K)[0]
     a = _ctx(t, B=2, rebin_every=0, skin=0.3 * t.params.h)
     ya, _ = a.rollout(u)
+    m = _ctx(t, B=2, rebin_every=0, skin=0.3 * t.params.h, rebuild_path=2)
+    ym, _ = m.rollout(u)
+    assert np.array_equal(ya, ym)     # both rebuild paths produce the same sort and lists
+    m.close()
     steps, reb = a.counters()
     assert np.all(steps == K * t.params.n_sub)
     assert np.all(reb >= 1) and np.all(reb < steps / 4)
