@@ -110,6 +110,8 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->eps_h2 = (float)(fp->eps * h * h);
     P->wcb = (float)(fp->w_cb_const / (h * h));
     P->dwcb = (float)(fp->w_cb_const / (h * h * h));
+    P->mdwcb3 = (float)(fp->mass * 3.0 * fp->w_cb_const / (h * h * h));
+    P->inv_mass = (float)(1.0 / fp->mass);
     P->dws3 = (float)(-30.0 / (M_PI * std::pow(h, 5)));
     P->gsign2m2 = (float)(fp->ghost_pressure_sign * 2.0 * fp->mass * fp->mass);
     P->gx = (float)fp->gravity[0];

@@ -44,6 +44,7 @@ struct DevParams {
     float mass, m2, rho0, k, gamma1;
     float alpha2h, beta, eps_h2;
     float wcb, dwcb, dws3;  // C/h^2, C/h^3, -30/(pi h^5)
+    float mdwcb3, inv_mass; // m * 3C/h^3 (force sums are in units of 3C/h^3), 1/m
     float gsign2m2;         // ghost_pressure_sign * 2 m^2
     float gx, gy, dt;
     float wall_r2;          // particles with |x - r|^2 <= wall_r2 see no ghost within 2h

@@ -225,6 +225,15 @@ __device__ __forceinline__ float w_masked(const DevParams& P, float4 xi, float4 
     return (valid && r2 < P.H2) ? w : 0.0f;
 }
 
+// W_cb polynomial of a list candidate (no validity mask: list padding points at the particle
+// itself and contributes exactly W(0) = 4, which the caller subtracts).
+__device__ __forceinline__ float w_list(const DevParams& P, float4 xi, float4 xj) {
+    const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+    const float r = r2 * rsqrtf(fmaxf(r2, 1e-30f));   // exactly 0 at r2 = 0
+    const float w = wcb_poly(r * P.inv_h);
+    return r2 < P.H2 ? w : 0.0f;
+}
+
 // Load through the read-only path unless the data was written earlier in the same kernel.
 template <bool NC, class T>
 __device__ __forceinline__ T ld(const T* p) {
@@ -245,13 +254,13 @@ __device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D,
         for (int k = 0; k < n; k += 4) {
             const uint2 w = ld<NC>(nq);
             nq += P.N;
-            const float4 x0 = ld<NC>(pv + i + quad_offset(w, 0));
-            const float4 x1 = ld<NC>(pv + i + quad_offset(w, 1));
-            const float4 x2 = ld<NC>(pv + i + quad_offset(w, 2));
-            const float4 x3 = ld<NC>(pv + i + quad_offset(w, 3));
-            wf += w_masked(P, xi, x0, k < n) + w_masked(P, xi, x1, k + 1 < n) +
-                  w_masked(P, xi, x2, k + 2 < n) + w_masked(P, xi, x3, k + 3 < n);
+            const float4 x0 = ld<NC>(pv + (uint32_t)(i + quad_offset(w, 0)));
+            const float4 x1 = ld<NC>(pv + (uint32_t)(i + quad_offset(w, 1)));
+            const float4 x2 = ld<NC>(pv + (uint32_t)(i + quad_offset(w, 2)));
+            const float4 x3 = ld<NC>(pv + (uint32_t)(i + quad_offset(w, 3)));
+            wf += (w_list(P, xi, x0) + w_list(P, xi, x1)) + (w_list(P, xi, x2) + w_list(P, xi, x3));
         }
+        wf -= 4.0f * (float)(((n + 3) & ~3) - n);   // padding entries (self) added W(0) = 4 each
     } else {
         for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), ld<NC>(D.skey + o + i),
                             [&](uint32_t j) { wf += w_masked(P, xi, ld<NC>(pv + j), j != (uint32_t)i); });
@@ -486,21 +495,41 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
 // reduced per CTA (warp shuffle -> fp64 per warp -> fixed order) into D.part.
 // ---------------------------------------------------------------------------------------
 // (-pressure + viscous) pair term per m^2, times r_ij, accumulated into (sx, sy).
+// The sums (sx, sy) are in units of 3C/h^3: dW/dr = (3C/h^3) d(q) with
+// d(q) = q (3q - 4) for q < 1 and -(2 - q)^2 for 1 <= q < 2 (Eq. cubicspline differentiated).
+// r2 is clamped before rsqrt, so the self pair and list padding (dx = dy = 0) and coincident
+// particles contribute exactly zero (zero gradient at r = 0, reading A8) without a mask.
 __device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2 ai, float4 xj,
-                                           float2 aj, bool valid, float& sx, float& sy) {
+                                           float2 aj, float& sx, float& sy) {
     const float dx = __fsub_rn(xi.x, xj.x), dy = __fsub_rn(xi.y, xj.y);
     const float r2 = dist2(dx, dy);
-    const float rs = rsqrtf(r2);                                   // 1 / r (inf at r = 0)
-    const float gw = P.dwcb * dwcb_poly(r2 * rs * P.inv_h) * rs;   // W'(r) / r
+    const float rs = rsqrtf(fmaxf(r2, 1e-30f));                    // 1 / r
+    const float q = r2 * rs * P.inv_h;
+    const float t = 2.0f - q;
+    const float d = q < 1.0f ? q * (3.0f * q - 4.0f) : -(t * t);
     const float vr = (xi.z - xj.z) * dx + (xi.w - xj.w) * dy;
     const float visc = __fdividef(P.alpha2h * vr, (ai.x + aj.x) * (r2 + P.eps_h2));
-    float s = (visc - (ai.y + aj.y)) * gw;
-    s = (valid && r2 < P.H2 && r2 > 0.0f) ? s : 0.0f;              // exact predicate (A19)
+    float s = (visc - (ai.y + aj.y)) * (d * rs);
+    s = r2 < P.H2 ? s : 0.0f;                                      // exact predicate (A19)
     sx += s * dx;
     sy += s * dy;
 }
 
-__global__ void __launch_bounds__(TILE, 5) k_force(DevParams P, DevPtrs D, float damping) {
+// masked variant for the cell-scan fallback (candidates may include j == i)
+__device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2 ai, float4 xj,
+                                           float2 aj, bool valid, float& sx, float& sy) {
+    float tx = 0.0f, ty = 0.0f;
+    pair_force(P, xi, ai, xj, aj, tx, ty);
+    if (valid) {
+        sx += tx;
+        sy += ty;
+    }
+}
+
+#ifndef SPH_FORCE_MINB
+#define SPH_FORCE_MINB 5
+#endif
+__global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, DevPtrs D, float damping) {
     const int b = blockIdx.y;
     RolloutState* rs = D.rs + b;
     if (rs->frozen) return;   // CTA-uniform (before any warp-level collective)
@@ -521,16 +550,18 @@ __global__ void __launch_bounds__(TILE, 5) k_force(DevParams P, DevPtrs D, float
             for (int k = 0; k < n; k += 4) {
                 const uint2 w = __ldg(nq);
                 nq += P.N;
-                const int j0 = i + quad_offset(w, 0), j1 = i + quad_offset(w, 1);
-                const int j2 = i + quad_offset(w, 2), j3 = i + quad_offset(w, 3);
+                const uint32_t j0 = (uint32_t)(i + quad_offset(w, 0));
+                const uint32_t j1 = (uint32_t)(i + quad_offset(w, 1));
+                const uint32_t j2 = (uint32_t)(i + quad_offset(w, 2));
+                const uint32_t j3 = (uint32_t)(i + quad_offset(w, 3));
                 const float4 x0 = __ldg(pv + j0), x1 = __ldg(pv + j1);
                 const float4 x2 = __ldg(pv + j2), x3 = __ldg(pv + j3);
                 const float2 a0 = __ldg(aux + j0), a1 = __ldg(aux + j1);
                 const float2 a2 = __ldg(aux + j2), a3 = __ldg(aux + j3);
-                pair_force(P, xi, ai, x0, a0, k < n, sx, sy);
-                pair_force(P, xi, ai, x1, a1, k + 1 < n, sx, sy);
-                pair_force(P, xi, ai, x2, a2, k + 2 < n, sx, sy);
-                pair_force(P, xi, ai, x3, a3, k + 3 < n, sx, sy);
+                pair_force(P, xi, ai, x0, a0, sx, sy);   // padding entries are the particle
+                pair_force(P, xi, ai, x1, a1, sx, sy);   // itself: exact zero contribution
+                pair_force(P, xi, ai, x2, a2, sx, sy);
+                pair_force(P, xi, ai, x3, a3, sx, sy);
             }
         } else {
             for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
@@ -567,8 +598,8 @@ __global__ void __launch_bounds__(TILE, 5) k_force(DevParams P, DevPtrs D, float
         });
         fbx = -gxs;
         fby = -gys;
-        const float ax = P.mass * sx + gxs / P.mass + P.gx;
-        const float ay = P.mass * sy + gys / P.mass + P.gy;
+        const float ax = P.mdwcb3 * sx + gxs * P.inv_mass + P.gx;   // m * 3C/h^3 * sum
+        const float ay = P.mdwcb3 * sy + gys * P.inv_mass + P.gy;
         float4 xn;
         xn.z = xi.z + P.dt * ax;
         xn.w = xi.w + P.dt * ay;
