@@ -313,6 +313,7 @@ def run_ours(a):
     st = ctx.get_status()[0]
     n_failed = int((st != 0).sum())
     steps_done, rebuilds = ctx.counters()
+    y_checksum = float(y_timed.double().abs().sum().item())   # determinism monitor
     updates = world * B * t.n_fluid * sp.n_sub * a.steps
     value = updates / (ms_max / 1e3)
     # NCCL gather of the trajectory dataset (config C5; the only collective on the path)
@@ -383,7 +384,8 @@ def run_ours(a):
                    "parallelism": f"ensemble dp{world}",
                    "l2": f"no flush: working set {ctx_bytes_gb(t, B):.2f} GB > 126 MB L2",
                    "failed_rollouts": n_failed, "gather_ms": gather_ms,
-                   "substeps_per_rebuild": float(steps_done.mean() / max(rebuilds.mean(), 1))},
+                   "substeps_per_rebuild": float(steps_done.mean() / max(rebuilds.mean(), 1)),
+                   "y_checksum": y_checksum},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 3 * 4,
                 "d2h_bytes_per_step": B * (6 + 3) * 4, "steps": K_e2e},
         "gpu_launches": launches,

@@ -337,7 +337,7 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        const bool fits = P.N > 0 && smem <= 200 * 1024;
+        const bool fits = P.N > 0 && P.N < 65536 && P.ncell < 65535 && smem <= 200 * 1024;
         bool want = tp->rebuild_path == 1 || (tp->rebuild_path == 0 && fits);
         if (want && !fits) {
             sph_destroy(ctx);

@@ -241,29 +241,32 @@ __device__ __forceinline__ T ld(const T* p) {
     else return *p;
 }
 
-// Density + EOS of slot i of rollout b (state pv = the rollout's current buffer).
-template <bool NC>
-__device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D, int b, int i,
-                                           const float4* __restrict__ pv) {
+// Density + EOS of slot i of rollout b.  pos(j) returns the (x, y) of slot j of the rollout
+// (global state buffer, or the shared-memory copy inside k_rebuild_small).
+template <bool NC, class PosF>
+__device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& D, int b, int i,
+                                             PosF&& pos) {
     const size_t o = (size_t)b * P.N;
-    const float4 xi = ld<NC>(pv + i);
+    const float2 p = pos((uint32_t)i);
+    const float4 xi = make_float4(p.x, p.y, 0.f, 0.f);
     float wf = 4.0f;   // self term W_cb(0) ("all particles"): (2-0)^3 - 4 (1-0)^3 = 4
     const int n = ld<NC>(D.ncnt + o + i);
+    auto as4 = [](float2 v) { return make_float4(v.x, v.y, 0.f, 0.f); };
     if (n != NL_OVERFLOW) {
         const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
         for (int k = 0; k < n; k += 4) {
             const uint2 w = ld<NC>(nq);
             nq += P.N;
-            const float4 x0 = ld<NC>(pv + (uint32_t)(i + quad_offset(w, 0)));
-            const float4 x1 = ld<NC>(pv + (uint32_t)(i + quad_offset(w, 1)));
-            const float4 x2 = ld<NC>(pv + (uint32_t)(i + quad_offset(w, 2)));
-            const float4 x3 = ld<NC>(pv + (uint32_t)(i + quad_offset(w, 3)));
+            const float4 x0 = as4(pos((uint32_t)(i + quad_offset(w, 0))));
+            const float4 x1 = as4(pos((uint32_t)(i + quad_offset(w, 1))));
+            const float4 x2 = as4(pos((uint32_t)(i + quad_offset(w, 2))));
+            const float4 x3 = as4(pos((uint32_t)(i + quad_offset(w, 3))));
             wf += (w_list(P, xi, x0) + w_list(P, xi, x1)) + (w_list(P, xi, x2) + w_list(P, xi, x3));
         }
         wf -= 4.0f * (float)(((n + 3) & ~3) - n);   // padding entries (self) added W(0) = 4 each
     } else {
         for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), ld<NC>(D.skey + o + i),
-                            [&](uint32_t j) { wf += w_masked(P, xi, ld<NC>(pv + j), j != (uint32_t)i); });
+                            [&](uint32_t j) { wf += w_masked(P, xi, as4(pos(j)), j != (uint32_t)i); });
     }
     float wg = 0.0f;
     const Geom gm = D.geom[b];
@@ -282,6 +285,15 @@ __device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D,
     const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
     const float pr = P.k * (rho - P.rho0);
     D.aux[o + i] = make_float2(rho, __fdividef(pr, rho * rho));
+}
+
+template <bool NC>
+__device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D, int b, int i,
+                                           const float4* __restrict__ pv) {
+    density_core<NC>(P, D, b, i, [&](uint32_t j) {
+        const float4 v = ld<NC>(pv + j);
+        return make_float2(v.x, v.y);
+    });
 }
 
 // skip_rebuilding = 1 when rollouts that rebuild this substep get their densities from
@@ -350,16 +362,28 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_plan(DevParams P, DevPtrs D) {
 }
 
 // neighbour candidate list of slot i (see k_nlist) from a given cell-start table
+template <class PosF>
+__device__ __forceinline__ void build_list_core(const DevParams& P, const DevPtrs& D, int b, int i,
+                                                const uint32_t* cs, uint32_t cell, PosF&& pos);
 template <bool NC>
 __device__ __forceinline__ void build_list(const DevParams& P, const DevPtrs& D, int b, int i,
                                            const float4* pv, const uint32_t* cs, uint32_t cell) {
+    build_list_core(P, D, b, i, cs, cell, [&](uint32_t j) {
+        const float4 v = ld<NC>(pv + j);
+        return make_float2(v.x, v.y);
+    });
+}
+
+template <class PosF>
+__device__ __forceinline__ void build_list_core(const DevParams& P, const DevPtrs& D, int b, int i,
+                                                const uint32_t* cs, uint32_t cell, PosF&& pos) {
     const size_t o = (size_t)b * P.N;
-    const float4 xi = ld<NC>(pv + i);
+    const float2 xi = pos((uint32_t)i);
     uint2* nq = D.nbr + (size_t)b * KQ * P.N + i;
     int n = 0;
     uint32_t acc0 = 0u, acc1 = 0u;
     for_cell_candidates(P, cs, cell, [&](uint32_t j) {
-        const float4 xj = ld<NC>(pv + j);
+        const float2 xj = pos(j);
         const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
         if (j != (uint32_t)i && r2 < P.RL2 && n != NL_OVERFLOW) {
             const int off = (int)j - i;
@@ -393,6 +417,9 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
 }
 
 // dynamic shared memory: start[ncell + 1] u32 | key[N] u32 | perm[N] u32 | rank[N] u16
+// After the gather, key|perm (8N bytes) is reused for the rollout's positions (float2[N]) and
+// rank for each slot's cell (u16; host guarantees ncell < 65536), so list building and the
+// densities read positions from shared memory.
 __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) {
     extern __shared__ uint32_t smem[];
     __shared__ uint32_t wt[RB_T / 32];
@@ -400,6 +427,8 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
     uint32_t* s_key = s_start + (P.ncell + 1);
     uint32_t* s_perm = s_key + P.N;
     uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_perm + P.N);
+    float2* s_pos = reinterpret_cast<float2*>(s_key);   // aliases key|perm after the gather
+    uint16_t* s_cell = s_rank;                           // aliases rank after the scatter
     const int count = *D.rcount;
     const int T = RB_T, tid = threadIdx.x;
     for (int w = blockIdx.x; w < count; w += gridDim.x) {
@@ -466,19 +495,29 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
             }
         }
         __syncthreads();
-        // 5. gather into cell order
+        // 5. gather into cell order (slot cells kept as u16 in the rank area)
         for (int d = tid; d < P.N; d += T) {
             const uint32_t src = s_perm[d];
             pv1[d] = pv0[src];
             id1[d] = id0[src];
-            D.skey[o + d] = s_key[src];
+            const uint32_t c = s_key[src];
+            D.skey[o + d] = c;
+            s_cell[d] = (uint16_t)c;
         }
         __syncthreads();
-        // 6. neighbour lists (cell starts from shared memory, fresh state: coherent loads)
-        for (int i = tid; i < P.N; i += T) build_list<false>(P, D, b, i, pv1, s_start, s_key[s_perm[i]]);
+        // positions of the new order into shared memory (key|perm are dead now)
+        for (int d = tid; d < P.N; d += T) {
+            const float4 v = pv1[d];
+            s_pos[d] = make_float2(v.x, v.y);
+        }
         __syncthreads();
-        // 7. densities of the rebuilt rollout
-        for (int i = tid; i < P.N; i += T) density_at<false>(P, D, b, i, pv1);
+        // 6. neighbour lists (cell starts and positions from shared memory)
+        for (int i = tid; i < P.N; i += T)
+            build_list_core(P, D, b, i, s_start, (uint32_t)s_cell[i], [&](uint32_t j) { return s_pos[j]; });
+        __syncthreads();
+        // 7. densities of the rebuilt rollout (lists just written: coherent loads)
+        for (int i = tid; i < P.N; i += T)
+            density_core<false>(P, D, b, i, [&](uint32_t j) { return s_pos[j]; });
         __syncthreads();
     }
 }

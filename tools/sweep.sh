@@ -10,7 +10,7 @@ import sys,json
 l=sys.stdin.read().strip()
 try:
   d=json.loads(l); r=d['roofline']
-  print('value %.3e' % d['value'], 'reb/sub %.1f' % d['config']['substeps_per_rebuild'], {k: round(v*1e3,1) for k,v in r['kernel_ms_all'].items()}, 'sub_us', round(r['substep_ms_profiled']*1e3,1))
+  print('value %.3e' % d['value'], 'chk %.9e' % d['config'].get('y_checksum',0), 'reb/sub %.1f' % d['config']['substeps_per_rebuild'], {k: round(v*1e3,1) for k,v in r['kernel_ms_all'].items()}, 'sub_us', round(r['substep_ms_profiled']*1e3,1))
 except Exception as e: print('ERR', l[-500:])
 "
 done
