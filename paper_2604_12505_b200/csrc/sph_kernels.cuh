@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
     extern __shared__ uint32_t smem[];
     __shared__ uint32_t wt[RB_T / 32];
     uint32_t* s_start = smem;
-    uint32_t* s_key = s_start + (P.ncell + 1);
+    uint32_t* s_key = s_start + ((P.ncell + 1 + 3) & ~3);   // 16-byte aligned (float2 alias)
     uint32_t* s_perm = s_key + P.N;
     uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_perm + P.N);
     float2* s_pos = reinterpret_cast<float2*>(s_key);   // aliases key|perm after the gather
