@@ -39,6 +39,8 @@ struct sph_ctx {
 };
 
 static std::string g_init_err;
+static const size_t kDensitySmem = (size_t)MAXSTAGE * 16;                      // TMA window
+static const size_t kForceSmem = (size_t)MAXSTAGE * 16 + (size_t)(MAXSTAGE + 2) * 8;
 
 #define CK(expr)                                                                       \
     do {                                                                               \
@@ -160,7 +162,7 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     put(d.pv[1], BN * 16);
     put(d.id[0], BN * 4);
     put(d.id[1], BN * 4);
-    put(d.aux, BN * 8);
+    put(d.aux, BN * 8 + 16);   // +1 element: the force kernel's 16-B aligned TMA slice
     put(d.skey, BN * 4);
     put(d.nbr, BN * KQ * 8);
     put(d.ncnt, BN);
@@ -220,11 +222,11 @@ static void launch_rebuild_and_density(sph_ctx* ctx) {
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
         k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
         cudaEventRecord(ctx->ev_join, ctx->side);
-        k_density<<<gp, TILE, 0, s>>>(P, ctx->D, 1);
+        k_density<<<gp, TILE, kDensitySmem, s>>>(P, ctx->D, 1);
         cudaStreamWaitEvent(s, ctx->ev_join, 0);
     } else {
         launch_rebin(ctx);
-        k_density<<<gp, TILE, 0, s>>>(P, ctx->D, 0);
+        k_density<<<gp, TILE, kDensitySmem, s>>>(P, ctx->D, 0);
     }
 }
 
@@ -233,7 +235,7 @@ static void launch_substep(sph_ctx* ctx, float damping, int pin) {
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
     launch_rebuild_and_density(ctx);
-    k_force<<<gp, TILE, 0, s>>>(P, ctx->D, damping);
+    k_force<<<gp, TILE, kForceSmem, s>>>(P, ctx->D, damping);
     k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, pin, ctx->ghost_angle0);
 }
 
@@ -634,9 +636,9 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
             launch_rebin(ctx);
         }
         cudaEventRecord(ev[1], s);
-        k_density<<<gp, TILE, 0, s>>>(P, ctx->D, ctx->small ? 1 : 0);
+        k_density<<<gp, TILE, kDensitySmem, s>>>(P, ctx->D, ctx->small ? 1 : 0);
         cudaEventRecord(ev[2], s);
-        k_force<<<gp, TILE, 0, s>>>(P, ctx->D, 1.0f);
+        k_force<<<gp, TILE, kForceSmem, s>>>(P, ctx->D, 1.0f);
         cudaEventRecord(ev[3], s);
         k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
         cudaEventRecord(ev[4], s);

@@ -69,6 +69,7 @@ struct RolloutState {
     int bad_particle;
     float disp;          // bound on any particle's displacement relative to the body
                          // translation since the last rebuild
+    int span;            // max |j - i| over all neighbour-list entries (staging window)
 };
 
 struct Geom {            // float copy of the body state used by the particle kernels
@@ -107,6 +108,38 @@ struct DevPtrs {
     int* dbg_cnt;        // [3][N] debug neighbour counts
     int* dbg_idx;        // [3][N][DBG_CAP] debug neighbour ids
 };
+
+// ---------------------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk global -> shared, completion on an mbarrier)
+// ---------------------------------------------------------------------------------------
+constexpr int MAXSTAGE = 1024;   // slots of a CTA's neighbour window staged in shared memory
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes) : "memory");
+}
+// bytes and both addresses must be multiples of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
 
 // ---------------------------------------------------------------------------------------
 // Small device helpers

@@ -14,6 +14,7 @@ __global__ void __launch_bounds__(TILE) k_hash(DevParams P, DevPtrs D) {
     RolloutState* rs = D.rs + b;
     if (rs->frozen || !rs->need_rebin) return;
     const int i = blockIdx.x * TILE + threadIdx.x;
+    if (i == 0) rs->span = 0;   // recomputed by k_nlist (kernel boundary orders the atomics)
     if (i >= P.N) return;
     const size_t o = (size_t)b * P.N;
     const float4 x = D.pv[rs->sp][o + i];
@@ -298,13 +299,41 @@ __device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D,
 
 // skip_rebuilding = 1 when rollouts that rebuild this substep get their densities from
 // k_rebuild_small (which runs concurrently on another branch of the graph).
+// Staging window of a CTA tile: every list neighbour j of a slot i in [t0, t0 + TILE) has
+// |j - i| <= span, so [lo, hi) covers the tile and all its candidates (sorted row-major cells).
+__device__ __forceinline__ void stage_window(const DevParams& P, int span, int t0, int* lo, int* hi) {
+    *lo = max(t0 - span, 0);
+    *hi = min(t0 + TILE + span, P.N);
+}
+
+// dynamic shared memory: pv[MAXSTAGE] float4 (TMA-staged neighbour window)
 __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D, int skip_rebuilding) {
+    extern __shared__ float4 s_pv[];
+    __shared__ __align__(8) uint64_t bar;
     const int b = blockIdx.y;
     const RolloutState* rs = D.rs + b;
-    if (rs->frozen || (skip_rebuilding && rs->need_rebin)) return;
-    const int i = blockIdx.x * TILE + threadIdx.x;
-    if (i >= P.N) return;
-    density_at<true>(P, D, b, i, D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N);
+    if (rs->frozen || (skip_rebuilding && rs->need_rebin)) return;   // CTA-uniform
+    const int t0 = blockIdx.x * TILE;
+    const int i = t0 + threadIdx.x;
+    const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
+    int lo, hi;
+    stage_window(P, rs->span, t0, &lo, &hi);
+    if (hi - lo <= MAXSTAGE) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            mbar_expect_tx(&bar, (uint32_t)(hi - lo) * 16u);
+            bulk_g2s(s_pv, pv + lo, (uint32_t)(hi - lo) * 16u, &bar);
+        }
+        __syncthreads();
+        mbar_wait(&bar, 0);
+        if (i < P.N)
+            density_core<true>(P, D, b, i, [&](uint32_t j) {
+                const float4 v = s_pv[j - lo];
+                return make_float2(v.x, v.y);
+            });
+    } else if (i < P.N) {
+        density_at<true>(P, D, b, i, pv);
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -362,25 +391,14 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_plan(DevParams P, DevPtrs D) {
 }
 
 // neighbour candidate list of slot i (see k_nlist) from a given cell-start table
+// Returns max |j - i| over the list entries (the staging window of k_density / k_force).
 template <class PosF>
-__device__ __forceinline__ void build_list_core(const DevParams& P, const DevPtrs& D, int b, int i,
-                                                const uint32_t* cs, uint32_t cell, PosF&& pos);
-template <bool NC>
-__device__ __forceinline__ void build_list(const DevParams& P, const DevPtrs& D, int b, int i,
-                                           const float4* pv, const uint32_t* cs, uint32_t cell) {
-    build_list_core(P, D, b, i, cs, cell, [&](uint32_t j) {
-        const float4 v = ld<NC>(pv + j);
-        return make_float2(v.x, v.y);
-    });
-}
-
-template <class PosF>
-__device__ __forceinline__ void build_list_core(const DevParams& P, const DevPtrs& D, int b, int i,
-                                                const uint32_t* cs, uint32_t cell, PosF&& pos) {
+__device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs& D, int b, int i,
+                                               const uint32_t* cs, uint32_t cell, PosF&& pos) {
     const size_t o = (size_t)b * P.N;
     const float2 xi = pos((uint32_t)i);
     uint2* nq = D.nbr + (size_t)b * KQ * P.N + i;
-    int n = 0;
+    int n = 0, span = 0;
     uint32_t acc0 = 0u, acc1 = 0u;
     for_cell_candidates(P, cs, cell, [&](uint32_t j) {
         const float2 xj = pos(j);
@@ -391,6 +409,7 @@ __device__ __forceinline__ void build_list_core(const DevParams& P, const DevPtr
                 n = NL_OVERFLOW;
                 return;
             }
+            span = max(span, abs(off));
             const uint32_t bits = (uint32_t)(uint16_t)(int16_t)off << (16 * (n & 1));
             if (n & 2) acc1 |= bits;
             else acc0 |= bits;
@@ -403,17 +422,26 @@ __device__ __forceinline__ void build_list_core(const DevParams& P, const DevPtr
     });
     if (n != NL_OVERFLOW && (n & 3)) nq[(size_t)(n >> 2) * P.N] = make_uint2(acc0, acc1);
     D.ncnt[o + i] = (uint8_t)n;
+    return n == NL_OVERFLOW ? 0 : span;   // overflowed particles read global memory
 }
 
 __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
     const int b = blockIdx.y;
-    const RolloutState* rs = D.rs + b;
+    RolloutState* rs = D.rs + b;
     if (rs->frozen || !rs->need_rebin) return;
     const int i = blockIdx.x * TILE + threadIdx.x;
-    if (i >= P.N) return;
-    const size_t o = (size_t)b * P.N;
-    build_list<true>(P, D, b, i, D.pv[rs->sp ^ 1] + o, D.cstart + (size_t)b * (P.ncell + 1),
-                     D.skey[o + i]);
+    int span = 0;
+    if (i < P.N) {
+        const size_t o = (size_t)b * P.N;
+        const float4* pv = D.pv[rs->sp ^ 1] + o;
+        span = build_list_core(P, D, b, i, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i],
+                               [&](uint32_t j) {
+                                   const float4 v = __ldg(pv + j);
+                                   return make_float2(v.x, v.y);
+                               });
+    }
+    span = __reduce_max_sync(0xffffffffu, span);
+    if ((threadIdx.x & 31) == 0 && span > 0) atomicMax(&rs->span, span);
 }
 
 // dynamic shared memory: start[ncell + 1] u32 | key[N] u32 | perm[N] u32 | rank[N] u16
@@ -512,8 +540,18 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
         }
         __syncthreads();
         // 6. neighbour lists (cell starts and positions from shared memory)
+        int span = 0;
         for (int i = tid; i < P.N; i += T)
-            build_list_core(P, D, b, i, s_start, (uint32_t)s_cell[i], [&](uint32_t j) { return s_pos[j]; });
+            span = max(span, build_list_core(P, D, b, i, s_start, (uint32_t)s_cell[i],
+                                             [&](uint32_t j) { return s_pos[j]; }));
+        span = __reduce_max_sync(0xffffffffu, span);
+        if ((tid & 31) == 0) wt[tid >> 5] = (uint32_t)span;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t m = 0;
+            for (int q = 0; q < RB_T / 32; ++q) m = max(m, wt[q]);
+            rs->span = (int)m;
+        }
         __syncthreads();
         // 7. densities of the rebuilt rollout (lists just written: coherent loads)
         for (int i = tid; i < P.N; i += T)
@@ -565,43 +603,76 @@ __device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2
     }
 }
 
+// List walk of the force kernel: four candidates per 8-byte offset load.  PV / AX return the
+// state / aux of a slot (shared-memory window or global memory).
+template <class PV, class AX>
+__device__ __forceinline__ void force_list(const DevParams& P, const uint2* __restrict__ nq, int n,
+                                           int i, float4 xi, float2 ai, PV&& pvj, AX&& axj,
+                                           float& sx, float& sy) {
+    for (int k = 0; k < n; k += 4) {
+        const uint2 w = __ldg(nq);
+        nq += P.N;
+        const uint32_t j0 = (uint32_t)(i + quad_offset(w, 0));
+        const uint32_t j1 = (uint32_t)(i + quad_offset(w, 1));
+        const uint32_t j2 = (uint32_t)(i + quad_offset(w, 2));
+        const uint32_t j3 = (uint32_t)(i + quad_offset(w, 3));
+        const float4 x0 = pvj(j0), x1 = pvj(j1), x2 = pvj(j2), x3 = pvj(j3);
+        const float2 a0 = axj(j0), a1 = axj(j1), a2 = axj(j2), a3 = axj(j3);
+        pair_force(P, xi, ai, x0, a0, sx, sy);   // padding entries are the particle
+        pair_force(P, xi, ai, x1, a1, sx, sy);   // itself: exact zero contribution
+        pair_force(P, xi, ai, x2, a2, sx, sy);
+        pair_force(P, xi, ai, x3, a3, sx, sy);
+    }
+}
+
 #ifndef SPH_FORCE_MINB
 #define SPH_FORCE_MINB 5
 #endif
+// dynamic shared memory: pv[MAXSTAGE] float4 | aux[MAXSTAGE + 2] float2 (TMA-staged window)
 __global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, DevPtrs D, float damping) {
+    extern __shared__ float4 s_pv[];
+    float2* s_aux = reinterpret_cast<float2*>(s_pv + MAXSTAGE);
+    __shared__ __align__(8) uint64_t bar;
     const int b = blockIdx.y;
     RolloutState* rs = D.rs + b;
-    if (rs->frozen) return;   // CTA-uniform (before any warp-level collective)
-    const int i = blockIdx.x * TILE + threadIdx.x;
+    if (rs->frozen) return;   // CTA-uniform (before any barrier / warp-level collective)
+    const int t0 = blockIdx.x * TILE;
+    const int i = t0 + threadIdx.x;
     const size_t o = (size_t)b * P.N;
     const int cur = rs->sp ^ rs->need_rebin;
     const float4* __restrict__ pv = D.pv[cur] + o;
     const float2* __restrict__ aux = D.aux + o;
     float fbx = 0.0f, fby = 0.0f, tq = 0.0f, vmax = 0.0f;
     const Geom gm = D.geom[b];
+    int lo, hi;
+    stage_window(P, rs->span, t0, &lo, &hi);
+    const bool staged = hi - lo <= MAXSTAGE;   // CTA-uniform
+    // aux slice aligned to 16 bytes in global memory: [ga0, ga1) covers [o + lo, o + hi)
+    const size_t ga0 = (o + lo) & ~(size_t)1, ga1 = (o + hi + 1) & ~(size_t)1;
+    const int ash = (int)(o + lo - ga0);
+    if (staged) {
+        if (threadIdx.x == 0) {
+            const uint32_t bp = (uint32_t)(hi - lo) * 16u, ba = (uint32_t)(ga1 - ga0) * 8u;
+            mbar_init(&bar, 1);
+            mbar_expect_tx(&bar, bp + ba);
+            bulk_g2s(s_pv, pv + lo, bp, &bar);
+            bulk_g2s(s_aux, D.aux + ga0, ba, &bar);
+        }
+        __syncthreads();
+        mbar_wait(&bar, 0);
+    }
     if (i < P.N) {
-        const float4 xi = pv[i];
-        const float2 ai = aux[i];
+        const float4 xi = staged ? s_pv[i - lo] : pv[i];
+        const float2 ai = staged ? s_aux[i - lo + ash] : aux[i];
         float sx = 0.0f, sy = 0.0f;   // sum of (-pressure + viscous) * grad W / m^2
         const int n = D.ncnt[o + i];
-        if (n != NL_OVERFLOW) {
-            const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
-            for (int k = 0; k < n; k += 4) {
-                const uint2 w = __ldg(nq);
-                nq += P.N;
-                const uint32_t j0 = (uint32_t)(i + quad_offset(w, 0));
-                const uint32_t j1 = (uint32_t)(i + quad_offset(w, 1));
-                const uint32_t j2 = (uint32_t)(i + quad_offset(w, 2));
-                const uint32_t j3 = (uint32_t)(i + quad_offset(w, 3));
-                const float4 x0 = __ldg(pv + j0), x1 = __ldg(pv + j1);
-                const float4 x2 = __ldg(pv + j2), x3 = __ldg(pv + j3);
-                const float2 a0 = __ldg(aux + j0), a1 = __ldg(aux + j1);
-                const float2 a2 = __ldg(aux + j2), a3 = __ldg(aux + j3);
-                pair_force(P, xi, ai, x0, a0, sx, sy);   // padding entries are the particle
-                pair_force(P, xi, ai, x1, a1, sx, sy);   // itself: exact zero contribution
-                pair_force(P, xi, ai, x2, a2, sx, sy);
-                pair_force(P, xi, ai, x3, a3, sx, sy);
-            }
+        const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
+        if (n != NL_OVERFLOW && staged) {
+            force_list(P, nq, n, i, xi, ai, [&](uint32_t j) { return s_pv[j - lo]; },
+                       [&](uint32_t j) { return s_aux[j - lo + ash]; }, sx, sy);
+        } else if (n != NL_OVERFLOW) {
+            force_list(P, nq, n, i, xi, ai, [&](uint32_t j) { return __ldg(pv + j); },
+                       [&](uint32_t j) { return __ldg(aux + j); }, sx, sy);
         } else {
             for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
                 pair_force(P, xi, ai, __ldg(pv + j), __ldg(aux + j), j != (uint32_t)i, sx, sy);
