@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -126,6 +127,10 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     const float RL = (float)(2.0 * h + (tp->rebin_every ? 0.0 : tp->skin));
     P->RL2 = tp->rebin_every ? P->H2 : RL * RL;      // list radius (2h + skin)^2
     P->rebuild_disp = (float)(0.45 * tp->skin);      // < skin / 2 with margin for rounding
+    {   // experimental TMA staging of neighbour windows (off by default: slower)
+        const char* e = std::getenv("SPH_TMA_STAGE");
+        P->stage = (e && e[0] == '1') ? 1 : 0;
+    }
     // ghost-ring window (see for_ghost_candidates): only particles farther than d_min from the
     // centre can have a ghost within 2h; their ghosts lie within +-dphi of their polar angle.
     // |x - g| < s with |x| = d, |g| = R  =>  d > R - s  and  sin(dphi/2) < s / (2 sqrt(d R)).

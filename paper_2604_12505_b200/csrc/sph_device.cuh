@@ -52,6 +52,8 @@ struct DevParams {
     float ghost_scale;      // G / (2 pi)
     float rebuild_disp;     // rebuild when the displacement bound reaches this (< skin / 2)
     int rebin_every;
+    int stage;              // 1: TMA-stage each CTA's neighbour window in shared memory
+                            //    (experimental, env SPH_TMA_STAGE=1; slower on C3, see DESIGN)
     double dtd, m_body, J_body;
 };
 

@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D, int sk
     const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
     int lo, hi;
     stage_window(P, rs->span, t0, &lo, &hi);
-    if (hi - lo <= MAXSTAGE) {
+    if (P.stage && hi - lo <= MAXSTAGE) {
         if (threadIdx.x == 0) {
             mbar_init(&bar, 1);
             mbar_expect_tx(&bar, (uint32_t)(hi - lo) * 16u);
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, Dev
     const Geom gm = D.geom[b];
     int lo, hi;
     stage_window(P, rs->span, t0, &lo, &hi);
-    const bool staged = hi - lo <= MAXSTAGE;   // CTA-uniform
+    const bool staged = P.stage && hi - lo <= MAXSTAGE;   // CTA-uniform
     // aux slice aligned to 16 bytes in global memory: [ga0, ga1) covers [o + lo, o + hi)
     const size_t ga0 = (o + lo) & ~(size_t)1, ga1 = (o + hi + 1) & ~(size_t)1;
     const int ash = (int)(o + lo - ga0);

@@ -126,8 +126,10 @@ def settled_c1():
     return t2.snapped()
 
 
-@pytest.mark.parametrize("rebin_every,path", [(1, 0), (0, 0), (0, 2)])
-def test_200_step_body_trajectory(settled_c1, rebin_every, path):
+@pytest.mark.parametrize("rebin_every,path,stage", [(1, 0, 0), (0, 0, 0), (0, 2, 0), (0, 0, 1)])
+def test_200_step_body_trajectory(settled_c1, rebin_every, path, stage, monkeypatch):
+    """stage = 1 exercises the experimental TMA window staging (SPH_TMA_STAGE)."""
+    monkeypatch.setenv("SPH_TMA_STAGE", str(stage))
     t = settled_c1
     u = (5.0, 2.0, 1.0)
     kw = dict(rebuild_path=path) if rebin_every else dict(rebin_every=0, skin=0.2 * t.params.h,
