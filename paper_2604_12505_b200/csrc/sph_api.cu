@@ -31,6 +31,7 @@ struct sph_ctx {
     size_t stage_bytes = 0;
     int* dbg_buf = nullptr;
     int n_sub = 1;
+    int body_threads = BODY_T;   // k_body block size (from N only: reduction order fixed)
     // small-rollout rebuild path: k_rebuild_small on a forked branch (side stream + events)
     bool small = false;
     size_t small_smem = 0;
@@ -42,6 +43,7 @@ struct sph_ctx {
 static std::string g_init_err;
 static const size_t kDensitySmem = (size_t)MAXSTAGE * 16;                      // TMA window
 static const size_t kForceSmem = (size_t)MAXSTAGE * 16 + (size_t)(MAXSTAGE + 2) * 8;
+static const int kSmallMinBatch = 512;   // auto policy: per-rollout-CTA rebuild from this B on
 
 #define CK(expr)                                                                       \
     do {                                                                               \
@@ -199,9 +201,9 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
 // ---------------------------------------------------------------------------------------
 // Launch sequencing
 // ---------------------------------------------------------------------------------------
-static void launch_rebin(sph_ctx* ctx) {
+static void launch_rebin(sph_ctx* ctx, cudaStream_t s = nullptr) {
     const DevParams& P = ctx->P;
-    cudaStream_t s = ctx->stream;
+    if (!s) s = ctx->stream;
     dim3 gp(P.ntile, P.B), gs(P.nscan, P.B), gc((P.ncell + TILE - 1) / TILE, P.B);
     k_hash<<<gp, TILE, 0, s>>>(P, ctx->D);
     k_scan_reduce<<<gs, SCAN_T, 0, s>>>(P, ctx->D);
@@ -217,12 +219,49 @@ static void launch_rebin(sph_ctx* ctx) {
 // work list, then k_rebuild_small (one CTA per rebuilding rollout, side stream) runs
 // concurrently with k_density for every other rollout (fork/join via events; captured into
 // the tick graph as two parallel branches).
-static void launch_rebuild_and_density(sph_ctx* ctx) {
+// Multi-kernel path inside a graph capture: the plan kernel sets a conditional handle and the
+// eight grid-wide rebuild kernels sit in the body of an IF node (skipped when no rollout of
+// the batch needs a rebuild this substep).
+static cudaError_t add_conditional_rebin(sph_ctx* ctx) {
+    cudaStream_t s = ctx->stream;
+    cudaStreamCaptureStatus st;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    cudaError_t e = cudaStreamGetCaptureInfo(s, &st, nullptr, &g, &deps, &nd);
+    if (e != cudaSuccess) return e;
+    cudaGraphConditionalHandle h;
+    if ((e = cudaGraphConditionalHandleCreate(&h, g, 0, 0)) != cudaSuccess) return e;
+    k_rebuild_plan<<<1, RB_T, 0, s>>>(ctx->P, ctx->D, h, 1);
+    if ((e = cudaStreamGetCaptureInfo(s, &st, nullptr, &g, &deps, &nd)) != cudaSuccess) return e;
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    if ((e = cudaGraphAddNode(&node, g, deps, nd, &cp)) != cudaSuccess) return e;
+    if ((e = cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
+        return e;
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    if ((e = cudaStreamBeginCaptureToGraph(ctx->side, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+        return e;
+    launch_rebin(ctx, ctx->side);
+    return cudaStreamEndCapture(ctx->side, &body);
+}
+
+// Rebuild (only rollouts that need it) + densities.  Small path: the plan kernel builds the
+// work list, then k_rebuild_small (one CTA per rebuilding rollout, side stream) runs
+// concurrently with k_density for every other rollout (fork/join via events; captured into
+// the tick graph as two parallel branches).  Multi-kernel path: grid-wide rebuild kernels,
+// under an IF node when captured.
+static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
     if (ctx->small) {
-        k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D);
+        k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
         cudaEventRecord(ctx->ev_fork, s);
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
         k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
@@ -230,21 +269,30 @@ static void launch_rebuild_and_density(sph_ctx* ctx) {
         k_density<<<gp, TILE, kDensitySmem, s>>>(P, ctx->D, 1);
         cudaStreamWaitEvent(s, ctx->ev_join, 0);
     } else {
-        launch_rebin(ctx);
+        if (capturing) {
+            cudaError_t e = add_conditional_rebin(ctx);
+            if (e != cudaSuccess) return e;
+        } else {
+            launch_rebin(ctx);
+        }
         k_density<<<gp, TILE, kDensitySmem, s>>>(P, ctx->D, 0);
     }
+    return cudaSuccess;
 }
 
-static void launch_substep(sph_ctx* ctx, float damping, int pin) {
+static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool capturing = false) {
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
-    launch_rebuild_and_density(ctx);
+    cudaError_t e = launch_rebuild_and_density(ctx, capturing);
     k_force<<<gp, TILE, kForceSmem, s>>>(P, ctx->D, damping);
-    k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, pin, ctx->ghost_angle0);
+    k_body<<<P.B, ctx->body_threads, 0, s>>>(P, ctx->D, pin, ctx->ghost_angle0);
+    return e;
 }
 
-static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? 5 : 11; }
+// kernels per substep: small path 5 (plan, rebuild_small, density, force, body); multi-kernel
+// path 4 + 8 rebuild kernels (the 8 run only in substeps where some rollout rebuilds).
+static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? 5 : 12; }
 
 static sph_status check_launch(sph_ctx* ctx) {
     cudaError_t e = cudaGetLastError();
@@ -345,7 +393,10 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         const bool fits = P.N > 0 && P.N < 65536 && P.ncell < 65535 && smem <= 200 * 1024;
-        bool want = tp->rebuild_path == 1 || (tp->rebuild_path == 0 && fits);
+        // auto: the one-CTA rebuild of a rollout (~0.2 ms on one SM) hides under the densities
+        // of the other rollouts only for large batches; small batches use the grid-wide
+        // kernels (under a graph IF node).
+        bool want = tp->rebuild_path == 1 || (tp->rebuild_path == 0 && fits && P.B >= kSmallMinBatch);
         if (want && !fits) {
             sph_destroy(ctx);
             return fail(nullptr, SPH_EINVAL, "rebuild_path = 1 but the rollout does not fit in shared memory");
@@ -359,11 +410,13 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             ctx->small = true;
             ctx->small_smem = smem;
             ctx->small_grid = std::max(1, std::min(P.B, nsm));
-            if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess ||
-                (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
-                (e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess)
-                return bail("side stream", e);
         }
+        if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess)
+            return bail("side stream", e);
+        // k_body: enough threads to reduce the per-warp partials of big tanks (N only)
+        while (ctx->body_threads < 1024 && ctx->body_threads * 4 < P.npart) ctx->body_threads *= 2;
     }
     if ((e = cudaMemsetAsync(d_workspace, 0, total, s)) != cudaSuccess) return bail("memset", e);
     std::vector<double2> gb(std::max(n_ghost, 1));
@@ -466,8 +519,13 @@ static sph_status capture_tick_graph(sph_ctx* ctx) {
     if (ctx->tick_graph) return SPH_OK;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    for (int k = 0; k < ctx->n_sub; ++k) launch_substep(ctx, 1.0f, 0);
+    cudaError_t ce = cudaSuccess;
+    for (int k = 0; k < ctx->n_sub && ce == cudaSuccess; ++k) ce = launch_substep(ctx, 1.0f, 0, true);
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    if (ce != cudaSuccess) {
+        if (e == cudaSuccess) cudaGraphDestroy(g);
+        return fail(ctx, SPH_ECUDA, std::string("conditional node: ") + cudaGetErrorString(ce));
+    }
     if (e != cudaSuccess) return fail(ctx, SPH_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
     e = cudaGraphInstantiate(&ctx->tick_graph, g, 0);
     cudaGraphDestroy(g);
@@ -635,7 +693,7 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
     for (int it = 0; it < n_substeps; ++it) {
         cudaEventRecord(ev[0], s);
         if (ctx->small) {
-            k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D);
+            k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
             k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
         } else {
             launch_rebin(ctx);
@@ -645,7 +703,7 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
         cudaEventRecord(ev[2], s);
         k_force<<<gp, TILE, kForceSmem, s>>>(P, ctx->D, 1.0f);
         cudaEventRecord(ev[3], s);
-        k_body<<<P.B, BODY_T, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
+        k_body<<<P.B, ctx->body_threads, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
         cudaEventRecord(ev[4], s);
         sph_status st = check_launch(ctx);
         if (st) return st;

@@ -376,7 +376,11 @@ __device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t v, uint32_t* tota
     return base + x - v;
 }
 
-__global__ void __launch_bounds__(RB_T) k_rebuild_plan(DevParams P, DevPtrs D) {
+// set_cond != 0 (graph launch): also sets the IF node that guards the grid-wide rebuild
+// kernels, so substeps without any rebuild skip them entirely.
+__global__ void __launch_bounds__(RB_T) k_rebuild_plan(DevParams P, DevPtrs D,
+                                                       cudaGraphConditionalHandle cond,
+                                                       int set_cond) {
     __shared__ uint32_t wt[RB_T / 32];
     uint32_t base = 0;
     for (int b0 = 0; b0 < P.B; b0 += RB_T) {
@@ -387,7 +391,10 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_plan(DevParams P, DevPtrs D) {
         if (f) D.rlist[pos] = b;
         base += tot;
     }
-    if (threadIdx.x == 0) *D.rcount = (int)base;
+    if (threadIdx.x == 0) {
+        *D.rcount = (int)base;
+        if (set_cond) cudaGraphSetConditional(cond, base > 0 ? 1u : 0u);
+    }
 }
 
 // neighbour candidate list of slot i (see k_nlist) from a given cell-start table
@@ -743,9 +750,10 @@ __global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, Dev
 // ---------------------------------------------------------------------------------------
 // Ghost kinematics, Eq. kinematicghost, in fp64 from the fp64 body state.
 // ---------------------------------------------------------------------------------------
+// body[6], body[7] = cos(theta), sin(theta) (computed once per rollout)
 __device__ __forceinline__ void ghost_update(const DevParams& P, const DevPtrs& D, int b,
                                              const double* body, int tid, int nthr) {
-    const double c = cos(body[2]), s = sin(body[2]);
+    const double c = body[6], s = body[7];
     for (int g = tid; g < P.G; g += nthr) {
         const double2 q = D.ghost_b[g];
         const double ax = c * q.x - s * q.y, ay = s * q.x + c * q.y;
@@ -764,18 +772,21 @@ __device__ __forceinline__ void ghost_update(const DevParams& P, const DevPtrs& 
 //   m rddot = -sum G + (u_x, u_y),  J thddot = sum (r_g - r) x (-G) + tau,
 // symplectic Euler, status, rebuild policy, then ghosts for the next substep.
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(BODY_T) k_body(DevParams P, DevPtrs D, int pin,
-                                                 float ghost_angle0) {
+// blockDim.x = a power of two <= 1024, chosen from N only (so the reduction order, and hence
+// the bits, never depend on the batch size).
+__global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
+                                               float ghost_angle0) {
     const int b = blockIdx.x;
+    const int nt = blockDim.x;
     RolloutState* rs = D.rs + b;
-    __shared__ double4 red[BODY_T];
-    __shared__ double sbody[6];
+    __shared__ double4 red[1024];
+    __shared__ double sbody[8];
     __shared__ int sdead;
     if (threadIdx.x == 0) sdead = rs->frozen;
     __syncthreads();
     if (sdead) return;
     double4 s = make_double4(0, 0, 0, 0);
-    for (int t = threadIdx.x; t < P.npart; t += BODY_T) {
+    for (int t = threadIdx.x; t < P.npart; t += nt) {
         const double4 q = D.part[(size_t)b * P.npart + t];
         s.x += q.x;
         s.y += q.y;
@@ -784,7 +795,7 @@ __global__ void __launch_bounds__(BODY_T) k_body(DevParams P, DevPtrs D, int pin
     }
     red[threadIdx.x] = s;
     __syncthreads();
-    for (int w = BODY_T / 2; w > 0; w >>= 1) {
+    for (int w = nt / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) {
             double4 a = red[threadIdx.x], c = red[threadIdx.x + w];
             red[threadIdx.x] = make_double4(a.x + c.x, a.y + c.y, a.z + c.z, fmax(a.w, c.w));
@@ -814,6 +825,7 @@ __global__ void __launch_bounds__(BODY_T) k_body(DevParams P, DevPtrs D, int pin
             big = big || fabs(body[c]) > 1e9;
         }
         if (!fin || big) set_status(rs, fin ? 2 : 1, -1);
+        sincos(body[2], &sbody[7], &sbody[6]);
         D.geom[b] = Geom{(float)body[0], (float)body[1], (float)((double)body[2] + ghost_angle0),
                          (float)body[3], (float)body[4], {0.f, 0.f, 0.f}};
         const int nr = rs->need_rebin;
@@ -829,7 +841,7 @@ __global__ void __launch_bounds__(BODY_T) k_body(DevParams P, DevPtrs D, int pin
         if (rs->status) rs->frozen = 1;
     }
     __syncthreads();
-    ghost_update(P, D, b, sbody, threadIdx.x, BODY_T);
+    ghost_update(P, D, b, sbody, threadIdx.x, nt);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -883,7 +895,7 @@ __global__ void k_export(DevParams P, DevPtrs D, int b, float4* out, float* rho)
 __global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angle0) {
     const int b = b0 + blockIdx.x;
     RolloutState* rs = D.rs + b;
-    __shared__ double sbody[6];
+    __shared__ double sbody[8];
     if (threadIdx.x == 0) {
         rs->need_rebin = 1;
         rs->status = 0;
@@ -893,6 +905,7 @@ __global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angl
         rs->disp = 0.f;
         const double* body = D.body + (size_t)b * 6;
         for (int c = 0; c < 6; ++c) sbody[c] = body[c];
+        sincos(body[2], &sbody[7], &sbody[6]);
         D.geom[b] = Geom{(float)body[0], (float)body[1], (float)(body[2] + ghost_angle0),
                          (float)body[3], (float)body[4], {0.f, 0.f, 0.f}};
     }

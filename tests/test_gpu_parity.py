@@ -344,9 +344,9 @@ def test_adaptive_rebuilds_are_rare_and_results_match_every_step_mode(settled_c1
     t = settled_c1
     K = 8
     u = si.ensemble_inputs([3, 4], K)[0]
-    a = _ctx(t, B=2, rebin_every=0, skin=0.3 * t.params.h)
+    a = _ctx(t, B=2, rebin_every=0, skin=0.3 * t.params.h)        # auto: grid-wide (+ IF node)
     ya, _ = a.rollout(u)
-    m = _ctx(t, B=2, rebin_every=0, skin=0.3 * t.params.h, rebuild_path=2)
+    m = _ctx(t, B=2, rebin_every=0, skin=0.3 * t.params.h, rebuild_path=1)   # per-rollout CTA
     ym, _ = m.rollout(u)
     assert np.array_equal(ya, ym)     # both rebuild paths produce the same sort and lists
     m.close()
