@@ -41,8 +41,12 @@ struct sph_ctx {
 };
 
 static std::string g_init_err;
-static const size_t kDensitySmem = (size_t)MAXSTAGE * 16;                      // TMA window
-static const size_t kForceSmem = (size_t)MAXSTAGE * 16 + (size_t)(MAXSTAGE + 2) * 8;
+// dynamic shared memory of the neighbour kernels: only with TMA window staging (a reservation
+// would otherwise shrink the L1 carve-out the neighbour gathers live in)
+static size_t density_smem(const DevParams& P) { return P.stage ? (size_t)MAXSTAGE * 16 : 0; }
+static size_t force_smem(const DevParams& P) {
+    return P.stage ? (size_t)MAXSTAGE * 16 + (size_t)(MAXSTAGE + 2) * 8 : 0;
+}
 static const int kSmallMinBatch = 512;   // auto policy: per-rollout-CTA rebuild from this B on
 
 #define CK(expr)                                                                       \
@@ -266,7 +270,7 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
         k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
         cudaEventRecord(ctx->ev_join, ctx->side);
-        k_density<<<gp, TILE, kDensitySmem, s>>>(P, ctx->D, 1);
+        k_density<<<gp, TILE, density_smem(P), s>>>(P, ctx->D, 1);
         cudaStreamWaitEvent(s, ctx->ev_join, 0);
     } else {
         if (capturing) {
@@ -275,7 +279,7 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
         } else {
             launch_rebin(ctx);
         }
-        k_density<<<gp, TILE, kDensitySmem, s>>>(P, ctx->D, 0);
+        k_density<<<gp, TILE, density_smem(P), s>>>(P, ctx->D, 0);
     }
     return cudaSuccess;
 }
@@ -285,7 +289,7 @@ static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool cap
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
     cudaError_t e = launch_rebuild_and_density(ctx, capturing);
-    k_force<<<gp, TILE, kForceSmem, s>>>(P, ctx->D, damping);
+    k_force<<<gp, TILE, force_smem(P), s>>>(P, ctx->D, damping);
     k_body<<<P.B, ctx->body_threads, 0, s>>>(P, ctx->D, pin, ctx->ghost_angle0);
     return e;
 }
@@ -699,9 +703,9 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
             launch_rebin(ctx);
         }
         cudaEventRecord(ev[1], s);
-        k_density<<<gp, TILE, kDensitySmem, s>>>(P, ctx->D, ctx->small ? 1 : 0);
+        k_density<<<gp, TILE, density_smem(P), s>>>(P, ctx->D, ctx->small ? 1 : 0);
         cudaEventRecord(ev[2], s);
-        k_force<<<gp, TILE, kForceSmem, s>>>(P, ctx->D, 1.0f);
+        k_force<<<gp, TILE, force_smem(P), s>>>(P, ctx->D, 1.0f);
         cudaEventRecord(ev[3], s);
         k_body<<<P.B, ctx->body_threads, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
         cudaEventRecord(ev[4], s);
