@@ -205,6 +205,25 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
 // ---------------------------------------------------------------------------------------
 // Launch sequencing
 // ---------------------------------------------------------------------------------------
+static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding) {
+    const DevParams& P = ctx->P;
+    dim3 gp(P.ntile, P.B);
+    if (P.stage) k_density<true><<<gp, TILE, density_smem(P), s>>>(P, ctx->D, skip_rebuilding);
+    else k_density<false><<<gp, TILE, 0, s>>>(P, ctx->D, skip_rebuilding);
+}
+
+static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping) {
+    const DevParams& P = ctx->P;
+    dim3 gp(P.ntile, P.B);
+    if (P.stage) k_force<true><<<gp, TILE, force_smem(P), s>>>(P, ctx->D, damping);
+    else k_force<false><<<gp, TILE, 0, s>>>(P, ctx->D, damping);
+}
+
+static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0) {
+    k_body<<<ctx->P.B, ctx->body_threads, (size_t)ctx->body_threads * sizeof(double4), s>>>(
+        ctx->P, ctx->D, pin, ghost_angle0);
+}
+
 static void launch_rebin(sph_ctx* ctx, cudaStream_t s = nullptr) {
     const DevParams& P = ctx->P;
     if (!s) s = ctx->stream;
@@ -270,7 +289,7 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
         k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
         cudaEventRecord(ctx->ev_join, ctx->side);
-        k_density<<<gp, TILE, density_smem(P), s>>>(P, ctx->D, 1);
+        launch_density(ctx, s,1);
         cudaStreamWaitEvent(s, ctx->ev_join, 0);
     } else {
         if (capturing) {
@@ -279,7 +298,7 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
         } else {
             launch_rebin(ctx);
         }
-        k_density<<<gp, TILE, density_smem(P), s>>>(P, ctx->D, 0);
+        launch_density(ctx, s,0);
     }
     return cudaSuccess;
 }
@@ -289,8 +308,8 @@ static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool cap
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
     cudaError_t e = launch_rebuild_and_density(ctx, capturing);
-    k_force<<<gp, TILE, force_smem(P), s>>>(P, ctx->D, damping);
-    k_body<<<P.B, ctx->body_threads, 0, s>>>(P, ctx->D, pin, ctx->ghost_angle0);
+    launch_force(ctx, s,damping);
+    launch_body(ctx, s,pin, ctx->ghost_angle0);
     return e;
 }
 
@@ -703,11 +722,11 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
             launch_rebin(ctx);
         }
         cudaEventRecord(ev[1], s);
-        k_density<<<gp, TILE, density_smem(P), s>>>(P, ctx->D, ctx->small ? 1 : 0);
+        launch_density(ctx, s,ctx->small ? 1 : 0);
         cudaEventRecord(ev[2], s);
-        k_force<<<gp, TILE, force_smem(P), s>>>(P, ctx->D, 1.0f);
+        launch_force(ctx, s,1.0f);
         cudaEventRecord(ev[3], s);
-        k_body<<<P.B, ctx->body_threads, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
+        launch_body(ctx, s,0, ctx->ghost_angle0);
         cudaEventRecord(ev[4], s);
         sph_status st = check_launch(ctx);
         if (st) return st;

@@ -307,6 +307,7 @@ __device__ __forceinline__ void stage_window(const DevParams& P, int span, int t
 }
 
 // dynamic shared memory: pv[MAXSTAGE] float4 (TMA-staged neighbour window)
+template <bool STAGE>
 __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D, int skip_rebuilding) {
     extern __shared__ float4 s_pv[];
     __shared__ __align__(8) uint64_t bar;
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D, int sk
     const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
     int lo, hi;
     stage_window(P, rs->span, t0, &lo, &hi);
-    if (P.stage && hi - lo <= MAXSTAGE) {
+    if (STAGE && hi - lo <= MAXSTAGE) {
         if (threadIdx.x == 0) {
             mbar_init(&bar, 1);
             mbar_expect_tx(&bar, (uint32_t)(hi - lo) * 16u);
@@ -636,6 +637,7 @@ __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __re
 #define SPH_FORCE_MINB 5
 #endif
 // dynamic shared memory: pv[MAXSTAGE] float4 | aux[MAXSTAGE + 2] float2 (TMA-staged window)
+template <bool STAGE>
 __global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, DevPtrs D, float damping) {
     extern __shared__ float4 s_pv[];
     float2* s_aux = reinterpret_cast<float2*>(s_pv + MAXSTAGE);
@@ -653,7 +655,7 @@ __global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, Dev
     const Geom gm = D.geom[b];
     int lo, hi;
     stage_window(P, rs->span, t0, &lo, &hi);
-    const bool staged = P.stage && hi - lo <= MAXSTAGE;   // CTA-uniform
+    const bool staged = STAGE && hi - lo <= MAXSTAGE;   // CTA-uniform
     // aux slice aligned to 16 bytes in global memory: [ga0, ga1) covers [o + lo, o + hi)
     const size_t ga0 = (o + lo) & ~(size_t)1, ga1 = (o + hi + 1) & ~(size_t)1;
     const int ash = (int)(o + lo - ga0);
@@ -779,7 +781,7 @@ __global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
     const int b = blockIdx.x;
     const int nt = blockDim.x;
     RolloutState* rs = D.rs + b;
-    __shared__ double4 red[1024];
+    extern __shared__ double4 red[];   // [blockDim.x]
     __shared__ double sbody[8];
     __shared__ int sdead;
     if (threadIdx.x == 0) sdead = rs->frozen;
