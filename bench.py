@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--rollouts", type=int, default=0, help="override rollouts per GPU")
     ap.add_argument("--rebin-every", type=int, default=0,
                     help="1: rebuild cell list + neighbour lists every substep; 0: adaptive (skin)")
-    ap.add_argument("--skin", type=float, default=0.15, help="Verlet skin in units of h (adaptive)")
+    ap.add_argument("--skin", type=float, default=0.1, help="Verlet skin in units of h (adaptive)")
     ap.add_argument("--settle-seconds", type=float, default=2.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-substeps", type=int, default=20)

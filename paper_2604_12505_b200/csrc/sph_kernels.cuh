@@ -408,26 +408,40 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
     uint2* nq = D.nbr + (size_t)b * KQ * P.N + i;
     int n = 0, span = 0;
     uint32_t acc0 = 0u, acc1 = 0u;
-    for_cell_candidates(P, cs, cell, [&](uint32_t j) {
-        const float2 xj = pos(j);
-        const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-        if (j != (uint32_t)i && r2 < P.RL2 && n != NL_OVERFLOW) {
-            const int off = (int)j - i;
-            if (n >= KMAX || off < -32768 || off > 32767) {
-                n = NL_OVERFLOW;
-                return;
+    // SIMT-friendly: a branch-free hit mask over up to 32 candidates of a cell-row segment,
+    // then only the set bits are appended (ascending j, the same order as a plain scan).
+    const int cy = (int)cell / P.nx, cx = (int)cell - cy * P.nx;
+    for (int dy = -1; dy <= 1; ++dy) {
+        const int c0 = (cy + dy) * P.nx + cx - 1;
+        const int j0 = (int)cs[c0], j1 = (int)cs[c0 + 3];
+        for (int base = j0; base < j1; base += 32) {
+            const int cnt = min(32, j1 - base);
+            uint32_t m = 0u;
+            for (int k = 0; k < cnt; ++k) {
+                const float2 xj = pos((uint32_t)(base + k));
+                const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+                m |= (base + k != i && r2 < P.RL2) ? (1u << k) : 0u;
             }
-            span = max(span, abs(off));
-            const uint32_t bits = (uint32_t)(uint16_t)(int16_t)off << (16 * (n & 1));
-            if (n & 2) acc1 |= bits;
-            else acc0 |= bits;
-            ++n;
-            if ((n & 3) == 0) {
-                nq[(size_t)((n >> 2) - 1) * P.N] = make_uint2(acc0, acc1);
-                acc0 = acc1 = 0u;
+            while (m != 0u && n != NL_OVERFLOW) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1u;
+                const int off = base + k - i;
+                if (n >= KMAX || off < -32768 || off > 32767) {
+                    n = NL_OVERFLOW;
+                    break;
+                }
+                span = max(span, abs(off));
+                const uint32_t bits = (uint32_t)(uint16_t)(int16_t)off << (16 * (n & 1));
+                if (n & 2) acc1 |= bits;
+                else acc0 |= bits;
+                ++n;
+                if ((n & 3) == 0) {
+                    nq[(size_t)((n >> 2) - 1) * P.N] = make_uint2(acc0, acc1);
+                    acc0 = acc1 = 0u;
+                }
             }
         }
-    });
+    }
     if (n != NL_OVERFLOW && (n & 3)) nq[(size_t)(n >> 2) * P.N] = make_uint2(acc0, acc1);
     D.ncnt[o + i] = (uint8_t)n;
     return n == NL_OVERFLOW ? 0 : span;   // overflowed particles read global memory
