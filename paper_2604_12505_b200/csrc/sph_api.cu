@@ -224,7 +224,9 @@ static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle
         ctx->P, ctx->D, pin, ghost_angle0);
 }
 
-static void launch_rebin(sph_ctx* ctx, cudaStream_t s = nullptr) {
+// Grid-wide counting sort by cell of every rollout with need_rebin (7 kernels); with_nlist adds
+// the grid-wide list build (debug path; the step uses k_nlist_density instead).
+static void launch_rebin(sph_ctx* ctx, cudaStream_t s = nullptr, bool with_nlist = false) {
     const DevParams& P = ctx->P;
     if (!s) s = ctx->stream;
     dim3 gp(P.ntile, P.B), gs(P.nscan, P.B), gc((P.ncell + TILE - 1) / TILE, P.B);
@@ -235,7 +237,13 @@ static void launch_rebin(sph_ctx* ctx, cudaStream_t s = nullptr) {
     k_scatter<<<gp, TILE, 0, s>>>(P, ctx->D);
     k_cellsort<<<gc, TILE, 0, s>>>(P, ctx->D);
     k_gather<<<gp, TILE, 0, s>>>(P, ctx->D);
-    k_nlist<<<gp, TILE, 0, s>>>(P, ctx->D);
+    if (with_nlist) k_nlist<<<gp, TILE, 0, s>>>(P, ctx->D);
+}
+
+// lists + densities of the rebuilt rollouts (work list), spread over the whole GPU
+static void launch_nlist_density(sph_ctx* ctx, cudaStream_t s) {
+    const DevParams& P = ctx->P;
+    k_nlist_density<<<dim3(P.ntile, std::min(P.B, 64)), TILE, 0, s>>>(P, ctx->D);
 }
 
 // Rebuild (only rollouts that need it) + densities.  Small path: the plan kernel builds the
@@ -287,19 +295,21 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
         cudaEventRecord(ctx->ev_fork, s);
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
-        k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
+        k_rebuild_small<false><<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
         cudaEventRecord(ctx->ev_join, ctx->side);
-        launch_density(ctx, s,1);
+        launch_density(ctx, s, 1);
         cudaStreamWaitEvent(s, ctx->ev_join, 0);
     } else {
         if (capturing) {
             cudaError_t e = add_conditional_rebin(ctx);
             if (e != cudaSuccess) return e;
         } else {
+            k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
             launch_rebin(ctx);
         }
-        launch_density(ctx, s,0);
+        launch_density(ctx, s, 1);
     }
+    launch_nlist_density(ctx, s);
     return cudaSuccess;
 }
 
@@ -315,7 +325,7 @@ static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool cap
 
 // kernels per substep: small path 5 (plan, rebuild_small, density, force, body); multi-kernel
 // path 4 + 8 rebuild kernels (the 8 run only in substeps where some rollout rebuilds).
-static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? 5 : 12; }
+static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? 6 : 12; }
 
 static sph_status check_launch(sph_ctx* ctx) {
     cudaError_t e = cudaGetLastError();
@@ -424,7 +434,7 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             sph_destroy(ctx);
             return fail(nullptr, SPH_EINVAL, "rebuild_path = 1 but the rollout does not fit in shared memory");
         }
-        if (want && cudaFuncSetAttribute(k_rebuild_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (want && cudaFuncSetAttribute(k_rebuild_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem) != cudaSuccess) {
             cudaGetLastError();
             want = false;
@@ -672,7 +682,7 @@ sph_status sph_debug_neighbours(sph_ctx* ctx, int rollout, int64_t* nf_off, int3
     D.dbg_idx = ctx->dbg_buf + 3 * (size_t)std::max(P.N, 1);
     // rebuild the cell list of the current state into the other buffer (state untouched)
     k_force_rebin<<<1, 1, 0, s>>>(ctx->D.rs, rollout);
-    launch_rebin(ctx);
+    launch_rebin(ctx, s, true);
     if (P.N > 0) k_debug_neighbours<<<(P.N + 255) / 256, 256, 0, s>>>(P, D, rollout);
     sph_status st = check_launch(ctx);
     if (st) return st;
@@ -715,14 +725,12 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
     // rollouts' densities) or the eight rebuild kernels (multi-kernel path).
     for (int it = 0; it < n_substeps; ++it) {
         cudaEventRecord(ev[0], s);
-        if (ctx->small) {
-            k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
-            k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
-        } else {
-            launch_rebin(ctx);
-        }
+        k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
+        if (ctx->small) k_rebuild_small<false><<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
+        else launch_rebin(ctx);
+        launch_nlist_density(ctx, s);   // (runs after k_density in the step; same work)
         cudaEventRecord(ev[1], s);
-        launch_density(ctx, s,ctx->small ? 1 : 0);
+        launch_density(ctx, s, 1);
         cudaEventRecord(ev[2], s);
         launch_force(ctx, s,1.0f);
         cudaEventRecord(ev[3], s);

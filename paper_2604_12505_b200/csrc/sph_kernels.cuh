@@ -470,6 +470,9 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
 // After the gather, key|perm (8N bytes) is reused for the rollout's positions (float2[N]) and
 // rank for each slot's cell (u16; host guarantees ncell < 65536), so list building and the
 // densities read positions from shared memory.
+// LISTS = false: sort only (production path: lists + densities then run grid-wide in
+// k_nlist_density); LISTS = true: the whole rebuild + densities in this CTA.
+template <bool LISTS>
 __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) {
     extern __shared__ uint32_t smem[];
     __shared__ uint32_t wt[RB_T / 32];
@@ -555,6 +558,11 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
             s_cell[d] = (uint16_t)c;
         }
         __syncthreads();
+        if constexpr (!LISTS) {      // lists + densities follow in k_nlist_density (grid-wide)
+            if (tid == 0) rs->span = 0;
+            __syncthreads();
+            continue;
+        }
         // positions of the new order into shared memory (key|perm are dead now)
         for (int d = tid; d < P.N; d += T) {
             const float4 v = pv1[d];
@@ -579,6 +587,32 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
         for (int i = tid; i < P.N; i += T)
             density_core<false>(P, D, b, i, [&](uint32_t j) { return s_pos[j]; });
         __syncthreads();
+    }
+}
+
+// Neighbour lists + densities of the rollouts in the rebuild work list, grid-wide:
+// grid = (tiles, Y); CTA (x, y) handles tile x of work items y, y + Y, ...  The cell table,
+// slot cells and sorted state come from the sort (k_rebuild_small<false> or the grid-wide
+// rebuild kernels); the list just written by a thread is read back by the same thread.
+__global__ void __launch_bounds__(TILE) k_nlist_density(DevParams P, DevPtrs D) {
+    const int count = *D.rcount;
+    const int i = blockIdx.x * TILE + threadIdx.x;
+    for (int w = blockIdx.y; w < count; w += gridDim.y) {
+        const int b = D.rlist[w];
+        RolloutState* rs = D.rs + b;
+        const size_t o = (size_t)b * P.N;
+        const float4* __restrict__ pv = D.pv[rs->sp ^ 1] + o;   // sorted (rebuilt) buffer
+        auto pos = [&](uint32_t j) {
+            const float4 v = __ldg(pv + j);
+            return make_float2(v.x, v.y);
+        };
+        int span = 0;
+        if (i < P.N) {
+            span = build_list_core(P, D, b, i, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], pos);
+            density_core<false>(P, D, b, i, pos);
+        }
+        span = __reduce_max_sync(0xffffffffu, span);
+        if ((threadIdx.x & 31) == 0 && span > 0) atomicMax(&rs->span, span);
     }
 }
 
