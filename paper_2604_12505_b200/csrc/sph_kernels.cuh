@@ -242,6 +242,29 @@ __device__ __forceinline__ T ld(const T* p) {
     else return *p;
 }
 
+// Wall term gamma1 sum_g W_cb(r_ig) (Eq. density_update), EOS, and the (rho, P/rho^2) store,
+// given the fluid sum wf (self term included, in units of C/h^2).
+__device__ __forceinline__ void finish_density(const DevParams& P, const DevPtrs& D, int b, int i,
+                                               float2 xi, float wf) {
+    float wg = 0.0f;
+    const Geom gm = D.geom[b];
+    const float4* gst = D.gst + (size_t)b * P.G;
+    const float2* glo = D.glo + (size_t)b * P.G;
+    for_ghost_candidates(P, gm, xi, P.ghost_K, P.wall_r2, [&](int g) {
+        const float4 xg = __ldg(gst + g);
+        const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
+        if (dist2(dx, dy) < P.H2) {
+            const float2 lo = __ldg(glo + g);
+            const float ex = dx - lo.x, ey = dy - lo.y;
+            const float r2 = ex * ex + ey * ey;
+            wg += wcb_poly(r2 > 0.0f ? r2 * rsqrtf(r2) * P.inv_h : 0.0f);
+        }
+    });
+    const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
+    const float pr = P.k * (rho - P.rho0);
+    D.aux[(size_t)b * P.N + i] = make_float2(rho, __fdividef(pr, rho * rho));
+}
+
 // Density + EOS of slot i of rollout b.  pos(j) returns the (x, y) of slot j of the rollout
 // (global state buffer, or the shared-memory copy inside k_rebuild_small).
 template <bool NC, class PosF>
@@ -269,23 +292,7 @@ __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& 
         for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), ld<NC>(D.skey + o + i),
                             [&](uint32_t j) { wf += w_masked(P, xi, as4(pos(j)), j != (uint32_t)i); });
     }
-    float wg = 0.0f;
-    const Geom gm = D.geom[b];
-    const float4* gst = D.gst + (size_t)b * P.G;
-    const float2* glo = D.glo + (size_t)b * P.G;
-    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), P.ghost_K, P.wall_r2, [&](int g) {
-        const float4 xg = __ldg(gst + g);
-        const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
-        if (dist2(dx, dy) < P.H2) {
-            const float2 lo = __ldg(glo + g);
-            const float ex = dx - lo.x, ey = dy - lo.y;
-            const float r2 = ex * ex + ey * ey;
-            wg += wcb_poly(r2 > 0.0f ? r2 * rsqrtf(r2) * P.inv_h : 0.0f);
-        }
-    });
-    const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
-    const float pr = P.k * (rho - P.rho0);
-    D.aux[o + i] = make_float2(rho, __fdividef(pr, rho * rho));
+    finish_density(P, D, b, i, p, wf);
 }
 
 template <bool NC>
@@ -400,51 +407,68 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_plan(DevParams P, DevPtrs D,
 
 // neighbour candidate list of slot i (see k_nlist) from a given cell-start table
 // Returns max |j - i| over the list entries (the staging window of k_density / k_force).
-template <class PosF>
+// DENS = true also accumulates the fluid density sum of the appended (2h + skin) candidates
+// that lie within 2h into *wf (self term included); on list overflow *wf is not valid.
+template <bool DENS = false, class PosF>
 __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs& D, int b, int i,
-                                               const uint32_t* cs, uint32_t cell, PosF&& pos) {
+                                               const uint32_t* cs, uint32_t cell, PosF&& pos,
+                                               float* wf_out = nullptr) {
     const size_t o = (size_t)b * P.N;
     const float2 xi = pos((uint32_t)i);
     uint2* nq = D.nbr + (size_t)b * KQ * P.N + i;
-    int n = 0, span = 0;
-    uint32_t acc0 = 0u, acc1 = 0u;
-    // SIMT-friendly: a branch-free hit mask over up to 32 candidates of a cell-row segment,
-    // then only the set bits are appended (ascending j, the same order as a plain scan).
+    int n = 0, first = 0, last = 0;
+    bool ovf = false;
+    uint64_t acc = 0;           // the last four offsets, oldest in the low 16 bits
+    float wf = 4.0f;            // self term W_cb(0)
+    // SIMT-friendly: a branch-free hit mask over up to 32 candidates of a cell-row segment
+    // (shift-in, bit 0 = last candidate), then only the set bits are appended, highest bit
+    // first (= ascending j, the order of a plain scan).
     const int cy = (int)cell / P.nx, cx = (int)cell - cy * P.nx;
-    for (int dy = -1; dy <= 1; ++dy) {
+    for (int dy = -1; dy <= 1 && !ovf; ++dy) {
         const int c0 = (cy + dy) * P.nx + cx - 1;
         const int j0 = (int)cs[c0], j1 = (int)cs[c0 + 3];
-        for (int base = j0; base < j1; base += 32) {
+        for (int base = j0; base < j1 && !ovf; base += 32) {
             const int cnt = min(32, j1 - base);
             uint32_t m = 0u;
             for (int k = 0; k < cnt; ++k) {
                 const float2 xj = pos((uint32_t)(base + k));
                 const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-                m |= (base + k != i && r2 < P.RL2) ? (1u << k) : 0u;
+                m = (m << 1) | (r2 < P.RL2 ? 1u : 0u);
             }
-            while (m != 0u && n != NL_OVERFLOW) {
-                const int k = __ffs(m) - 1;
-                m &= m - 1u;
-                const int off = base + k - i;
-                if (n >= KMAX || off < -32768 || off > 32767) {
-                    n = NL_OVERFLOW;
+            const int self = i - base;
+            if (self >= 0 && self < cnt) m &= ~(1u << (cnt - 1 - self));
+            while (m != 0u) {
+                const int p = 31 - __clz(m);
+                m ^= 1u << p;
+                const int j = base + cnt - 1 - p;
+                const int off = j - i;
+                if (n >= KMAX || (unsigned)(off + 32768) > 65535u) {
+                    ovf = true;
                     break;
                 }
-                span = max(span, abs(off));
-                const uint32_t bits = (uint32_t)(uint16_t)(int16_t)off << (16 * (n & 1));
-                if (n & 2) acc1 |= bits;
-                else acc0 |= bits;
-                ++n;
-                if ((n & 3) == 0) {
-                    nq[(size_t)((n >> 2) - 1) * P.N] = make_uint2(acc0, acc1);
-                    acc0 = acc1 = 0u;
+                first = n == 0 ? off : first;
+                last = off;
+                acc = (acc >> 16) | ((uint64_t)(uint16_t)(int16_t)off << 48);
+                if ((++n & 3) == 0) {
+                    *nq = make_uint2((uint32_t)acc, (uint32_t)(acc >> 32));
+                    nq += P.N;
+                }
+                if (DENS) {
+                    const float2 xj = pos((uint32_t)j);
+                    const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+                    const float w = wcb_poly(r2 * rsqrtf(fmaxf(r2, 1e-30f)) * P.inv_h);
+                    wf += r2 < P.H2 ? w : 0.0f;
                 }
             }
         }
     }
-    if (n != NL_OVERFLOW && (n & 3)) nq[(size_t)(n >> 2) * P.N] = make_uint2(acc0, acc1);
-    D.ncnt[o + i] = (uint8_t)n;
-    return n == NL_OVERFLOW ? 0 : span;   // overflowed particles read global memory
+    if (!ovf && (n & 3)) {   // last partial quad: align to the low lanes, pad with 0 (= self)
+        acc >>= 16 * (4 - (n & 3));
+        *nq = make_uint2((uint32_t)acc, (uint32_t)(acc >> 32));
+    }
+    D.ncnt[o + i] = (uint8_t)(ovf ? NL_OVERFLOW : n);
+    if (DENS && wf_out) *wf_out = wf;
+    return ovf ? -1 : max(-first, last);   // entries ascend in j: first = min, last = max
 }
 
 __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
@@ -608,8 +632,11 @@ __global__ void __launch_bounds__(TILE) k_nlist_density(DevParams P, DevPtrs D) 
         };
         int span = 0;
         if (i < P.N) {
-            span = build_list_core(P, D, b, i, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], pos);
-            density_core<false>(P, D, b, i, pos);
+            float wf;
+            span = build_list_core<true>(P, D, b, i, D.cstart + (size_t)b * (P.ncell + 1),
+                                         D.skey[o + i], pos, &wf);
+            if (span >= 0) finish_density(P, D, b, i, pos((uint32_t)i), wf);
+            else density_core<false>(P, D, b, i, pos);   // list overflow: cell-scan density
         }
         span = __reduce_max_sync(0xffffffffu, span);
         if ((threadIdx.x & 31) == 0 && span > 0) atomicMax(&rs->span, span);
