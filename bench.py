@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--rebin-every", type=int, default=0,
                     help="1: rebuild cell list + neighbour lists every substep; 0: adaptive (skin)")
     ap.add_argument("--skin", type=float, default=0.1, help="Verlet skin in units of h (adaptive)")
-    ap.add_argument("--settle-seconds", type=float, default=2.0)
+    ap.add_argument("--settle-seconds", type=float, default=4.0,
+                    help="damped settle of the initial tank (reading A17; ell=4 needs >= 4 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-substeps", type=int, default=20)
     return ap.parse_args()
@@ -134,7 +135,8 @@ def make_workload(name):
 def settle_on_gpu(t, seconds, device):
     """Damped settle (reading A17) of one tank on the GPU (product path, untimed)."""
     from paper_2604_12505_b200 import SphContext
-    ctx = SphContext(t.params, t.pv32(), t.ghost_b, n_rollouts=1, device=device)
+    ctx = SphContext(t.params, t.pv32(), t.ghost_b, n_rollouts=1, device=device, rebin_every=0,
+                     skin=0.1 * t.params.h)
     n = int(round(seconds / t.params.dt))
     ctx.settle(math.exp(-10.0 * t.params.dt), n)
     pv = ctx.get_particles(0)
@@ -142,7 +144,12 @@ def settle_on_gpu(t, seconds, device):
     ctx.close()
     if st[0] != 0:
         raise RuntimeError(f"settle failed with status {st[0]}")
+    SETTLE_INFO["residual_max_speed"] = float(np.abs(pv[:, 2:]).max())
+    SETTLE_INFO["seconds"] = seconds
     return pv
+
+
+SETTLE_INFO = {}
 
 
 def inputs_for(global_ids, K):
@@ -383,7 +390,7 @@ def run_ours(a):
                    "dt": sp.dt, "rebin_every": a.rebin_every, "skin_h": a.skin,
                    "parallelism": f"ensemble dp{world}",
                    "l2": f"no flush: working set {ctx_bytes_gb(t, B):.2f} GB > 126 MB L2",
-                   "failed_rollouts": n_failed, "gather_ms": gather_ms,
+                   "failed_rollouts": n_failed, "gather_ms": gather_ms, "settle": SETTLE_INFO,
                    "substeps_per_rebuild": float(steps_done.mean() / max(rebuilds.mean(), 1)),
                    "y_checksum": y_checksum},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 3 * 4,

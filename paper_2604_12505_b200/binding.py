@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsphb200.so")
+LIB_PATH = os.environ.get("SPH_LIB_PATH") or os.path.join(_HERE, "libsphb200.so")
 
 SPH_OK, SPH_EINVAL, SPH_ENOMEM, SPH_ECUDA, SPH_EBLOWUP, SPH_ESTATE = 0, 1, 2, 3, 4, 6
 TIMER_NAMES = ["rebuild", "density", "force", "body", "substep"]
