@@ -212,11 +212,12 @@ static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding) {
     else k_density<false><<<gp, TILE, 0, s>>>(P, ctx->D, skip_rebuilding);
 }
 
-static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping) {
+// mode: 0 all rollouts, 1 non-rebuilding rollouts, 2 rebuilt rollouts (work list)
+static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode = 0) {
     const DevParams& P = ctx->P;
-    dim3 gp(P.ntile, P.B);
-    if (P.stage) k_force<true><<<gp, TILE, force_smem(P), s>>>(P, ctx->D, damping);
-    else k_force<false><<<gp, TILE, 0, s>>>(P, ctx->D, damping);
+    dim3 gp(P.ntile, mode == 2 ? std::min(P.B, 64) : P.B);
+    if (P.stage) k_force<true><<<gp, TILE, force_smem(P), s>>>(P, ctx->D, damping, mode);
+    else k_force<false><<<gp, TILE, 0, s>>>(P, ctx->D, damping, mode);
 }
 
 static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0) {
@@ -291,14 +292,15 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
-    if (ctx->small) {
+    if (ctx->small) {   // (forces are launched by launch_substep, see there)
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
         cudaEventRecord(ctx->ev_fork, s);
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
         k_rebuild_small<false><<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
+        launch_nlist_density(ctx, ctx->side);
         cudaEventRecord(ctx->ev_join, ctx->side);
         launch_density(ctx, s, 1);
-        cudaStreamWaitEvent(s, ctx->ev_join, 0);
+        return cudaSuccess;
     } else {
         if (capturing) {
             cudaError_t e = add_conditional_rebin(ctx);
@@ -318,14 +320,23 @@ static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool cap
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
     cudaError_t e = launch_rebuild_and_density(ctx, capturing);
-    launch_force(ctx, s,damping);
-    launch_body(ctx, s,pin, ctx->ghost_angle0);
+    if (ctx->small) {
+        // The rebuild branch (sort -> lists + densities of the rebuilt rollouts) runs on the side
+        // stream concurrently with density AND forces of every other rollout; only the forces
+        // of the rebuilt rollouts wait for it.
+        launch_force(ctx, s, damping, 1);
+        cudaStreamWaitEvent(s, ctx->ev_join, 0);
+        launch_force(ctx, s, damping, 2);
+    } else {
+        launch_force(ctx, s, damping, 0);
+    }
+    launch_body(ctx, s, pin, ctx->ghost_angle0);
     return e;
 }
 
 // kernels per substep: small path 5 (plan, rebuild_small, density, force, body); multi-kernel
 // path 4 + 8 rebuild kernels (the 8 run only in substeps where some rollout rebuilds).
-static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? 6 : 12; }
+static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? 7 : 12; }
 
 static sph_status check_launch(sph_ctx* ctx) {
     cudaError_t e = cudaGetLastError();

@@ -713,14 +713,14 @@ __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __re
 #endif
 // dynamic shared memory: pv[MAXSTAGE] float4 | aux[MAXSTAGE + 2] float2 (TMA-staged window)
 template <bool STAGE>
-__global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, DevPtrs D, float damping) {
+__device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D, float damping,
+                                           int b, int tile) {
     extern __shared__ float4 s_pv[];
     float2* s_aux = reinterpret_cast<float2*>(s_pv + MAXSTAGE);
     __shared__ __align__(8) uint64_t bar;
-    const int b = blockIdx.y;
     RolloutState* rs = D.rs + b;
     if (rs->frozen) return;   // CTA-uniform (before any barrier / warp-level collective)
-    const int t0 = blockIdx.x * TILE;
+    const int t0 = tile * TILE;
     const int i = t0 + threadIdx.x;
     const size_t o = (size_t)b * P.N;
     const int cur = rs->sp ^ rs->need_rebin;
@@ -820,8 +820,26 @@ __global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, Dev
         vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
     }
     if ((threadIdx.x & 31) == 0)
-        D.part[(size_t)b * P.npart + blockIdx.x * (TILE / 32) + (threadIdx.x >> 5)] =
+        D.part[(size_t)b * P.npart + tile * (TILE / 32) + (threadIdx.x >> 5)] =
             make_double4(fbx, fby, tq, vmax);
+    if (STAGE) __syncthreads();   // the staging barrier may be re-initialised for the next tile
+}
+
+// mode 0: every rollout (grid.y = B); 1: rollouts that do NOT rebuild this substep (their
+// densities are ready while the rebuild branch still runs); 2: the rebuilt rollouts of the
+// work list (grid.y-stride over it), after the rebuild branch joined.
+template <bool STAGE>
+__global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, DevPtrs D,
+                                                                float damping, int mode) {
+    if (mode == 2) {
+        const int count = *D.rcount;
+        for (int w = blockIdx.y; w < count; w += gridDim.y)
+            force_tile<STAGE>(P, D, damping, D.rlist[w], blockIdx.x);
+        return;
+    }
+    const int b = blockIdx.y;
+    if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
+    force_tile<STAGE>(P, D, damping, b, blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------------------
