@@ -274,13 +274,16 @@ __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& 
     const float2 p = pos((uint32_t)i);
     const float4 xi = make_float4(p.x, p.y, 0.f, 0.f);
     float wf = 4.0f;   // self term W_cb(0) ("all particles"): (2-0)^3 - 4 (1-0)^3 = 4
+    const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
+    uint2 wn = ld<NC>(nq);   // first offsets, independent of the count load; then the next
+                             // quad's offsets stay in flight while this one is evaluated
     const int n = ld<NC>(D.ncnt + o + i);
     auto as4 = [](float2 v) { return make_float4(v.x, v.y, 0.f, 0.f); };
     if (n != NL_OVERFLOW) {
-        const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
         for (int k = 0; k < n; k += 4) {
-            const uint2 w = ld<NC>(nq);
+            const uint2 w = wn;
             nq += P.N;
+            if (k + 4 < n) wn = ld<NC>(nq);
             const float4 x0 = as4(pos((uint32_t)(i + quad_offset(w, 0))));
             const float4 x1 = as4(pos((uint32_t)(i + quad_offset(w, 1))));
             const float4 x2 = as4(pos((uint32_t)(i + quad_offset(w, 2))));
@@ -690,11 +693,13 @@ __device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2
 // state / aux of a slot (shared-memory window or global memory).
 template <class PV, class AX>
 __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __restrict__ nq, int n,
-                                           int i, float4 xi, float2 ai, PV&& pvj, AX&& axj,
-                                           float& sx, float& sy) {
+                                           uint2 q0, int i, float4 xi, float2 ai, PV&& pvj,
+                                           AX&& axj, float& sx, float& sy) {
+    uint2 wn = q0;   // offsets stream from DRAM: keep the next quad's load in flight
     for (int k = 0; k < n; k += 4) {
-        const uint2 w = __ldg(nq);
+        const uint2 w = wn;
         nq += P.N;
+        if (k + 4 < n) wn = __ldg(nq);
         const uint32_t j0 = (uint32_t)(i + quad_offset(w, 0));
         const uint32_t j1 = (uint32_t)(i + quad_offset(w, 1));
         const uint32_t j2 = (uint32_t)(i + quad_offset(w, 2));
@@ -749,13 +754,14 @@ __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D,
         const float4 xi = staged ? s_pv[i - lo] : pv[i];
         const float2 ai = staged ? s_aux[i - lo + ash] : aux[i];
         float sx = 0.0f, sy = 0.0f;   // sum of (-pressure + viscous) * grad W / m^2
-        const int n = D.ncnt[o + i];
         const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
+        const uint2 q0 = __ldg(nq);            // first offsets, independent of the count load
+        const int n = D.ncnt[o + i];
         if (n != NL_OVERFLOW && staged) {
-            force_list(P, nq, n, i, xi, ai, [&](uint32_t j) { return s_pv[j - lo]; },
+            force_list(P, nq, n, q0, i, xi, ai, [&](uint32_t j) { return s_pv[j - lo]; },
                        [&](uint32_t j) { return s_aux[j - lo + ash]; }, sx, sy);
         } else if (n != NL_OVERFLOW) {
-            force_list(P, nq, n, i, xi, ai, [&](uint32_t j) { return __ldg(pv + j); },
+            force_list(P, nq, n, q0, i, xi, ai, [&](uint32_t j) { return __ldg(pv + j); },
                        [&](uint32_t j) { return __ldg(aux + j); }, sx, sy);
         } else {
             for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
