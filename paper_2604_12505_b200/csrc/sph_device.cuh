@@ -157,11 +157,12 @@ __device__ __forceinline__ float dist2(float dx, float dy) {
 }
 
 // Cubic spline (Eq. cubicspline) without its constant C/h^2; q = r/h < 2.
+// (2-q)^3 - 4(1-q)^3 expanded = 4 - 6q^2 + 3q^3 (q < 1); (2-q)^3 (1 <= q < 2).
 __device__ __forceinline__ float wcb_poly(float q) {
-    float a = 2.0f - q, b = 1.0f - q;
-    float w = a * a * a;
-    if (q < 1.0f) w -= 4.0f * b * b * b;
-    return w;
+    const float a = 2.0f - q;
+    const float inner = fmaf(q * q, fmaf(3.0f, q, -6.0f), 4.0f);
+    const float outer = a * a * a;
+    return q < 1.0f ? inner : outer;
 }
 
 // dW/dq of the cubic spline without C/h^3.
