@@ -286,11 +286,14 @@ __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& 
             if (k + 4 < n) wn = ld<NC>(nq);
             const float4 x0 = as4(pos((uint32_t)(i + quad_offset(w, 0))));
             const float4 x1 = as4(pos((uint32_t)(i + quad_offset(w, 1))));
-            const float4 x2 = as4(pos((uint32_t)(i + quad_offset(w, 2))));
-            const float4 x3 = as4(pos((uint32_t)(i + quad_offset(w, 3))));
-            wf += (w_list(P, xi, x0) + w_list(P, xi, x1)) + (w_list(P, xi, x2) + w_list(P, xi, x3));
+            wf += w_list(P, xi, x0) + w_list(P, xi, x1);
+            if (k + 2 < n) {   // pairs granularity (see force_list)
+                const float4 x2 = as4(pos((uint32_t)(i + quad_offset(w, 2))));
+                const float4 x3 = as4(pos((uint32_t)(i + quad_offset(w, 3))));
+                wf += w_list(P, xi, x2) + w_list(P, xi, x3);
+            }
         }
-        wf -= 4.0f * (float)(((n + 3) & ~3) - n);   // padding entries (self) added W(0) = 4 each
+        wf -= 4.0f * (float)(((n + 1) & ~1) - n);   // padding entries (self) added W(0) = 4 each
     } else {
         for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), ld<NC>(D.skey + o + i),
                             [&](uint32_t j) { wf += w_masked(P, xi, as4(pos(j)), j != (uint32_t)i); });
@@ -700,16 +703,22 @@ __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __re
         const uint2 w = wn;
         nq += P.N;
         if (k + 4 < n) wn = __ldg(nq);
+        // pairs granularity: the second half of a quad only when some lane of the warp needs it
+        // (padding entries are the particle itself: exact zero contribution)
         const uint32_t j0 = (uint32_t)(i + quad_offset(w, 0));
         const uint32_t j1 = (uint32_t)(i + quad_offset(w, 1));
-        const uint32_t j2 = (uint32_t)(i + quad_offset(w, 2));
-        const uint32_t j3 = (uint32_t)(i + quad_offset(w, 3));
-        const float4 x0 = pvj(j0), x1 = pvj(j1), x2 = pvj(j2), x3 = pvj(j3);
-        const float2 a0 = axj(j0), a1 = axj(j1), a2 = axj(j2), a3 = axj(j3);
-        pair_force(P, xi, ai, x0, a0, sx, sy);   // padding entries are the particle
-        pair_force(P, xi, ai, x1, a1, sx, sy);   // itself: exact zero contribution
-        pair_force(P, xi, ai, x2, a2, sx, sy);
-        pair_force(P, xi, ai, x3, a3, sx, sy);
+        const float4 x0 = pvj(j0), x1 = pvj(j1);
+        const float2 a0 = axj(j0), a1 = axj(j1);
+        pair_force(P, xi, ai, x0, a0, sx, sy);
+        pair_force(P, xi, ai, x1, a1, sx, sy);
+        if (k + 2 < n) {
+            const uint32_t j2 = (uint32_t)(i + quad_offset(w, 2));
+            const uint32_t j3 = (uint32_t)(i + quad_offset(w, 3));
+            const float4 x2 = pvj(j2), x3 = pvj(j3);
+            const float2 a2 = axj(j2), a3 = axj(j3);
+            pair_force(P, xi, ai, x2, a2, sx, sy);
+            pair_force(P, xi, ai, x3, a3, sx, sy);
+        }
     }
 }
 
