@@ -723,7 +723,7 @@ __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __re
 }
 
 #ifndef SPH_FORCE_MINB
-#define SPH_FORCE_MINB 5
+#define SPH_FORCE_MINB 6   // 40 registers: occupancy beats the small spill (measured sweep 3..8)
 #endif
 // dynamic shared memory: pv[MAXSTAGE] float4 | aux[MAXSTAGE + 2] float2 (TMA-staged window)
 template <bool STAGE>
