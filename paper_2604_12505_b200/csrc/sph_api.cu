@@ -175,6 +175,7 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     put(d.id[1], BN * 4);
     put(d.aux, BN * 8 + 16);   // +1 element: the force kernel's 16-B aligned TMA slice
     put(d.skey, BN * 4);
+    put(d.xb, BN * 8);
     put(d.nbr, BN * KQ * 8);
     put(d.ncnt, BN);
     put(d.key, BN * 4);

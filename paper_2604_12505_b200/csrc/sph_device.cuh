@@ -72,6 +72,7 @@ struct RolloutState {
     float disp;          // bound on any particle's displacement relative to the body
                          // translation since the last rebuild
     int span;            // max |j - i| over all neighbour-list entries (staging window)
+    float rbx, rby;      // body position (float) at the last rebuild
 };
 
 struct Geom {            // float copy of the body state used by the particle kernels
@@ -85,6 +86,7 @@ struct DevPtrs {
     uint32_t* id[2];     // [B][N] canonical id of each slot
     float2* aux;         // [B][N] (rho, P / rho^2)
     uint32_t* skey;      // [B][N] cell of each slot at the last rebuild
+    float2* xb;          // [B][N] position of each slot at the last rebuild (Verlet criterion)
     uint2* nbr;          // [B][KQ][N] neighbour candidates: 4 int16 slot offsets j - i per uint2
     uint8_t* ncnt;       // [B][N] list length (NL_OVERFLOW: scan the cells instead)
     uint32_t* key;       // [B][N] rebuild scratch: cell of each (unsorted) slot

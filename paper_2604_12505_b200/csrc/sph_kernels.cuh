@@ -14,7 +14,11 @@ __global__ void __launch_bounds__(TILE) k_hash(DevParams P, DevPtrs D) {
     RolloutState* rs = D.rs + b;
     if (rs->frozen || !rs->need_rebin) return;
     const int i = blockIdx.x * TILE + threadIdx.x;
-    if (i == 0) rs->span = 0;   // recomputed by k_nlist (kernel boundary orders the atomics)
+    if (i == 0) {
+        rs->span = 0;           // recomputed by k_nlist (kernel boundary orders the atomics)
+        rs->rbx = D.geom[b].rx; // body position at this rebuild (Verlet criterion)
+        rs->rby = D.geom[b].ry;
+    }
     if (i >= P.N) return;
     const size_t o = (size_t)b * P.N;
     const float4 x = D.pv[rs->sp][o + i];
@@ -202,6 +206,8 @@ __global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) {
     D.pv[sp ^ 1][o + d] = D.pv[sp][o + src];
     D.id[ip ^ 1][o + d] = D.id[ip][o + src];
     D.skey[o + d] = D.key[o + src];
+    const float4 x = D.pv[sp ^ 1][o + d];
+    D.xb[o + d] = make_float2(x.x, x.y);   // positions at this rebuild (Verlet criterion)
 }
 
 // ---------------------------------------------------------------------------------------
@@ -581,15 +587,21 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
         // 5. gather into cell order (slot cells kept as u16 in the rank area)
         for (int d = tid; d < P.N; d += T) {
             const uint32_t src = s_perm[d];
-            pv1[d] = pv0[src];
+            const float4 v = pv0[src];
+            pv1[d] = v;
             id1[d] = id0[src];
             const uint32_t c = s_key[src];
             D.skey[o + d] = c;
+            D.xb[o + d] = make_float2(v.x, v.y);   // positions at this rebuild (Verlet)
             s_cell[d] = (uint16_t)c;
         }
         __syncthreads();
         if constexpr (!LISTS) {      // lists + densities follow in k_nlist_density (grid-wide)
-            if (tid == 0) rs->span = 0;
+            if (tid == 0) {
+                rs->span = 0;
+                rs->rbx = gm.rx;     // body position at this rebuild (Verlet criterion)
+                rs->rby = gm.ry;
+            }
             __syncthreads();
             continue;
         }
@@ -817,9 +829,12 @@ __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D,
         xn.z *= damping;
         xn.w *= damping;
         D.pv[cur ^ 1][o + i] = xn;
-        // speed relative to the body translation (bounds the drift of inter-particle vectors)
-        const float rvx = xn.z - gm.vx, rvy = xn.w - gm.vy;
-        vmax = sqrtf(rvx * rvx + rvy * rvy);
+        // Verlet criterion on actual displacements: displacement since the last rebuild
+        // relative to the body translation since then (k_body adds this step's body drift).
+        // vmax carries the squared displacement through the reductions.
+        const float2 xb = __ldg(D.xb + o + i);
+        const float ddx = (xn.x - xb.x) - (gm.rx - rs->rbx), ddy = (xn.y - xb.y) - (gm.ry - rs->rby);
+        vmax = ddx * ddx + ddy * ddy;
         const bool finite = isfinite(xn.x) && isfinite(xn.y) && isfinite(xn.z) && isfinite(xn.w);
         if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || fabsf(xn.z) > 1e9f ||
             fabsf(xn.w) > 1e9f)
@@ -944,8 +959,11 @@ __global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
         rs->rebuilds += nr;
         // drift of any particle relative to the body translation in this substep:
         // dt |v_i' - rdot_n'| <= dt (|v_i' - rdot_n| + dt |rddot|)
-        const double d = P.dtd * (f.w + P.dtd * sqrt(ax * ax + ay * ay));
-        rs->disp = (float)(nr ? d : (double)rs->disp + d);
+        // max over particles of |(x_i - x_i^build) - (r_n - r^build)| (from k_force) plus the
+        // body's drift in this substep: a strict bound on every particle's displacement
+        // relative to the body translation since the last rebuild (Verlet criterion)
+        const double d = sqrt(f.w) + P.dtd * sqrt(body[3] * body[3] + body[4] * body[4]);
+        rs->disp = (float)d;
         rs->need_rebin = P.rebin_every ? 1 : (rs->disp >= P.rebuild_disp ? 1 : 0);
         rs->step += 1;
         if (rs->status) rs->frozen = 1;
