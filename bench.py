@@ -53,7 +53,9 @@ def parse():
     ap.add_argument("--rollouts", type=int, default=0, help="override rollouts per GPU")
     ap.add_argument("--rebin-every", type=int, default=0,
                     help="1: rebuild cell list + neighbour lists every substep; 0: adaptive (skin)")
-    ap.add_argument("--skin", type=float, default=0.1, help="Verlet skin in units of h (adaptive)")
+    ap.add_argument("--skin", type=float, default=0.15, help="Verlet skin in units of h (adaptive)")
+    ap.add_argument("--live-every", type=int, default=4,
+                    help="live kernel timing: event nodes every N-th substep of the timed ticks (0 = off)")
     ap.add_argument("--settle-seconds", type=float, default=4.0,
                     help="damped settle of the initial tank (reading A17; ell=4 needs >= 4 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -307,11 +309,16 @@ def run_ours(a):
     u_dev = torch.from_numpy(u_host).to(dev)
     y_dev = torch.empty((B, K_all, 6), dtype=torch.float32, device=dev)
     ua_dev = torch.empty((B, K_all, 3), dtype=torch.float32, device=dev)
+    # live kernel timing: event-record nodes in the tick graph around density / force of every
+    # LIVE_EVERY-th substep of the timed rollout (enabled before the warm-up, which captures
+    # the graph; accumulators reset after it)
+    ctx.set_live_timing(a.live_every)
     # warm-up (also captures the per-tick CUDA graph)
     if a.warmup:
         ctx.rollout(u_dev[:, :a.warmup].contiguous(), y_out=y_dev[:, :a.warmup].contiguous(),
                     u_applied=ua_dev[:, :a.warmup].contiguous())
     torch.cuda.synchronize(dev)
+    ctx.live_timing(reset=True)
     u_timed = u_dev[:, a.warmup:].contiguous()
     y_timed = torch.empty((B, a.steps, 6), dtype=torch.float32, device=dev)
     ua_timed = torch.empty((B, a.steps, 3), dtype=torch.float32, device=dev)
@@ -322,14 +329,18 @@ def run_ours(a):
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")   # ncu --nvtx-include "timed/" selects these launches
     e0.record(ctx.stream)
     ctx.rollout(u_timed, y_out=y_timed, u_applied=ua_timed)
     e1.record(ctx.stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     ck = clocks.stop()
     ms = e0.elapsed_time(e1)
+    live = ctx.live_timing(reset=True)
+    ctx.set_live_timing(0)
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -375,18 +386,26 @@ def run_ours(a):
     # ---- per-kernel device times (CUDA events on the context stream, same data) -----------
     prof = ctx.profile(a.profile_substeps)
     kern = {k: v for k, v in prof.items() if k != "substep"}
-    top = max(("density", "force"), key=lambda k: kern[k])
+    # dominant kernel and its duration per substep: live in-graph events of the timed region
+    # (k_force = the sum of its launches in a substep); isolated timings as context
+    if live["samples"]:
+        top = max(("density", "force"), key=lambda k: live[k])
+        kms, kms_src = live[top], f"live: CUDA event nodes in the timed tick graph, every {a.live_every}th substep ({live['samples']} samples)"
+    else:
+        top = max(("density", "force"), key=lambda k: kern[k])
+        kms, kms_src = kern[top], "isolated: sph_profile_substeps after the timed region"
     alg = algorithmic_bytes(top, t.n_fluid, t.n_ghost, B)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
-    achieved = alg / (kern[top] / 1e3) / 1e9
+    achieved = alg / (kms / 1e3) / 1e9
     roof = {"bound": "hbm", "kernel": f"k_{top}", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic_from_profiles(top, name),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6.65 TB/s",
-            "algorithmic_bytes_per_launch": alg, "kernel_ms": kern[top],
-            "kernel_share_of_substep": kern[top] / prof["substep"],
-            "kernel_ms_all": kern, "substep_ms_profiled": prof["substep"]}
+            "algorithmic_bytes_per_launch": alg, "kernel_ms": kms, "kernel_ms_source": kms_src,
+            "kernel_share_of_substep": kms / live["substep"] if live["samples"] else kms / prof["substep"],
+            "live_ms": {k: live[k] for k in ("density", "force", "substep")},
+            "isolated_ms": kern, "substep_ms_isolated": prof["substep"]}
     launches = a.steps * (1 + sp.n_sub * ctx.launches_per_substep())
     ctx.close()
     if rank != 0:
@@ -401,7 +420,7 @@ def run_ours(a):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (body f64)",
-        "data": "synthetic (seeded lattice tank, GPU damped settle, multisine+pulse excitation)",
+        "data": "synthetic (seeded lattice tank, " + ("oracle-settled snapshot" if SETTLE_INFO.get("source", "").startswith("bench_data") else "GPU damped settle") + ", multisine+pulse excitation)",
         "config": {"workload": desc, "rollouts_per_gpu": B, "fluid_per_rollout": t.n_fluid,
                    "ghosts_per_rollout": t.n_ghost, "substeps_per_step": sp.n_sub,
                    "dt": sp.dt, "rebin_every": a.rebin_every, "skin_h": a.skin,

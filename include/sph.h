@@ -170,6 +170,19 @@ enum {
 };
 sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms);
 
+/* Live kernel timing inside sph_rollout_batch (the production path, CUDA graph included).
+ * every > 0: the tick graph is re-captured with event-record nodes around the density launch,
+ * the force launch(es) and the whole substep of every `every`-th substep; after each tick the
+ * host synchronises the context stream (one host round trip per tick) and adds the elapsed
+ * times to accumulators.  every = 0 disables it (graph re-captured without the nodes).
+ * sph_get_live_timing writes the sums in ms over the sampled substeps into
+ * ms_sum[SPH_NUM_LIVE] (order SPH_LIVE_*) and their count into *n_samples (nullable);
+ * reset != 0 zeroes the accumulators afterwards.  In the small-rollout path the density and
+ * the first force launch overlap the rebuild branch, so these are in-situ durations. */
+enum { SPH_LIVE_DENSITY = 0, SPH_LIVE_FORCE = 1, SPH_LIVE_SUBSTEP = 2, SPH_NUM_LIVE = 3 };
+sph_status sph_set_live_timing(sph_ctx* ctx, int every);
+sph_status sph_get_live_timing(sph_ctx* ctx, double* ms_sum, int64_t* n_samples, int reset);
+
 /* Per-rollout counters (host arrays of B, nullable): substeps taken and cell-list / neighbour-
  * list rebuilds performed (with rebin_every = 0 rebuilds happen only when the displacement
  * bound requires them). */

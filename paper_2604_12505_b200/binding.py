@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("SPH_LIB_PATH") or os.path.join(_HERE, "libsphb200.so"
 
 SPH_OK, SPH_EINVAL, SPH_ENOMEM, SPH_ECUDA, SPH_EBLOWUP, SPH_ESTATE = 0, 1, 2, 3, 4, 6
 TIMER_NAMES = ["rebuild", "density", "force", "body", "substep"]
+LIVE_NAMES = ["density", "force", "substep"]   # SPH_LIVE_* order
 
 
 class FluidParams(C.Structure):
@@ -68,6 +69,8 @@ def lib():
             "sph_debug_cells": (i32, [vp, i32, vp, vp]),
             "sph_debug_neighbours": (i32, [vp, i32, vp, vp, i64, vp, vp, i64, vp, vp, i64]),
             "sph_profile_substeps": (i32, [vp, i32, vp]),
+            "sph_set_live_timing": (i32, [vp, i32]),
+            "sph_get_live_timing": (i32, [vp, vp, vp, i32]),
             "sph_launches_per_substep": (i32, [vp]),
             "sph_get_counters": (i32, [vp, vp, vp]),
             "sph_get_sizes": (None, [vp, vp, vp, vp, vp]),
@@ -86,7 +89,8 @@ def exported_symbols():
     return ["sph_workspace_bytes", "sph_init_tank", "sph_set_state", "sph_set_body_state",
             "sph_get_particles", "sph_get_ghosts", "sph_step", "sph_rollout_batch",
             "sph_get_body_state", "sph_settle", "sph_get_status", "sph_debug_cells",
-            "sph_debug_neighbours", "sph_profile_substeps", "sph_launches_per_substep", "sph_get_counters",
+            "sph_debug_neighbours", "sph_profile_substeps", "sph_set_live_timing", "sph_get_live_timing",
+            "sph_launches_per_substep", "sph_get_counters",
             "sph_get_sizes", "sph_last_error", "sph_destroy"]
 
 
@@ -286,6 +290,22 @@ class SphContext:
         self._check(self.L.sph_profile_substeps(self.ctx, int(n_substeps), ms.ctypes.data),
                     "sph_profile_substeps")
         return dict(zip(TIMER_NAMES, ms.tolist()))
+
+    def set_live_timing(self, every: int):
+        """Event-record nodes in the tick graph around density / force / substep of every
+        `every`-th substep (0 = off); see sph_set_live_timing."""
+        self._check(self.L.sph_set_live_timing(self.ctx, int(every)), "sph_set_live_timing")
+
+    def live_timing(self, reset: bool = True):
+        """Mean in-situ ms per sampled substep: {"density", "force", "substep", "samples"}."""
+        ms = np.zeros(len(LIVE_NAMES), np.float64)
+        n = np.zeros(1, np.int64)
+        self._check(self.L.sph_get_live_timing(self.ctx, ms.ctypes.data, n.ctypes.data,
+                                               1 if reset else 0), "sph_get_live_timing")
+        k = int(n[0])
+        out = {name: (float(v) / k if k else None) for name, v in zip(LIVE_NAMES, ms)}
+        out["samples"] = k
+        return out
 
     def counters(self):
         steps = np.zeros(self.B, np.int64)

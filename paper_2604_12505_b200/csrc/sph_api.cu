@@ -38,7 +38,16 @@ struct sph_ctx {
     int small_grid = 0;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // live kernel timing inside the tick graph (sph_set_live_timing): event-record nodes around
+    // the density / force launches of every live_every-th substep, read after each tick
+    int live_every = 0;
+    std::vector<cudaEvent_t> live_ev;   // [sampled substep][LIVE_SLOTS]
+    double live_ms[SPH_NUM_LIVE] = {0, 0, 0};
+    int64_t live_n = 0;
 };
+
+// event slots of one sampled substep
+enum { LV_SUB0 = 0, LV_DEN0, LV_DEN1, LV_F1_0, LV_F1_1, LV_F2_0, LV_F2_1, LV_SUB1, LIVE_SLOTS };
 
 static std::string g_init_err;
 // dynamic shared memory of the neighbour kernels: only with TMA window staging (a reservation
@@ -289,7 +298,13 @@ static cudaError_t add_conditional_rebin(sph_ctx* ctx) {
 // concurrently with k_density for every other rollout (fork/join via events; captured into
 // the tick graph as two parallel branches).  Multi-kernel path: grid-wide rebuild kernels,
 // under an IF node when captured.
-static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
+// Timing mark of a live-timed substep (ev == nullptr: not sampled).  Only used while capturing
+// the tick graph: an external event record becomes an event-record node of the graph.
+static void live_mark(cudaEvent_t* ev, int slot, cudaStream_t s) {
+    if (ev) cudaEventRecordWithFlags(ev[slot], s, cudaEventRecordExternal);
+}
+
+static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cudaEvent_t* ev) {
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
@@ -300,7 +315,9 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
         k_rebuild_small<false><<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
         launch_nlist_density(ctx, ctx->side);
         cudaEventRecord(ctx->ev_join, ctx->side);
+        live_mark(ev, LV_DEN0, s);
         launch_density(ctx, s, 1);
+        live_mark(ev, LV_DEN1, s);
         return cudaSuccess;
     } else {
         if (capturing) {
@@ -310,29 +327,48 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing) {
             k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
             launch_rebin(ctx);
         }
+        live_mark(ev, LV_DEN0, s);
         launch_density(ctx, s, 1);
+        live_mark(ev, LV_DEN1, s);
     }
     launch_nlist_density(ctx, s);
     return cudaSuccess;
 }
 
-static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool capturing = false) {
+// k = substep index inside the captured tick (live timing samples every live_every-th one)
+static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool capturing = false,
+                                  int k = -1) {
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
-    cudaError_t e = launch_rebuild_and_density(ctx, capturing);
+    cudaEvent_t* ev = nullptr;
+    if (capturing && ctx->live_every > 0 && k >= 0 && k % ctx->live_every == 0)
+        ev = ctx->live_ev.data() + (size_t)(k / ctx->live_every) * LIVE_SLOTS;
+    live_mark(ev, LV_SUB0, s);
+    cudaError_t e = launch_rebuild_and_density(ctx, capturing, ev);
     if (ctx->small) {
         // The rebuild branch (sort -> lists + densities of the rebuilt rollouts) runs on the side
         // stream concurrently with density AND forces of every other rollout; only the forces
         // of the rebuilt rollouts wait for it.
+        live_mark(ev, LV_F1_0, s);
         launch_force(ctx, s, damping, 1);
+        live_mark(ev, LV_F1_1, s);
         cudaStreamWaitEvent(s, ctx->ev_join, 0);
+        live_mark(ev, LV_F2_0, s);
         launch_force(ctx, s, damping, 2);
+        live_mark(ev, LV_F2_1, s);
     } else {
+        live_mark(ev, LV_F1_0, s);
         launch_force(ctx, s, damping, 0);
+        live_mark(ev, LV_F1_1, s);
     }
     launch_body(ctx, s, pin, ctx->ghost_angle0);
+    live_mark(ev, LV_SUB1, s);
     return e;
+}
+
+static int live_samples(const sph_ctx* ctx) {
+    return ctx->live_every > 0 ? (ctx->n_sub + ctx->live_every - 1) / ctx->live_every : 0;
 }
 
 // kernels per substep: small path 5 (plan, rebuild_small, density, force, body); multi-kernel
@@ -560,12 +596,63 @@ sph_status sph_step(sph_ctx* ctx, const float* u, int n_substeps, int ptr_on_dev
     return SPH_OK;
 }
 
+static sph_status accumulate_live(sph_ctx* ctx) {
+    auto el = [&](const cudaEvent_t* ev, int a, int b, double* acc) -> cudaError_t {
+        float m = 0.f;
+        cudaError_t e = cudaEventElapsedTime(&m, ev[a], ev[b]);
+        if (e == cudaSuccess) *acc += m;
+        return e;
+    };
+    for (int q = 0; q < live_samples(ctx); ++q) {
+        const cudaEvent_t* ev = ctx->live_ev.data() + (size_t)q * LIVE_SLOTS;
+        CK(el(ev, LV_DEN0, LV_DEN1, &ctx->live_ms[SPH_LIVE_DENSITY]));
+        CK(el(ev, LV_F1_0, LV_F1_1, &ctx->live_ms[SPH_LIVE_FORCE]));
+        if (ctx->small) CK(el(ev, LV_F2_0, LV_F2_1, &ctx->live_ms[SPH_LIVE_FORCE]));
+        CK(el(ev, LV_SUB0, LV_SUB1, &ctx->live_ms[SPH_LIVE_SUBSTEP]));
+        ++ctx->live_n;
+    }
+    return SPH_OK;
+}
+
+sph_status sph_set_live_timing(sph_ctx* ctx, int every) {
+    if (!ctx || every < 0) return SPH_EINVAL;
+    if (every == ctx->live_every) return SPH_OK;
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->tick_graph) {   // re-captured with (or without) the timing nodes on next use
+        cudaGraphExecDestroy(ctx->tick_graph);
+        ctx->tick_graph = nullptr;
+    }
+    for (auto e : ctx->live_ev) cudaEventDestroy(e);
+    ctx->live_ev.clear();
+    ctx->live_every = every;
+    const size_t n = (size_t)live_samples(ctx) * LIVE_SLOTS;
+    for (size_t q = 0; q < n; ++q) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        ctx->live_ev.push_back(e);
+    }
+    for (double& m : ctx->live_ms) m = 0.0;
+    ctx->live_n = 0;
+    return SPH_OK;
+}
+
+sph_status sph_get_live_timing(sph_ctx* ctx, double* ms_sum, int64_t* n_samples, int reset) {
+    if (!ctx || !ms_sum) return SPH_EINVAL;
+    for (int t = 0; t < SPH_NUM_LIVE; ++t) ms_sum[t] = ctx->live_ms[t];
+    if (n_samples) *n_samples = ctx->live_n;
+    if (reset) {
+        for (double& m : ctx->live_ms) m = 0.0;
+        ctx->live_n = 0;
+    }
+    return SPH_OK;
+}
+
 static sph_status capture_tick_graph(sph_ctx* ctx) {
     if (ctx->tick_graph) return SPH_OK;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     cudaError_t ce = cudaSuccess;
-    for (int k = 0; k < ctx->n_sub && ce == cudaSuccess; ++k) ce = launch_substep(ctx, 1.0f, 0, true);
+    for (int k = 0; k < ctx->n_sub && ce == cudaSuccess; ++k) ce = launch_substep(ctx, 1.0f, 0, true, k);
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
     if (ce != cudaSuccess) {
         if (e == cudaSuccess) cudaGraphDestroy(g);
@@ -613,6 +700,11 @@ sph_status sph_rollout_batch(sph_ctx* ctx, const float* u_seq, int K, const sph_
     for (int k = 0; k < K; ++k) {
         k_tick<<<tg, tb, 0, s>>>(P, ctx->D, du, dth, dy, dua, K, k, pd ? 1 : 0, pd ? pd->Kp : 0.0, pd ? pd->Kd : 0.0);
         CK(cudaGraphLaunch(ctx->tick_graph, s));
+        if (ctx->live_every > 0) {   // read this tick's timing nodes before the next launch
+            CK(cudaStreamSynchronize(s));
+            st = accumulate_live(ctx);
+            if (st) return st;
+        }
     }
     st = check_launch(ctx);
     if (st) return st;
@@ -798,6 +890,7 @@ void sph_destroy(sph_ctx* ctx) {
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    for (auto e : ctx->live_ev) cudaEventDestroy(e);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

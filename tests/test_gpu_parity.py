@@ -208,6 +208,28 @@ def test_graph_rollout_equals_direct_steps(settled_c1):
     b.close()
 
 
+@pytest.mark.parametrize("path", [1, 2])
+def test_live_timing_nodes_do_not_change_results(settled_c1, path):
+    """Event-record nodes in the tick graph (bench's live kernel timing) leave the trajectory
+    bitwise unchanged, and the sampled times are consistent (parts <= whole substep)."""
+    t = settled_c1
+    K = 2
+    u = si.ensemble_inputs([3, 4], K)[0]
+    a = _ctx(t, B=2, rebin_every=0, skin=0.15 * t.params.h, rebuild_path=path)
+    ya, _ = a.rollout(u)
+    b = _ctx(t, B=2, rebin_every=0, skin=0.15 * t.params.h, rebuild_path=path)
+    b.set_live_timing(3)
+    yb, _ = b.rollout(u)
+    live = b.live_timing()
+    assert np.array_equal(ya, yb)
+    assert np.array_equal(a.get_particles(1), b.get_particles(1))
+    assert live["samples"] == K * ((t.params.n_sub + 2) // 3)
+    assert 0 < live["density"] < live["substep"] and 0 < live["force"] < live["substep"]
+    assert b.live_timing()["samples"] == 0   # reset
+    a.close()
+    b.close()
+
+
 def test_device_pointer_rollout_equals_host_pointer(settled_c1):
     import torch
     t = settled_c1
