@@ -50,12 +50,9 @@ struct sph_ctx {
 enum { LV_SUB0 = 0, LV_DEN0, LV_DEN1, LV_F1_0, LV_F1_1, LV_F2_0, LV_F2_1, LV_SUB1, LIVE_SLOTS };
 
 static std::string g_init_err;
-// dynamic shared memory of the neighbour kernels: only with TMA window staging (a reservation
-// would otherwise shrink the L1 carve-out the neighbour gathers live in)
-static size_t density_smem(const DevParams& P) { return P.stage ? (size_t)MAXSTAGE * 16 : 0; }
-static size_t force_smem(const DevParams& P) {
-    return P.stage ? (size_t)MAXSTAGE * 16 + (size_t)(MAXSTAGE + 2) * 8 : 0;
-}
+// dynamic shared memory of the ring kernels (state ring; + aux ring for the forces)
+static constexpr size_t kDensityRingSmem = (size_t)RING * 16;
+static constexpr size_t kForceRingSmem = (size_t)RING * 24;
 static const int kSmallMinBatch = 512;   // auto policy: per-rollout-CTA rebuild from this B on
 
 #define CK(expr)                                                                       \
@@ -142,9 +139,16 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     const float RL = (float)(2.0 * h + (tp->rebin_every ? 0.0 : tp->skin));
     P->RL2 = tp->rebin_every ? P->H2 : RL * RL;      // list radius (2h + skin)^2
     P->rebuild_disp = (float)(0.45 * tp->skin);      // < skin / 2 with margin for rounding
-    {   // experimental TMA staging of neighbour windows (off by default: slower)
-        const char* e = std::getenv("SPH_TMA_STAGE");
-        P->stage = (e && e[0] == '1') ? 1 : 0;
+    P->NA = (N + 1) & ~1;
+    {   // TMA-fed shared-memory ring kernels: opt-in (SPH_RING=1), measured no faster than the
+        // plain gather kernels on C3
+        const char* e = std::getenv("SPH_RING");
+        P->ring = (e && e[0] == '1') ? 1 : 0;
+        const char* c = std::getenv("SPH_RING_CHUNK");
+        P->chunk = (c && std::atoi(c) > 0) ? std::atoi(c) : 4;
+        P->nblk = std::max(1, (N + SW_T - 1) / SW_T);
+        P->chunk = std::min(P->chunk, P->nblk);
+        P->nchunk = (P->nblk + P->chunk - 1) / P->chunk;
     }
     // ghost-ring window (see for_ghost_candidates): only particles farther than d_min from the
     // centre can have a ghost within 2h; their ghosts lie within +-dphi of their polar angle.
@@ -182,7 +186,7 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     put(d.pv[1], BN * 16);
     put(d.id[0], BN * 4);
     put(d.id[1], BN * 4);
-    put(d.aux, BN * 8 + 16);   // +1 element: the force kernel's 16-B aligned TMA slice
+    put(d.aux, (size_t)P.B * P.NA * 8);   // rows of NA (even) elements: 16-B aligned
     put(d.skey, BN * 4);
     put(d.xb, BN * 8);
     put(d.nbr, BN * KQ * 8);
@@ -218,16 +222,20 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
 static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding) {
     const DevParams& P = ctx->P;
     dim3 gp(P.ntile, P.B);
-    if (P.stage) k_density<true><<<gp, TILE, density_smem(P), s>>>(P, ctx->D, skip_rebuilding);
-    else k_density<false><<<gp, TILE, 0, s>>>(P, ctx->D, skip_rebuilding);
+    if (P.ring)
+        k_density_ring<<<dim3(P.nchunk, P.B), SW_T, kDensityRingSmem, s>>>(P, ctx->D, skip_rebuilding);
+    else
+        k_density<<<gp, TILE, 0, s>>>(P, ctx->D, skip_rebuilding);
 }
 
 // mode: 0 all rollouts, 1 non-rebuilding rollouts, 2 rebuilt rollouts (work list)
 static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode = 0) {
     const DevParams& P = ctx->P;
-    dim3 gp(P.ntile, mode == 2 ? std::min(P.B, 64) : P.B);
-    if (P.stage) k_force<true><<<gp, TILE, force_smem(P), s>>>(P, ctx->D, damping, mode);
-    else k_force<false><<<gp, TILE, 0, s>>>(P, ctx->D, damping, mode);
+    const int gy = mode == 2 ? std::min(P.B, 64) : P.B;
+    if (P.ring)
+        k_force_ring<<<dim3(P.nchunk, gy), SW_T, kForceRingSmem, s>>>(P, ctx->D, damping, mode);
+    else
+        k_force<<<dim3(P.ntile, gy), TILE, 0, s>>>(P, ctx->D, damping, mode);
 }
 
 static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0) {
@@ -466,6 +474,16 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
         return SPH_ECUDA;
     };
     cudaError_t e;
+    if (P.ring) {   // ring kernels: 48 KB (force) / 32 KB (density) dynamic shared memory
+        cudaError_t e1 = cudaFuncSetAttribute(k_force_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)kForceRingSmem);
+        cudaError_t e2 = cudaFuncSetAttribute(k_density_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)kDensityRingSmem);
+        if (e1 != cudaSuccess || e2 != cudaSuccess) {
+            sph_destroy(ctx);
+            return fail(nullptr, SPH_ECUDA, "cannot raise the ring kernels' shared-memory limit");
+        }
+    }
     // rebuild path: one CTA per rebuilding rollout when its cell table and sort scratch fit in
     // shared memory (rebuild_path 0 = auto, 1 = force per-rollout CTA, 2 = force multi-kernel)
     {

@@ -52,8 +52,12 @@ struct DevParams {
     float ghost_scale;      // G / (2 pi)
     float rebuild_disp;     // rebuild when the displacement bound reaches this (< skin / 2)
     int rebin_every;
-    int stage;              // 1: TMA-stage each CTA's neighbour window in shared memory
-                            //    (experimental, env SPH_TMA_STAGE=1; slower on C3, see DESIGN)
+    int NA;                 // aux row stride per rollout = N rounded up to even (16-B rows)
+    int ring;               // 1: density / force kernels stream the state through a TMA-fed
+                            //    shared-memory ring (rollouts with span <= SW_T); opt-in via
+                            //    env SPH_RING=1 (default 0: plain global-gather kernels)
+    int nblk, chunk, nchunk;// ring kernels: super-tiles of SW_T slots per rollout, super-tiles
+                            // per CTA, CTAs per rollout
     double dtd, m_body, J_body;
 };
 
@@ -116,7 +120,13 @@ struct DevPtrs {
 // ---------------------------------------------------------------------------------------
 // TMA bulk copies (cp.async.bulk global -> shared, completion on an mbarrier)
 // ---------------------------------------------------------------------------------------
-constexpr int MAXSTAGE = 1024;   // slots of a CTA's neighbour window staged in shared memory
+// Ring kernels: a CTA of SW_T threads walks `chunk` consecutive super-tiles of SW_T slots of one
+// rollout; the state of the slots [512 (t - 1), 512 (t + 2)) sits in a 4-block shared-memory ring
+// (slot j at j & (RING - 1)) fed by TMA bulk copies one super-tile ahead.  Every list neighbour
+// of a slot in super-tile t lies in blocks t - 1 .. t + 1 when the rollout's span <= SW_T.
+constexpr int SW_T = 512;
+constexpr int RING_NB = 4;
+constexpr int RING = SW_T * RING_NB;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -136,6 +146,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+// L2 prefetch of a global range (address and size multiples of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     asm volatile(

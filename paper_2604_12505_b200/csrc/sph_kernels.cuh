@@ -268,14 +268,16 @@ __device__ __forceinline__ void finish_density(const DevParams& P, const DevPtrs
     });
     const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
     const float pr = P.k * (rho - P.rho0);
-    D.aux[(size_t)b * P.N + i] = make_float2(rho, __fdividef(pr, rho * rho));
+    D.aux[(size_t)b * P.NA + i] = make_float2(rho, __fdividef(pr, rho * rho));
 }
 
-// Density + EOS of slot i of rollout b.  pos(j) returns the (x, y) of slot j of the rollout
-// (global state buffer, or the shared-memory copy inside k_rebuild_small).
-template <bool NC, class PosF>
+// Density + EOS of slot i of rollout b.  pos(j) returns the (x, y) of list neighbour j of the
+// rollout (global state buffer, shared-memory ring, or the shared-memory copy inside
+// k_rebuild_small); posg(j) that of a cell-scan candidate (list overflow; may lie outside a
+// ring window, so the ring kernel passes a global-memory reader here).
+template <bool NC, class PosF, class PosG>
 __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& D, int b, int i,
-                                             PosF&& pos) {
+                                             PosF&& pos, PosG&& posg) {
     const size_t o = (size_t)b * P.N;
     const float2 p = pos((uint32_t)i);
     const float4 xi = make_float4(p.x, p.y, 0.f, 0.f);
@@ -302,9 +304,15 @@ __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& 
         wf -= 4.0f * (float)(((n + 1) & ~1) - n);   // padding entries (self) added W(0) = 4 each
     } else {
         for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), ld<NC>(D.skey + o + i),
-                            [&](uint32_t j) { wf += w_masked(P, xi, as4(pos(j)), j != (uint32_t)i); });
+                            [&](uint32_t j) { wf += w_masked(P, xi, as4(posg(j)), j != (uint32_t)i); });
     }
     finish_density(P, D, b, i, p, wf);
+}
+
+template <bool NC, class PosF>
+__device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& D, int b, int i,
+                                             PosF&& pos) {
+    density_core<NC>(P, D, b, i, pos, pos);
 }
 
 template <bool NC>
@@ -317,43 +325,127 @@ __device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D,
 }
 
 // skip_rebuilding = 1 when rollouts that rebuild this substep get their densities from
-// k_rebuild_small (which runs concurrently on another branch of the graph).
-// Staging window of a CTA tile: every list neighbour j of a slot i in [t0, t0 + TILE) has
-// |j - i| <= span, so [lo, hi) covers the tile and all its candidates (sorted row-major cells).
-__device__ __forceinline__ void stage_window(const DevParams& P, int span, int t0, int* lo, int* hi) {
-    *lo = max(t0 - span, 0);
-    *hi = min(t0 + TILE + span, P.N);
-}
-
-// dynamic shared memory: pv[MAXSTAGE] float4 (TMA-staged neighbour window)
-template <bool STAGE>
+// k_nlist_density (which runs concurrently on another branch of the graph).
+// Plain variant: neighbour positions gathered from global memory through L1.
 __global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D, int skip_rebuilding) {
-    extern __shared__ float4 s_pv[];
-    __shared__ __align__(8) uint64_t bar;
     const int b = blockIdx.y;
     const RolloutState* rs = D.rs + b;
     if (rs->frozen || (skip_rebuilding && rs->need_rebin)) return;   // CTA-uniform
-    const int t0 = blockIdx.x * TILE;
-    const int i = t0 + threadIdx.x;
+    const int i = blockIdx.x * TILE + threadIdx.x;
     const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
-    int lo, hi;
-    stage_window(P, rs->span, t0, &lo, &hi);
-    if (STAGE && hi - lo <= MAXSTAGE) {
-        if (threadIdx.x == 0) {
-            mbar_init(&bar, 1);
-            mbar_expect_tx(&bar, (uint32_t)(hi - lo) * 16u);
-            bulk_g2s(s_pv, pv + lo, (uint32_t)(hi - lo) * 16u, &bar);
+    if (i < P.N) density_at<true>(P, D, b, i, pv);
+}
+
+// ---------------------------------------------------------------------------------------
+// Shared-memory ring (see SW_T): TMA bulk copies of whole super-tile blocks, one mbarrier per
+// ring block, phase parity per block kept in a CTA-uniform bit mask.
+// ---------------------------------------------------------------------------------------
+struct RingIO {
+    float4* s_pv;          // [RING]
+    float2* s_aux;         // [RING] (force) or nullptr (density)
+    uint64_t* bar;         // [RING_NB] "full" barriers (TMA transaction count)
+    uint32_t* rel;         // [RING_NB] warps done with the block in a ring slot
+    const float4* pv;      // rollout's state rows (global)
+    const float2* aux;     // rollout's aux row (global, 16-B aligned: stride NA)
+    const uint2* nbr;      // rollout's neighbour-list rows [KQ][N] (L2 prefetch)
+    uint32_t ph = 0;       // expected parity per ring block (per thread, uniform)
+
+    // one thread: start the copy of super-tile block k into ring block k % RING_NB and prefetch
+    // the list rows of super-tile k - 1 (first used one tile later) into L2
+    __device__ __forceinline__ void issue(const DevParams& P, int k) const {
+        const int cnt = min(SW_T, P.N - k * SW_T);
+        const int r = k & (RING_NB - 1);
+        const uint32_t bp = (uint32_t)cnt * 16u;
+        const uint32_t ba = s_aux ? (uint32_t)((cnt + 1) & ~1) * 8u : 0u;   // even: 16-B multiple
+        mbar_expect_tx(&bar[r], cnt > 0 ? bp + ba : 0u);   // (N = 0: plain arrive)
+        if (cnt <= 0) return;
+        bulk_g2s(s_pv + r * SW_T, pv + (size_t)k * SW_T, bp, &bar[r]);
+        if (s_aux) bulk_g2s(s_aux + r * SW_T, aux + (size_t)k * SW_T, ba, &bar[r]);
+        if (k >= 1) prefetch_lists(P, k - 1);
+    }
+    __device__ __forceinline__ void prefetch_lists(const DevParams& P, int t) const {
+        const int cnt = min(SW_T, P.N - t * SW_T);
+        for (int q = 0; q < KQ; ++q) {
+            const uintptr_t a0 = reinterpret_cast<uintptr_t>(nbr + (size_t)q * P.N + (size_t)t * SW_T);
+            const uintptr_t lo = a0 & ~(uintptr_t)15, hi = (a0 + (uintptr_t)cnt * 8 + 15) & ~(uintptr_t)15;
+            bulk_prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
         }
-        __syncthreads();
-        mbar_wait(&bar, 0);
+    }
+    // every thread: wait until block k has landed
+    __device__ __forceinline__ void wait(int k) {
+        const int r = k & (RING_NB - 1);
+        mbar_wait(&bar[r], (ph >> r) & 1u);
+        ph ^= 1u << r;
+    }
+};
+
+// Drives one CTA over super-tiles [ta, tb) of a rollout (P.nblk blocks), warps independently.
+// Super-tile t reads blocks t-1 .. t+1, so the chunk needs blocks lo = max(ta-1, 0) .. hi =
+// min(tb, nblk-1).  The prologue fills the ring with blocks lo .. lo+3; block k > lo+3 goes into
+// the slot of block k-4, which the last super-tile reading it (k-3) releases: when a warp
+// finishes super-tile t it releases block t-1, and the last warp to do so starts the copy of
+// block t+3.  A warp waits only for the blocks its next super-tile reads; warps may drift
+// apart by about one super-tile; no CTA barrier inside the walk.
+template <class Body>
+__device__ __forceinline__ void ring_walk(const DevParams& P, RingIO& io, int ta, int tb, Body&& body) {
+    const int nw = blockDim.x >> 5;
+    const int lo = max(ta - 1, 0), hi = min(tb, P.nblk - 1);
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < RING_NB; ++r) {
+            mbar_init(&io.bar[r], 1);
+            io.rel[r] = 0u;
+        }
+        if (ta < P.nblk) io.prefetch_lists(P, ta);
+        for (int k = lo; k <= min(lo + RING_NB - 1, hi); ++k) io.issue(P, k);
+    }
+    __syncthreads();
+    for (int k = lo; k <= min(ta + 1, hi); ++k) io.wait(k);
+    for (int t = ta; t < tb; ++t) {
+        if (t > ta && t + 1 <= hi) io.wait(t + 1);
+        body(t);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0 && t - 1 >= lo) {
+            const int r = (t - 1) & (RING_NB - 1);
+            __threadfence_block();   // this warp's reads of block t-1 precede the release
+            if (atomicAdd(&io.rel[r], 1u) == (uint32_t)(nw - 1)) {
+                io.rel[r] = 0u;
+                if (t + 3 <= hi && t + 3 > lo + RING_NB - 1) io.issue(P, t + 3);
+            }
+        }
+    }
+    __syncthreads();   // ring reusable (mode 2 walks several rollouts with one CTA)
+}
+
+// Ring variant of k_density: grid (nchunk, B); dynamic smem RING float4.
+__global__ void __launch_bounds__(SW_T, 4) k_density_ring(DevParams P, DevPtrs D, int skip_rebuilding) {
+    extern __shared__ float4 ring_pv[];
+    __shared__ __align__(8) uint64_t bar[RING_NB];
+    __shared__ uint32_t rel[RING_NB];
+    const int b = blockIdx.y;
+    const RolloutState* rs = D.rs + b;
+    if (rs->frozen || (skip_rebuilding && rs->need_rebin)) return;   // CTA-uniform
+    const int ta = blockIdx.x * P.chunk, tb = min(ta + P.chunk, P.nblk);
+    const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
+    auto posg = [&](uint32_t j) {
+        const float4 v = __ldg(pv + j);
+        return make_float2(v.x, v.y);
+    };
+    if (rs->span > SW_T) {   // wide rows (large tanks): plain gathers
+        for (int t = ta; t < tb; ++t) {
+            const int i = t * SW_T + threadIdx.x;
+            if (i < P.N) density_at<true>(P, D, b, i, pv);
+        }
+        return;
+    }
+    RingIO io{ring_pv, nullptr, bar, rel, pv, nullptr, D.nbr + (size_t)b * KQ * P.N};
+    ring_walk(P, io, ta, tb, [&](int t) {
+        const int i = t * SW_T + threadIdx.x;
         if (i < P.N)
             density_core<true>(P, D, b, i, [&](uint32_t j) {
-                const float4 v = s_pv[j - lo];
+                const float4 v = ring_pv[j & (RING - 1)];
                 return make_float2(v.x, v.y);
-            });
-    } else if (i < P.N) {
-        density_at<true>(P, D, b, i, pv);
-    }
+            }, posg);
+    });
 }
 
 // ---------------------------------------------------------------------------------------
@@ -737,139 +829,192 @@ __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __re
 #ifndef SPH_FORCE_MINB
 #define SPH_FORCE_MINB 6   // 40 registers: occupancy beats the small spill (measured sweep 3..8)
 #endif
-// dynamic shared memory: pv[MAXSTAGE] float4 | aux[MAXSTAGE + 2] float2 (TMA-staged window)
-template <bool STAGE>
-__device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D, float damping,
-                                           int b, int tile) {
-    extern __shared__ float4 s_pv[];
-    float2* s_aux = reinterpret_cast<float2*>(s_pv + MAXSTAGE);
-    __shared__ __align__(8) uint64_t bar;
-    RolloutState* rs = D.rs + b;
-    if (rs->frozen) return;   // CTA-uniform (before any barrier / warp-level collective)
-    const int t0 = tile * TILE;
-    const int i = t0 + threadIdx.x;
-    const size_t o = (size_t)b * P.N;
-    const int cur = rs->sp ^ rs->need_rebin;
-    const float4* __restrict__ pv = D.pv[cur] + o;
-    const float2* __restrict__ aux = D.aux + o;
+
+// Body partial accumulators of one thread (reaction force, torque, squared displacement).
+struct BodyAcc {
     float fbx = 0.0f, fby = 0.0f, tq = 0.0f, vmax = 0.0f;
-    const Geom gm = D.geom[b];
-    int lo, hi;
-    stage_window(P, rs->span, t0, &lo, &hi);
-    const bool staged = STAGE && hi - lo <= MAXSTAGE;   // CTA-uniform
-    // aux slice aligned to 16 bytes in global memory: [ga0, ga1) covers [o + lo, o + hi)
-    const size_t ga0 = (o + lo) & ~(size_t)1, ga1 = (o + hi + 1) & ~(size_t)1;
-    const int ash = (int)(o + lo - ga0);
-    if (staged) {
-        if (threadIdx.x == 0) {
-            const uint32_t bp = (uint32_t)(hi - lo) * 16u, ba = (uint32_t)(ga1 - ga0) * 8u;
-            mbar_init(&bar, 1);
-            mbar_expect_tx(&bar, bp + ba);
-            bulk_g2s(s_pv, pv + lo, bp, &bar);
-            bulk_g2s(s_aux, D.aux + ga0, ba, &bar);
-        }
-        __syncthreads();
-        mbar_wait(&bar, 0);
-    }
-    if (i < P.N) {
-        const float4 xi = staged ? s_pv[i - lo] : pv[i];
-        const float2 ai = staged ? s_aux[i - lo + ash] : aux[i];
-        float sx = 0.0f, sy = 0.0f;   // sum of (-pressure + viscous) * grad W / m^2
-        const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
-        const uint2 q0 = __ldg(nq);            // first offsets, independent of the count load
-        const int n = D.ncnt[o + i];
-        if (n != NL_OVERFLOW && staged) {
-            force_list(P, nq, n, q0, i, xi, ai, [&](uint32_t j) { return s_pv[j - lo]; },
-                       [&](uint32_t j) { return s_aux[j - lo + ash]; }, sx, sy);
-        } else if (n != NL_OVERFLOW) {
-            force_list(P, nq, n, q0, i, xi, ai, [&](uint32_t j) { return __ldg(pv + j); },
-                       [&](uint32_t j) { return __ldg(aux + j); }, sx, sy);
-        } else {
-            for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
-                pair_force(P, xi, ai, __ldg(pv + j), __ldg(aux + j), j != (uint32_t)i, sx, sy);
-            });
-        }
-        float gxs = 0.0f, gys = 0.0f;   // sum_g G_ig
-        const float4* gst = D.gst + (size_t)b * P.G;
-        const float2* glo = D.glo + (size_t)b * P.G;
-        const float2* garm = D.garm + (size_t)b * P.G;
-        const float cp = P.gsign2m2 * ai.y;                    // wall pressure coefficient
-        const float cvb = __fdividef(P.m2 * P.beta, ai.x);      // m^2 beta / rho_i
-        for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), P.ghost_K1, P.wall1_r2, [&](int g) {
-            const float4 xg = __ldg(gst + g);
-            float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
-            if (dist2(dx, dy) < P.h2) {
-                const float2 lo = __ldg(glo + g);
-                dx -= lo.x;
-                dy -= lo.y;
-                const float r2 = dx * dx + dy * dy;
-                if (!(r2 > 0.0f)) return;
-                const float rs = rsqrtf(r2);
-                const float hr = P.h - r2 * rs;
-                const float gw = P.dws3 * hr * hr * rs;
-                const float vr = (xi.z - xg.z) * dx + (xi.w - xg.w) * dy;
-                const float cv = __fdividef(cvb * fminf(vr, 0.0f), r2 + P.eps_h2);
-                const float c = (cp + cv) * gw;
-                const float Gx = c * dx, Gy = c * dy;
-                gxs += Gx;
-                gys += Gy;
-                const float2 a = __ldg(garm + g);
-                tq -= a.x * Gy - a.y * Gx;     // (r_g - r) x (-G_ig)
-            }
+};
+
+// Forces, wall, integration and Verlet displacement of slot i (i < N) of rollout b.
+// pvj / axj read list neighbours (global or ring); pv / aux are the rollout's global rows
+// (cell-scan fallback of overflowing lists).
+template <class PV, class AX>
+__device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs& D, float damping,
+                                               int b, int i, int cur, const Geom& gm,
+                                               const RolloutState* rs, float4 xi, float2 ai,
+                                               const float4* __restrict__ pv,
+                                               const float2* __restrict__ aux, PV&& pvj, AX&& axj,
+                                               BodyAcc& acc) {
+    const size_t o = (size_t)b * P.N;
+    float sx = 0.0f, sy = 0.0f;   // sum of (-pressure + viscous) * grad W / m^2
+    const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
+    const uint2 q0 = __ldg(nq);            // first offsets, independent of the count load
+    const int n = D.ncnt[o + i];
+    if (n != NL_OVERFLOW) {
+        force_list(P, nq, n, q0, i, xi, ai, pvj, axj, sx, sy);
+    } else {
+        for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
+            pair_force(P, xi, ai, __ldg(pv + j), __ldg(aux + j), j != (uint32_t)i, sx, sy);
         });
-        fbx = -gxs;
-        fby = -gys;
-        const float ax = P.mdwcb3 * sx + gxs * P.inv_mass + P.gx;   // m * 3C/h^3 * sum
-        const float ay = P.mdwcb3 * sy + gys * P.inv_mass + P.gy;
-        float4 xn;
-        xn.z = xi.z + P.dt * ax;
-        xn.w = xi.w + P.dt * ay;
-        xn.x = xi.x + P.dt * xn.z;
-        xn.y = xi.y + P.dt * xn.w;
-        xn.z *= damping;
-        xn.w *= damping;
-        D.pv[cur ^ 1][o + i] = xn;
-        // Verlet criterion on actual displacements: displacement since the last rebuild
-        // relative to the body translation since then (k_body adds this step's body drift).
-        // vmax carries the squared displacement through the reductions.
-        const float2 xb = __ldg(D.xb + o + i);
-        const float ddx = (xn.x - xb.x) - (gm.rx - rs->rbx), ddy = (xn.y - xb.y) - (gm.ry - rs->rby);
-        vmax = ddx * ddx + ddy * ddy;
-        const bool finite = isfinite(xn.x) && isfinite(xn.y) && isfinite(xn.z) && isfinite(xn.w);
-        if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || fabsf(xn.z) > 1e9f ||
-            fabsf(xn.w) > 1e9f)
-            set_status(rs, finite ? 2 : 1, (int)D.id[rs->ip ^ rs->need_rebin][o + i]);
     }
-    // body partials: warp butterfly (deterministic order), one fp64 partial per warp written
-    // straight to global memory (no CTA barrier: warps finish independently)
+    float gxs = 0.0f, gys = 0.0f;   // sum_g G_ig
+    const float4* gst = D.gst + (size_t)b * P.G;
+    const float2* glo = D.glo + (size_t)b * P.G;
+    const float2* garm = D.garm + (size_t)b * P.G;
+    const float cp = P.gsign2m2 * ai.y;                    // wall pressure coefficient
+    const float cvb = __fdividef(P.m2 * P.beta, ai.x);      // m^2 beta / rho_i
+    float tq = 0.0f;
+    for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), P.ghost_K1, P.wall1_r2, [&](int g) {
+        const float4 xg = __ldg(gst + g);
+        float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
+        if (dist2(dx, dy) < P.h2) {
+            const float2 lo = __ldg(glo + g);
+            dx -= lo.x;
+            dy -= lo.y;
+            const float r2 = dx * dx + dy * dy;
+            if (!(r2 > 0.0f)) return;
+            const float rs = rsqrtf(r2);
+            const float hr = P.h - r2 * rs;
+            const float gw = P.dws3 * hr * hr * rs;
+            const float vr = (xi.z - xg.z) * dx + (xi.w - xg.w) * dy;
+            const float cv = __fdividef(cvb * fminf(vr, 0.0f), r2 + P.eps_h2);
+            const float c = (cp + cv) * gw;
+            const float Gx = c * dx, Gy = c * dy;
+            gxs += Gx;
+            gys += Gy;
+            const float2 a = __ldg(garm + g);
+            tq -= a.x * Gy - a.y * Gx;     // (r_g - r) x (-G_ig)
+        }
+    });
+    acc.fbx = -gxs;
+    acc.fby = -gys;
+    acc.tq = tq;
+    const float ax = P.mdwcb3 * sx + gxs * P.inv_mass + P.gx;   // m * 3C/h^3 * sum
+    const float ay = P.mdwcb3 * sy + gys * P.inv_mass + P.gy;
+    float4 xn;
+    xn.z = xi.z + P.dt * ax;
+    xn.w = xi.w + P.dt * ay;
+    xn.x = xi.x + P.dt * xn.z;
+    xn.y = xi.y + P.dt * xn.w;
+    xn.z *= damping;
+    xn.w *= damping;
+    D.pv[cur ^ 1][o + i] = xn;
+    // Verlet criterion on actual displacements: displacement since the last rebuild
+    // relative to the body translation since then (k_body adds this step's body drift).
+    // vmax carries the squared displacement through the reductions.
+    const float2 xb = __ldg(D.xb + o + i);
+    const float ddx = (xn.x - xb.x) - (gm.rx - rs->rbx), ddy = (xn.y - xb.y) - (gm.ry - rs->rby);
+    acc.vmax = ddx * ddx + ddy * ddy;
+    const bool finite = isfinite(xn.x) && isfinite(xn.y) && isfinite(xn.z) && isfinite(xn.w);
+    if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || fabsf(xn.z) > 1e9f ||
+        fabsf(xn.w) > 1e9f)
+        set_status(const_cast<RolloutState*>(rs), finite ? 2 : 1,
+                   (int)D.id[rs->ip ^ rs->need_rebin][o + i]);
+}
+
+// Body partials: warp butterfly (deterministic order), one fp64 partial per warp of 32 slots,
+// index q = slot / 32 within the rollout (written straight to global memory, no CTA barrier).
+__device__ __forceinline__ void write_partial(const DevParams& P, const DevPtrs& D, int b, int q,
+                                              BodyAcc a) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
-        fbx += __shfl_xor_sync(0xffffffffu, fbx, d);
-        fby += __shfl_xor_sync(0xffffffffu, fby, d);
-        tq += __shfl_xor_sync(0xffffffffu, tq, d);
-        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, d));
+        a.fbx += __shfl_xor_sync(0xffffffffu, a.fbx, d);
+        a.fby += __shfl_xor_sync(0xffffffffu, a.fby, d);
+        a.tq += __shfl_xor_sync(0xffffffffu, a.tq, d);
+        a.vmax = fmaxf(a.vmax, __shfl_xor_sync(0xffffffffu, a.vmax, d));
     }
-    if ((threadIdx.x & 31) == 0)
-        D.part[(size_t)b * P.npart + tile * (TILE / 32) + (threadIdx.x >> 5)] =
-            make_double4(fbx, fby, tq, vmax);
-    if (STAGE) __syncthreads();   // the staging barrier may be re-initialised for the next tile
+    if ((threadIdx.x & 31) == 0 && q < P.npart)
+        D.part[(size_t)b * P.npart + q] = make_double4(a.fbx, a.fby, a.tq, a.vmax);
+}
+
+__device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D, float damping,
+                                           int b, int tile) {
+    const RolloutState* rs = D.rs + b;
+    if (rs->frozen) return;   // CTA-uniform (before any warp-level collective)
+    const int i = tile * TILE + threadIdx.x;
+    const int cur = rs->sp ^ rs->need_rebin;
+    const float4* __restrict__ pv = D.pv[cur] + (size_t)b * P.N;
+    const float2* __restrict__ aux = D.aux + (size_t)b * P.NA;
+    BodyAcc acc;
+    if (i < P.N) {
+        const Geom gm = D.geom[b];
+        force_particle(P, D, damping, b, i, cur, gm, rs, pv[i], aux[i], pv, aux,
+                       [&](uint32_t j) { return __ldg(pv + j); },
+                       [&](uint32_t j) { return __ldg(aux + j); }, acc);
+    }
+    write_partial(P, D, b, i >> 5, acc);
 }
 
 // mode 0: every rollout (grid.y = B); 1: rollouts that do NOT rebuild this substep (their
 // densities are ready while the rebuild branch still runs); 2: the rebuilt rollouts of the
 // work list (grid.y-stride over it), after the rebuild branch joined.
-template <bool STAGE>
 __global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, DevPtrs D,
                                                                 float damping, int mode) {
     if (mode == 2) {
         const int count = *D.rcount;
         for (int w = blockIdx.y; w < count; w += gridDim.y)
-            force_tile<STAGE>(P, D, damping, D.rlist[w], blockIdx.x);
+            force_tile(P, D, damping, D.rlist[w], blockIdx.x);
         return;
     }
     const int b = blockIdx.y;
     if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
-    force_tile<STAGE>(P, D, damping, b, blockIdx.x);
+    force_tile(P, D, damping, b, blockIdx.x);
+}
+
+// Ring variant: CTA (x, y) walks super-tiles [x chunk, (x + 1) chunk) of rollout y (modes 0/1)
+// or of the work-list entries y, y + gridDim.y, ... (mode 2).  Dynamic smem: RING float4 |
+// RING float2.
+__device__ __forceinline__ void force_ring_chunk(const DevParams& P, const DevPtrs& D,
+                                                 float damping, int b, float4* ring_pv,
+                                                 float2* ring_aux, uint64_t* bar, uint32_t* rel) {
+    const RolloutState* rs = D.rs + b;
+    if (rs->frozen) return;   // CTA-uniform
+    const int ta = blockIdx.x * P.chunk, tb = min(ta + P.chunk, P.nblk);
+    const int cur = rs->sp ^ rs->need_rebin;
+    const float4* __restrict__ pv = D.pv[cur] + (size_t)b * P.N;
+    const float2* __restrict__ aux = D.aux + (size_t)b * P.NA;
+    const Geom gm = D.geom[b];
+    if (rs->span > SW_T) {   // wide rows: plain gathers
+        for (int t = ta; t < tb; ++t) {
+            const int i = t * SW_T + threadIdx.x;
+            BodyAcc acc;
+            if (i < P.N)
+                force_particle(P, D, damping, b, i, cur, gm, rs, pv[i], aux[i], pv, aux,
+                               [&](uint32_t j) { return __ldg(pv + j); },
+                               [&](uint32_t j) { return __ldg(aux + j); }, acc);
+            write_partial(P, D, b, i >> 5, acc);
+        }
+        return;
+    }
+    RingIO io{ring_pv, ring_aux, bar, rel, pv, aux, D.nbr + (size_t)b * KQ * P.N};
+    ring_walk(P, io, ta, tb, [&](int t) {
+        const int i = t * SW_T + threadIdx.x;
+        BodyAcc acc;
+        if (i < P.N) {
+            const uint32_t s = (uint32_t)i & (RING - 1);
+            force_particle(P, D, damping, b, i, cur, gm, rs, ring_pv[s], ring_aux[s], pv, aux,
+                           [&](uint32_t j) { return ring_pv[j & (RING - 1)]; },
+                           [&](uint32_t j) { return ring_aux[j & (RING - 1)]; }, acc);
+        }
+        write_partial(P, D, b, i >> 5, acc);
+    });
+}
+
+__global__ void __launch_bounds__(SW_T, 3) k_force_ring(DevParams P, DevPtrs D, float damping,
+                                                        int mode) {
+    extern __shared__ float4 ring_pv[];
+    float2* ring_aux = reinterpret_cast<float2*>(ring_pv + RING);
+    __shared__ __align__(8) uint64_t bar[RING_NB];
+    __shared__ uint32_t rel[RING_NB];
+    if (mode == 2) {
+        const int count = *D.rcount;
+        for (int w = blockIdx.y; w < count; w += gridDim.y)
+            force_ring_chunk(P, D, damping, D.rlist[w], ring_pv, ring_aux, bar, rel);
+        return;
+    }
+    const int b = blockIdx.y;
+    if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
+    force_ring_chunk(P, D, damping, b, ring_pv, ring_aux, bar, rel);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1007,7 +1152,7 @@ __global__ void k_import(DevParams P, DevPtrs D, int b0, const float4* __restric
     const size_t o = (size_t)b * P.N;
     D.pv[rs->sp][o + i] = in[i];
     D.id[rs->ip][o + i] = (uint32_t)i;
-    D.aux[o + i] = make_float2(0.f, 0.f);
+    D.aux[(size_t)b * P.NA + i] = make_float2(0.f, 0.f);
 }
 
 __global__ void k_export(DevParams P, DevPtrs D, int b, float4* out, float* rho) {
@@ -1017,7 +1162,7 @@ __global__ void k_export(DevParams P, DevPtrs D, int b, float4* out, float* rho)
     const size_t o = (size_t)b * P.N;
     const uint32_t id = D.id[rs->ip][o + i];
     out[id] = D.pv[rs->sp][o + i];
-    if (rho) rho[id] = D.aux[o + i].x;
+    if (rho) rho[id] = D.aux[(size_t)b * P.NA + i].x;
 }
 
 __global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angle0) {
