@@ -21,11 +21,16 @@ def nvcc():
     return "nvcc"
 
 
+STAMP = OUT + ".flags"   # flags of the last build (a flag change forces a rebuild)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(OUT) and \
+    extra = os.environ.get("SPH_NVCC_EXTRA", "").split()
+    flags = " ".join(NVCC_FLAGS + extra)
+    same_flags = os.path.exists(STAMP) and open(STAMP).read() == flags
+    if not force and same_flags and os.path.exists(OUT) and \
             os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in DEPS):
         return OUT
-    extra = os.environ.get("SPH_NVCC_EXTRA", "").split()
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", OUT + ".tmp", *SRC]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -33,6 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(HERE, "csrc", "ptxas_info.txt"), "w") as f:
         f.write(res.stderr)
     os.replace(OUT + ".tmp", OUT)
+    with open(STAMP, "w") as f:
+        f.write(flags)
     if verbose:
         print(res.stderr)
     return OUT

@@ -189,6 +189,14 @@ __device__ __forceinline__ float dwcb_poly(float q) {
     return d;
 }
 
+// Opaque copy of a pointer: stops the compiler from re-deriving it from (rollout, slot) index
+// arithmetic inside the neighbour loops, so a neighbour address is one IMAD.WIDE from it.
+template <class T>
+__device__ __forceinline__ const T* opaque(const T* p) {
+    asm("mov.b64 %0, %0;" : "+l"(p));
+    return p;
+}
+
 // t-th int16 offset (sign-extended) of a neighbour quad.
 __device__ __forceinline__ int quad_offset(uint2 w, int t) {
     const uint32_t h = (t & 2) ? w.y : w.x;

@@ -225,20 +225,24 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D);
 // The list is walked four candidates at a time: one 8-byte offset load, four independent
 // 16-byte state loads, then branch-free masked arithmetic.
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ float w_masked(const DevParams& P, float4 xi, float4 xj, bool valid) {
-    const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-    const float r = r2 > 0.0f ? r2 * rsqrtf(r2) : 0.0f;
-    const float w = wcb_poly(r * P.inv_h);
-    return (valid && r2 < P.H2) ? w : 0.0f;
+// W_cb polynomial of a list candidate (no validity mask: list padding points at the particle
+// itself and contributes exactly W(0) = 4, which the caller subtracts).  Support by shape, not
+// by predicate: W = max(2-q,0)^3 - 4 max(1-q,0)^3 is the cubic spline (Eq. cubicspline) for
+// every q >= 0 and exactly 0 beyond 2h; it differs from masking with the canonical predicate
+// r2 < (2h)^2 only by O(eps^3) at the rounding boundary (the neighbour SETS stay canonical:
+// they are fixed when the lists are built, reading A19).
+__device__ __forceinline__ float w_list(const DevParams& P, float4 xi, float4 xj) {
+    const float dx = xi.x - xj.x, dy = xi.y - xj.y;
+    const float r2 = fmaf(dx, dx, dy * dy);
+    const float q = r2 * rsqrtf(fmaxf(r2, 1e-30f)) * P.inv_h;   // exactly 0 at r2 = 0
+    const float a = fmaxf(2.0f - q, 0.0f), c = fmaxf(1.0f - q, 0.0f);
+    return fmaf(-4.0f * c, c * c, a * a * a);
 }
 
-// W_cb polynomial of a list candidate (no validity mask: list padding points at the particle
-// itself and contributes exactly W(0) = 4, which the caller subtracts).
-__device__ __forceinline__ float w_list(const DevParams& P, float4 xi, float4 xj) {
-    const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-    const float r = r2 * rsqrtf(fmaxf(r2, 1e-30f));   // exactly 0 at r2 = 0
-    const float w = wcb_poly(r * P.inv_h);
-    return r2 < P.H2 ? w : 0.0f;
+// cell-scan fallback: candidates include the particle itself (valid = false)
+__device__ __forceinline__ float w_masked(const DevParams& P, float4 xi, float4 xj, bool valid) {
+    const float w = w_list(P, xi, xj);
+    return valid ? w : 0.0f;
 }
 
 // Load through the read-only path unless the data was written earlier in the same kernel.
@@ -317,7 +321,8 @@ __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& 
 
 template <bool NC>
 __device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D, int b, int i,
-                                           const float4* __restrict__ pv) {
+                                           const float4* __restrict__ pv_) {
+    const float4* __restrict__ pv = opaque(pv_);
     density_core<NC>(P, D, b, i, [&](uint32_t j) {
         const float4 v = ld<NC>(pv + j);
         return make_float2(v.x, v.y);
@@ -559,9 +564,7 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
                 }
                 if (DENS) {
                     const float2 xj = pos((uint32_t)j);
-                    const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-                    const float w = wcb_poly(r2 * rsqrtf(fmaxf(r2, 1e-30f)) * P.inv_h);
-                    wf += r2 < P.H2 ? w : 0.0f;
+                    wf += w_list(P, make_float4(xi.x, xi.y, 0.f, 0.f), make_float4(xj.x, xj.y, 0.f, 0.f));
                 }
             }
         }
@@ -769,18 +772,20 @@ __global__ void __launch_bounds__(TILE) k_nlist_density(DevParams P, DevPtrs D) 
 // d(q) = q (3q - 4) for q < 1 and -(2 - q)^2 for 1 <= q < 2 (Eq. cubicspline differentiated).
 // r2 is clamped before rsqrt, so the self pair and list padding (dx = dy = 0) and coincident
 // particles contribute exactly zero (zero gradient at r = 0, reading A8) without a mask.
+// d(q) by shape, branch-free: d = 4 max(1-q,0)^2 - max(2-q,0)^2 equals q(3q-4) for q < 1 and
+// -(2-q)^2 for 1 <= q < 2, and is exactly 0 beyond 2h (skin candidates of the list); see w_list
+// for why no canonical predicate is needed here.
 __device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2 ai, float4 xj,
                                            float2 aj, float& sx, float& sy) {
-    const float dx = __fsub_rn(xi.x, xj.x), dy = __fsub_rn(xi.y, xj.y);
-    const float r2 = dist2(dx, dy);
+    const float dx = xi.x - xj.x, dy = xi.y - xj.y;
+    const float r2 = fmaf(dx, dx, dy * dy);
     const float rs = rsqrtf(fmaxf(r2, 1e-30f));                    // 1 / r
     const float q = r2 * rs * P.inv_h;
-    const float t = 2.0f - q;
-    const float d = q < 1.0f ? q * (3.0f * q - 4.0f) : -(t * t);
+    const float t = fmaxf(2.0f - q, 0.0f), u = fmaxf(1.0f - q, 0.0f);
+    const float d = fmaf(4.0f * u, u, -(t * t));
     const float vr = (xi.z - xj.z) * dx + (xi.w - xj.w) * dy;
     const float visc = __fdividef(P.alpha2h * vr, (ai.x + aj.x) * (r2 + P.eps_h2));
-    float s = (visc - (ai.y + aj.y)) * (d * rs);
-    s = r2 < P.H2 ? s : 0.0f;                                      // exact predicate (A19)
+    const float s = (visc - (ai.y + aj.y)) * (d * rs);
     sx += s * dx;
     sy += s * dy;
 }
@@ -797,11 +802,12 @@ __device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2
 }
 
 // List walk of the force kernel: four candidates per 8-byte offset load.  PV / AX return the
-// state / aux of a slot (shared-memory window or global memory).
+// state / aux of a neighbour given its signed slot offset from i (pointer arithmetic relative
+// to slot i's own address: one PRMT/SHF + one LEA pair per neighbour, no 64-bit index math).
 template <class PV, class AX>
 __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __restrict__ nq, int n,
-                                           uint2 q0, int i, float4 xi, float2 ai, PV&& pvj,
-                                           AX&& axj, float& sx, float& sy) {
+                                           uint2 q0, float4 xi, float2 ai, PV&& pvj, AX&& axj,
+                                           float& sx, float& sy) {
     uint2 wn = q0;   // offsets stream from DRAM: keep the next quad's load in flight
     for (int k = 0; k < n; k += 4) {
         const uint2 w = wn;
@@ -809,17 +815,15 @@ __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __re
         if (k + 4 < n) wn = __ldg(nq);
         // pairs granularity: the second half of a quad only when some lane of the warp needs it
         // (padding entries are the particle itself: exact zero contribution)
-        const uint32_t j0 = (uint32_t)(i + quad_offset(w, 0));
-        const uint32_t j1 = (uint32_t)(i + quad_offset(w, 1));
-        const float4 x0 = pvj(j0), x1 = pvj(j1);
-        const float2 a0 = axj(j0), a1 = axj(j1);
+        const int d0 = quad_offset(w, 0), d1 = quad_offset(w, 1);
+        const float4 x0 = pvj(d0), x1 = pvj(d1);
+        const float2 a0 = axj(d0), a1 = axj(d1);
         pair_force(P, xi, ai, x0, a0, sx, sy);
         pair_force(P, xi, ai, x1, a1, sx, sy);
         if (k + 2 < n) {
-            const uint32_t j2 = (uint32_t)(i + quad_offset(w, 2));
-            const uint32_t j3 = (uint32_t)(i + quad_offset(w, 3));
-            const float4 x2 = pvj(j2), x3 = pvj(j3);
-            const float2 a2 = axj(j2), a3 = axj(j3);
+            const int d2 = quad_offset(w, 2), d3 = quad_offset(w, 3);
+            const float4 x2 = pvj(d2), x3 = pvj(d3);
+            const float2 a2 = axj(d2), a3 = axj(d3);
             pair_force(P, xi, ai, x2, a2, sx, sy);
             pair_force(P, xi, ai, x3, a3, sx, sy);
         }
@@ -836,12 +840,13 @@ struct BodyAcc {
 };
 
 // Forces, wall, integration and Verlet displacement of slot i (i < N) of rollout b.
-// pvj / axj read list neighbours (global or ring); pv / aux are the rollout's global rows
-// (cell-scan fallback of overflowing lists).
+// pvj(d) / axj(d) read list neighbour i + d (global or ring); pv / aux are the rollout's global
+// rows (cell-scan fallback of overflowing lists).  The body geometry is loaded after the list
+// walk so it does not occupy registers during it.
 template <class PV, class AX>
 __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs& D, float damping,
-                                               int b, int i, int cur, const Geom& gm,
-                                               const RolloutState* rs, float4 xi, float2 ai,
+                                               int b, int i, int cur, const RolloutState* rs,
+                                               float4 xi, float2 ai,
                                                const float4* __restrict__ pv,
                                                const float2* __restrict__ aux, PV&& pvj, AX&& axj,
                                                BodyAcc& acc) {
@@ -851,12 +856,13 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
     const uint2 q0 = __ldg(nq);            // first offsets, independent of the count load
     const int n = D.ncnt[o + i];
     if (n != NL_OVERFLOW) {
-        force_list(P, nq, n, q0, i, xi, ai, pvj, axj, sx, sy);
+        force_list(P, nq, n, q0, xi, ai, pvj, axj, sx, sy);
     } else {
         for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
             pair_force(P, xi, ai, __ldg(pv + j), __ldg(aux + j), j != (uint32_t)i, sx, sy);
         });
     }
+    const Geom gm = D.geom[b];
     float gxs = 0.0f, gys = 0.0f;   // sum_g G_ig
     const float4* gst = D.gst + (size_t)b * P.G;
     const float2* glo = D.glo + (size_t)b * P.G;
@@ -937,10 +943,11 @@ __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D,
     const float2* __restrict__ aux = D.aux + (size_t)b * P.NA;
     BodyAcc acc;
     if (i < P.N) {
-        const Geom gm = D.geom[b];
-        force_particle(P, D, damping, b, i, cur, gm, rs, pv[i], aux[i], pv, aux,
-                       [&](uint32_t j) { return __ldg(pv + j); },
-                       [&](uint32_t j) { return __ldg(aux + j); }, acc);
+        const float4* __restrict__ pvi = opaque(pv + i);
+        const float2* __restrict__ axi = opaque(aux + i);
+        force_particle(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
+                       [&](int d) { return __ldg(pvi + d); },
+                       [&](int d) { return __ldg(axi + d); }, acc);
     }
     write_partial(P, D, b, i >> 5, acc);
 }
@@ -973,15 +980,17 @@ __device__ __forceinline__ void force_ring_chunk(const DevParams& P, const DevPt
     const int cur = rs->sp ^ rs->need_rebin;
     const float4* __restrict__ pv = D.pv[cur] + (size_t)b * P.N;
     const float2* __restrict__ aux = D.aux + (size_t)b * P.NA;
-    const Geom gm = D.geom[b];
     if (rs->span > SW_T) {   // wide rows: plain gathers
         for (int t = ta; t < tb; ++t) {
             const int i = t * SW_T + threadIdx.x;
             BodyAcc acc;
-            if (i < P.N)
-                force_particle(P, D, damping, b, i, cur, gm, rs, pv[i], aux[i], pv, aux,
-                               [&](uint32_t j) { return __ldg(pv + j); },
-                               [&](uint32_t j) { return __ldg(aux + j); }, acc);
+            if (i < P.N) {
+                const float4* __restrict__ pvi = pv + i;
+                const float2* __restrict__ axi = aux + i;
+                force_particle(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
+                               [&](int d) { return __ldg(pvi + d); },
+                               [&](int d) { return __ldg(axi + d); }, acc);
+            }
             write_partial(P, D, b, i >> 5, acc);
         }
         return;
@@ -992,9 +1001,9 @@ __device__ __forceinline__ void force_ring_chunk(const DevParams& P, const DevPt
         BodyAcc acc;
         if (i < P.N) {
             const uint32_t s = (uint32_t)i & (RING - 1);
-            force_particle(P, D, damping, b, i, cur, gm, rs, ring_pv[s], ring_aux[s], pv, aux,
-                           [&](uint32_t j) { return ring_pv[j & (RING - 1)]; },
-                           [&](uint32_t j) { return ring_aux[j & (RING - 1)]; }, acc);
+            force_particle(P, D, damping, b, i, cur, rs, ring_pv[s], ring_aux[s], pv, aux,
+                           [&](int d) { return ring_pv[(uint32_t)(i + d) & (RING - 1)]; },
+                           [&](int d) { return ring_aux[(uint32_t)(i + d) & (RING - 1)]; }, acc);
         }
         write_partial(P, D, b, i >> 5, acc);
     });
