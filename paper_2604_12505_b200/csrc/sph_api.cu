@@ -38,6 +38,7 @@ struct sph_ctx {
     int small_grid = 0;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool fork = true;   // small path: rebuild branch concurrent with density/forces (SPH_FORK=0: serial)
     // live kernel timing inside the tick graph (sph_set_live_timing): event-record nodes around
     // the density / force launches of every live_every-th substep, read after each tick
     int live_every = 0;
@@ -316,6 +317,15 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
+    if (ctx->small && !ctx->fork) {   // serial: sort + lists/densities of the rebuilt rollouts first
+        k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
+        k_rebuild_small<false><<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
+        launch_nlist_density(ctx, s);
+        live_mark(ev, LV_DEN0, s);
+        launch_density(ctx, s, 1);
+        live_mark(ev, LV_DEN1, s);
+        return cudaSuccess;
+    }
     if (ctx->small) {   // (forces are launched by launch_substep, see there)
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
         cudaEventRecord(ctx->ev_fork, s);
@@ -354,7 +364,7 @@ static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool cap
         ev = ctx->live_ev.data() + (size_t)(k / ctx->live_every) * LIVE_SLOTS;
     live_mark(ev, LV_SUB0, s);
     cudaError_t e = launch_rebuild_and_density(ctx, capturing, ev);
-    if (ctx->small) {
+    if (ctx->small && ctx->fork) {
         // The rebuild branch (sort -> lists + densities of the rebuilt rollouts) runs on the side
         // stream concurrently with density AND forces of every other rollout; only the forces
         // of the rebuilt rollouts wait for it.
@@ -381,7 +391,7 @@ static int live_samples(const sph_ctx* ctx) {
 
 // kernels per substep: small path 5 (plan, rebuild_small, density, force, body); multi-kernel
 // path 4 + 8 rebuild kernels (the 8 run only in substeps where some rollout rebuilds).
-static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? 7 : 12; }
+static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? (ctx->fork ? 7 : 6) : 12; }
 
 static sph_status check_launch(sph_ctx* ctx) {
     cudaError_t e = cudaGetLastError();
@@ -506,6 +516,8 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             want = false;
         }
         if (want) {
+            const char* f = std::getenv("SPH_FORK");
+            ctx->fork = !(f && f[0] == '0');
             ctx->small = true;
             ctx->small_smem = smem;
             ctx->small_grid = std::max(1, std::min(P.B, nsm));
@@ -625,7 +637,7 @@ static sph_status accumulate_live(sph_ctx* ctx) {
         const cudaEvent_t* ev = ctx->live_ev.data() + (size_t)q * LIVE_SLOTS;
         CK(el(ev, LV_DEN0, LV_DEN1, &ctx->live_ms[SPH_LIVE_DENSITY]));
         CK(el(ev, LV_F1_0, LV_F1_1, &ctx->live_ms[SPH_LIVE_FORCE]));
-        if (ctx->small) CK(el(ev, LV_F2_0, LV_F2_1, &ctx->live_ms[SPH_LIVE_FORCE]));
+        if (ctx->small && ctx->fork) CK(el(ev, LV_F2_0, LV_F2_1, &ctx->live_ms[SPH_LIVE_FORCE]));
         CK(el(ev, LV_SUB0, LV_SUB1, &ctx->live_ms[SPH_LIVE_SUBSTEP]));
         ++ctx->live_n;
     }
