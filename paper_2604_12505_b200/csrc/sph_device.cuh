@@ -197,6 +197,13 @@ __device__ __forceinline__ const T* opaque(const T* p) {
     return p;
 }
 
+// sqrt.approx.ftz.f32 (one MUFU.SQRT; relative error ~2^-23, exactly 0 at 0)
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // t-th int16 offset (sign-extended) of a neighbour quad.
 __device__ __forceinline__ int quad_offset(uint2 w, int t) {
     const uint32_t h = (t & 2) ? w.y : w.x;

@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D);
 __device__ __forceinline__ float w_list(const DevParams& P, float4 xi, float4 xj) {
     const float dx = xi.x - xj.x, dy = xi.y - xj.y;
     const float r2 = fmaf(dx, dx, dy * dy);
-    const float q = r2 * rsqrtf(fmaxf(r2, 1e-30f)) * P.inv_h;   // exactly 0 at r2 = 0
+    const float q = sqrt_approx(r2) * P.inv_h;                  // exactly 0 at r2 = 0
     const float a = fmaxf(2.0f - q, 0.0f), c = fmaxf(1.0f - q, 0.0f);
     return fmaf(-4.0f * c, c * c, a * a * a);
 }
@@ -920,15 +920,20 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
 
 // Body partials: warp butterfly (deterministic order), one fp64 partial per warp of 32 slots,
 // index q = slot / 32 within the rollout (written straight to global memory, no CTA barrier).
+// The wall reaction and torque are zero for warps away from the wall (most of them): their
+// butterflies are skipped (the warp-uniform test is exact: a sum of zeros is zero).  The squared
+// displacement is >= 0, so its maximum is an unsigned maximum of the bit patterns (one REDUX).
 __device__ __forceinline__ void write_partial(const DevParams& P, const DevPtrs& D, int b, int q,
                                               BodyAcc a) {
+    if (__any_sync(0xffffffffu, a.fbx != 0.0f || a.fby != 0.0f || a.tq != 0.0f)) {
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        a.fbx += __shfl_xor_sync(0xffffffffu, a.fbx, d);
-        a.fby += __shfl_xor_sync(0xffffffffu, a.fby, d);
-        a.tq += __shfl_xor_sync(0xffffffffu, a.tq, d);
-        a.vmax = fmaxf(a.vmax, __shfl_xor_sync(0xffffffffu, a.vmax, d));
+        for (int d = 16; d > 0; d >>= 1) {
+            a.fbx += __shfl_xor_sync(0xffffffffu, a.fbx, d);
+            a.fby += __shfl_xor_sync(0xffffffffu, a.fby, d);
+            a.tq += __shfl_xor_sync(0xffffffffu, a.tq, d);
+        }
     }
+    a.vmax = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(a.vmax)));
     if ((threadIdx.x & 31) == 0 && q < P.npart)
         D.part[(size_t)b * P.npart + q] = make_double4(a.fbx, a.fby, a.tq, a.vmax);
 }
