@@ -151,6 +151,17 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
         P->chunk = std::min(P->chunk, P->nblk);
         P->nchunk = (P->nblk + P->chunk - 1) / P->chunk;
     }
+    {   // CTA sizes of the plain density / force kernels (env SPH_DTILE / SPH_FTILE for sweeps).
+        // Small CTAs win (C3 sweep): a CTA's slot frees only when its
+        // slowest warp ends, and list lengths / wall work differ from warp to warp.
+        auto pick = [](const char* name, int def) {
+            const char* e = std::getenv(name);
+            const int v = e ? std::atoi(e) : def;
+            return (v == 64 || v == 128 || v == 256 || v == 512 || v == 1024) ? v : def;
+        };
+        P->td = pick("SPH_DTILE", 128);
+        P->tf = pick("SPH_FTILE", 64);
+    }
     // ghost-ring window (see for_ghost_candidates): only particles farther than d_min from the
     // centre can have a ghost within 2h; their ghosts lie within +-dphi of their polar angle.
     // |x - g| < s with |x| = d, |g| = R  =>  d > R - s  and  sin(dphi/2) < s / (2 sqrt(d R)).
@@ -226,7 +237,13 @@ static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding) {
     if (P.ring)
         k_density_ring<<<dim3(P.nchunk, P.B), SW_T, kDensityRingSmem, s>>>(P, ctx->D, skip_rebuilding);
     else
-        k_density<<<gp, TILE, 0, s>>>(P, ctx->D, skip_rebuilding);
+        switch (P.td) {
+            case 1024: k_density<1024><<<dim3((P.N + 1023) / 1024, P.B), 1024, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            case 512: k_density<512><<<dim3((P.N + 511) / 512, P.B), 512, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            case 128: k_density<128><<<dim3((P.N + 127) / 128, P.B), 128, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            case 64: k_density<64><<<dim3((P.N + 63) / 64, P.B), 64, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            default: k_density<256><<<dim3((P.N + 255) / 256, P.B), 256, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+        }
 }
 
 // mode: 0 all rollouts, 1 non-rebuilding rollouts, 2 rebuilt rollouts (work list)
@@ -236,7 +253,13 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
     if (P.ring)
         k_force_ring<<<dim3(P.nchunk, gy), SW_T, kForceRingSmem, s>>>(P, ctx->D, damping, mode);
     else
-        k_force<<<dim3(P.ntile, gy), TILE, 0, s>>>(P, ctx->D, damping, mode);
+        switch (P.tf) {
+            case 1024: k_force<1024><<<dim3((P.N + 1023) / 1024, gy), 1024, 0, s>>>(P, ctx->D, damping, mode); break;
+            case 512: k_force<512><<<dim3((P.N + 511) / 512, gy), 512, 0, s>>>(P, ctx->D, damping, mode); break;
+            case 128: k_force<128><<<dim3((P.N + 127) / 128, gy), 128, 0, s>>>(P, ctx->D, damping, mode); break;
+            case 64: k_force<64><<<dim3((P.N + 63) / 64, gy), 64, 0, s>>>(P, ctx->D, damping, mode); break;
+            default: k_force<256><<<dim3((P.N + 255) / 256, gy), 256, 0, s>>>(P, ctx->D, damping, mode); break;
+        }
 }
 
 static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0) {

@@ -332,11 +332,14 @@ __device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D,
 // skip_rebuilding = 1 when rollouts that rebuild this substep get their densities from
 // k_nlist_density (which runs concurrently on another branch of the graph).
 // Plain variant: neighbour positions gathered from global memory through L1.
-__global__ void __launch_bounds__(TILE) k_density(DevParams P, DevPtrs D, int skip_rebuilding) {
+// TD slots per CTA: a CTA gathers from [t0 - span, t0 + TD + span), so larger CTAs touch fewer
+// window lines per own slot (fewer compulsory L1 misses); TD is chosen on the host.
+template <int TD>
+__global__ void __launch_bounds__(TD) k_density(DevParams P, DevPtrs D, int skip_rebuilding) {
     const int b = blockIdx.y;
     const RolloutState* rs = D.rs + b;
     if (rs->frozen || (skip_rebuilding && rs->need_rebin)) return;   // CTA-uniform
-    const int i = blockIdx.x * TILE + threadIdx.x;
+    const int i = blockIdx.x * TD + threadIdx.x;
     const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
     if (i < P.N) density_at<true>(P, D, b, i, pv);
 }
@@ -938,11 +941,12 @@ __device__ __forceinline__ void write_partial(const DevParams& P, const DevPtrs&
         D.part[(size_t)b * P.npart + q] = make_double4(a.fbx, a.fby, a.tq, a.vmax);
 }
 
+template <int TF>
 __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D, float damping,
                                            int b, int tile) {
     const RolloutState* rs = D.rs + b;
     if (rs->frozen) return;   // CTA-uniform (before any warp-level collective)
-    const int i = tile * TILE + threadIdx.x;
+    const int i = tile * TF + threadIdx.x;
     const int cur = rs->sp ^ rs->need_rebin;
     const float4* __restrict__ pv = D.pv[cur] + (size_t)b * P.N;
     const float2* __restrict__ aux = D.aux + (size_t)b * P.NA;
@@ -960,17 +964,19 @@ __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D,
 // mode 0: every rollout (grid.y = B); 1: rollouts that do NOT rebuild this substep (their
 // densities are ready while the rebuild branch still runs); 2: the rebuilt rollouts of the
 // work list (grid.y-stride over it), after the rebuild branch joined.
-__global__ void __launch_bounds__(TILE, SPH_FORCE_MINB) k_force(DevParams P, DevPtrs D,
-                                                                float damping, int mode) {
+// TF slots per CTA (see k_density); 40 registers at 48 resident warps per SM for every TF.
+template <int TF>
+__global__ void __launch_bounds__(TF, SPH_FORCE_MINB * TILE / TF) k_force(DevParams P, DevPtrs D,
+                                                                          float damping, int mode) {
     if (mode == 2) {
         const int count = *D.rcount;
         for (int w = blockIdx.y; w < count; w += gridDim.y)
-            force_tile(P, D, damping, D.rlist[w], blockIdx.x);
+            force_tile<TF>(P, D, damping, D.rlist[w], blockIdx.x);
         return;
     }
     const int b = blockIdx.y;
     if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
-    force_tile(P, D, damping, b, blockIdx.x);
+    force_tile<TF>(P, D, damping, b, blockIdx.x);
 }
 
 // Ring variant: CTA (x, y) walks super-tiles [x chunk, (x + 1) chunk) of rollout y (modes 0/1)
