@@ -238,11 +238,11 @@ static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding) {
         k_density_ring<<<dim3(P.nchunk, P.B), SW_T, kDensityRingSmem, s>>>(P, ctx->D, skip_rebuilding);
     else
         switch (P.td) {
-            case 1024: k_density<1024><<<dim3((P.N + 1023) / 1024, P.B), 1024, 0, s>>>(P, ctx->D, skip_rebuilding); break;
-            case 512: k_density<512><<<dim3((P.N + 511) / 512, P.B), 512, 0, s>>>(P, ctx->D, skip_rebuilding); break;
-            case 128: k_density<128><<<dim3((P.N + 127) / 128, P.B), 128, 0, s>>>(P, ctx->D, skip_rebuilding); break;
-            case 64: k_density<64><<<dim3((P.N + 63) / 64, P.B), 64, 0, s>>>(P, ctx->D, skip_rebuilding); break;
-            default: k_density<256><<<dim3((P.N + 255) / 256, P.B), 256, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            case 1024: k_density<1024><<<dim3(std::max(1, (P.N + 1023) / 1024), P.B), 1024, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            case 512: k_density<512><<<dim3(std::max(1, (P.N + 511) / 512), P.B), 512, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            case 128: k_density<128><<<dim3(std::max(1, (P.N + 127) / 128), P.B), 128, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            case 64: k_density<64><<<dim3(std::max(1, (P.N + 63) / 64), P.B), 64, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            default: k_density<256><<<dim3(std::max(1, (P.N + 255) / 256), P.B), 256, 0, s>>>(P, ctx->D, skip_rebuilding); break;
         }
 }
 
@@ -254,11 +254,11 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
         k_force_ring<<<dim3(P.nchunk, gy), SW_T, kForceRingSmem, s>>>(P, ctx->D, damping, mode);
     else
         switch (P.tf) {
-            case 1024: k_force<1024><<<dim3((P.N + 1023) / 1024, gy), 1024, 0, s>>>(P, ctx->D, damping, mode); break;
-            case 512: k_force<512><<<dim3((P.N + 511) / 512, gy), 512, 0, s>>>(P, ctx->D, damping, mode); break;
-            case 128: k_force<128><<<dim3((P.N + 127) / 128, gy), 128, 0, s>>>(P, ctx->D, damping, mode); break;
-            case 64: k_force<64><<<dim3((P.N + 63) / 64, gy), 64, 0, s>>>(P, ctx->D, damping, mode); break;
-            default: k_force<256><<<dim3((P.N + 255) / 256, gy), 256, 0, s>>>(P, ctx->D, damping, mode); break;
+            case 1024: k_force<1024><<<dim3(std::max(1, (P.N + 1023) / 1024), gy), 1024, 0, s>>>(P, ctx->D, damping, mode); break;
+            case 512: k_force<512><<<dim3(std::max(1, (P.N + 511) / 512), gy), 512, 0, s>>>(P, ctx->D, damping, mode); break;
+            case 128: k_force<128><<<dim3(std::max(1, (P.N + 127) / 128), gy), 128, 0, s>>>(P, ctx->D, damping, mode); break;
+            case 64: k_force<64><<<dim3(std::max(1, (P.N + 63) / 64), gy), 64, 0, s>>>(P, ctx->D, damping, mode); break;
+            default: k_force<256><<<dim3(std::max(1, (P.N + 255) / 256), gy), 256, 0, s>>>(P, ctx->D, damping, mode); break;
         }
 }
 
@@ -580,7 +580,7 @@ sph_status sph_set_state(sph_ctx* ctx, int rollout, const float* fluid_pv, const
     cudaStream_t s = ctx->stream;
     if (P.N > 0) {
         CK(cudaMemcpyAsync(ctx->D.xfer, fluid_pv, sizeof(float4) * P.N, cudaMemcpyHostToDevice, s));
-        k_import<<<dim3((P.N + 255) / 256, nb), 256, 0, s>>>(P, ctx->D, b0, ctx->D.xfer);
+        k_import<<<dim3(std::max(1, (P.N + 255) / 256), nb), 256, 0, s>>>(P, ctx->D, b0, ctx->D.xfer);
     }
     if (body) {
         for (int b = b0; b < b0 + nb; ++b)
