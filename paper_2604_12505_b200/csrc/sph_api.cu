@@ -161,6 +161,7 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
         };
         P->td = pick("SPH_DTILE", 128);
         P->tf = pick("SPH_FTILE", 64);
+        P->tn = pick("SPH_NTILE", 128);
     }
     // ghost-ring window (see for_ghost_candidates): only particles farther than d_min from the
     // centre can have a ghost within 2h; their ghosts lie within +-dphi of their polar angle.
@@ -286,7 +287,12 @@ static void launch_rebin(sph_ctx* ctx, cudaStream_t s = nullptr, bool with_nlist
 // lists + densities of the rebuilt rollouts (work list), spread over the whole GPU
 static void launch_nlist_density(sph_ctx* ctx, cudaStream_t s) {
     const DevParams& P = ctx->P;
-    k_nlist_density<<<dim3(P.ntile, std::min(P.B, 64)), TILE, 0, s>>>(P, ctx->D);
+    const int gy = std::min(P.B, 64);
+    switch (P.tn) {
+        case 256: k_nlist_density<256><<<dim3(std::max(1, (P.N + 255) / 256), gy), 256, 0, s>>>(P, ctx->D); break;
+        case 64: k_nlist_density<64><<<dim3(std::max(1, (P.N + 63) / 64), gy), 64, 0, s>>>(P, ctx->D); break;
+        default: k_nlist_density<128><<<dim3(std::max(1, (P.N + 127) / 128), gy), 128, 0, s>>>(P, ctx->D); break;
+    }
 }
 
 // Rebuild (only rollouts that need it) + densities.  Small path: the plan kernel builds the

@@ -58,7 +58,7 @@ struct DevParams {
                             //    env SPH_RING=1 (default 0: plain global-gather kernels)
     int nblk, chunk, nchunk;// ring kernels: super-tiles of SW_T slots per rollout, super-tiles
                             // per CTA, CTAs per rollout
-    int td, tf;             // slots (threads) per CTA of k_density / k_force (64 .. 1024)
+    int td, tf, tn;         // slots (threads) per CTA of k_density / k_force / k_nlist_density
     double dtd, m_body, J_body;
 };
 

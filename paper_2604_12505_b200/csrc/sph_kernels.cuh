@@ -734,9 +734,10 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
 // grid = (tiles, Y); CTA (x, y) handles tile x of work items y, y + Y, ...  The cell table,
 // slot cells and sorted state come from the sort (k_rebuild_small<false> or the grid-wide
 // rebuild kernels); the list just written by a thread is read back by the same thread.
-__global__ void __launch_bounds__(TILE) k_nlist_density(DevParams P, DevPtrs D) {
+template <int TN>
+__global__ void __launch_bounds__(TN) k_nlist_density(DevParams P, DevPtrs D) {
     const int count = *D.rcount;
-    const int i = blockIdx.x * TILE + threadIdx.x;
+    const int i = blockIdx.x * TN + threadIdx.x;
     for (int w = blockIdx.y; w < count; w += gridDim.y) {
         const int b = D.rlist[w];
         RolloutState* rs = D.rs + b;
