@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(TN) k_nlist_density(DevParams P, DevPtrs D) {
         const int b = D.rlist[w];
         RolloutState* rs = D.rs + b;
         const size_t o = (size_t)b * P.N;
-        const float4* __restrict__ pv = D.pv[rs->sp ^ 1] + o;   // sorted (rebuilt) buffer
+        const float4* __restrict__ pv = opaque(D.pv[rs->sp ^ 1] + o);   // sorted (rebuilt) buffer
         auto pos = [&](uint32_t j) {
             const float4 v = __ldg(pv + j);
             return make_float2(v.x, v.y);
