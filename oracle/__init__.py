@@ -71,6 +71,8 @@ def lib():
                                   C.c_void_p, C.c_double, C.c_double, _D, C.c_void_p,
                                   C.POINTER(C.c_int64)]
         L.orc_rollout.restype = C.c_int
+        L.orc_deriv.argtypes = [P, C.c_int, _D, C.c_int, _D, _D, _D]
+        L.orc_jacobian_fd.argtypes = [P, C.c_int, _D, C.c_int, _D, _D, C.c_double, _D, _D]
         L.orc_cells_f32.argtypes = [C.c_int, _F, C.c_float, C.c_float, C.c_float, _I32]
         L.orc_neighbours_f32.argtypes = [C.c_int, _F, C.c_float, _I64, _I32, C.c_int64]
         L.orc_neighbours_f32.restype = C.c_int64
@@ -155,6 +157,38 @@ def forces(sp, pos, vel, rho, P, gpos, gvel, body):
     lib().orc_forces(C.byref(params(sp)), n, pos, vel, _c(rho), _c(P), gpos.shape[0], gpos, gvel,
                      _c(body), acc, Fb, C.byref(Tb))
     return acc, Fb, Tb.value
+
+
+def state_vector(pos, vel, body):
+    """x = [pos (n x 2), vel (n x 2), r_x, r_y, theta, rd_x, rd_y, thd] (orc_deriv layout)."""
+    return np.concatenate([_c(pos).ravel(), _c(vel).ravel(), _c(body).ravel()])
+
+
+def deriv(sp, x, ghost_b, u=(0.0, 0.0, 0.0)):
+    """Continuous-time f(x, u) of Sigma in the state_vector layout."""
+    x = _c(x)
+    n = (x.shape[0] - 6) // 4
+    gb = _c(ghost_b)
+    out = np.zeros_like(x)
+    lib().orc_deriv(C.byref(params(sp)), n, x, gb.shape[0], gb, _c(u), out)
+    return out
+
+
+def jacobian_fd(sp, x, ghost_b, u=(0.0, 0.0, 0.0), h_rel=1e-7):
+    """Central-difference A = df/dx (n_x x n_x), B = df/du (n_x x 3) of f at (x, u).
+
+    Default step 1e-7 (not SPEC's 1e-6): f has kinks (the one-sided wall viscosity
+    min(v.r, 0), the kernels' higher derivatives at q = 1, 2 and r = h) and on C1 states a
+    1e-6 stencil straddles one for a few entries (1e-4 relative change between h and 2h);
+    at 1e-7 steps h and 2h agree to 2e-9 of max|A| and rounding stays ~eps |f| / h."""
+    x = _c(x)
+    nx = x.shape[0]
+    n = (nx - 6) // 4
+    gb = _c(ghost_b)
+    A = np.zeros((nx, nx))
+    B = np.zeros((nx, 3))
+    lib().orc_jacobian_fd(C.byref(params(sp)), n, x, gb.shape[0], gb, _c(u), float(h_rel), A, B)
+    return A, B
 
 
 class State:

@@ -485,3 +485,83 @@ int64_t orc_ghost_neighbours_f32(int n, const float* pos, int ng, const float* g
     }
     return tot <= cap ? tot : -1;
 }
+
+/* ---- linearization (P:259 item 2; SPEC linearization module) ----
+ * Continuous-time state-transition function f of Sigma (Eq. NLmodel) with the state
+ * laid out as x = [pos (n x 2, canonical id order), vel (n x 2), r_x, r_y, theta, rd_x, rd_y,
+ * thd], n_x = 4n + 6, and u = (u_x, u_y, tau):
+ *   d pos_i / dt = vel_i,  d vel_i / dt = a_i (Algorithm 1 l.1-8),
+ *   d r / dt = rd,  d rd / dt = (F_b + u_xy) / m_B,  d theta / dt = thd,
+ *   d thd / dt = (T_b + tau) / J   (Eq. tankdynamics).               */
+void orc_deriv(const orc_params* p, int n, const double* x, int ng, const double* gB,
+               const double* u, double* xdot) {
+    size_t nn = (size_t)(n > 0 ? n : 1), gg = (size_t)(ng > 0 ? ng : 1);
+    const double* pos = x;
+    const double* vel = x + 2 * (size_t)n;
+    const double* body = x + 4 * (size_t)n;
+    double* gpos = (double*)malloc(sizeof(double) * 2 * gg);
+    double* gvel = (double*)malloc(sizeof(double) * 2 * gg);
+    double* rho = (double*)malloc(sizeof(double) * nn);
+    double* P = (double*)malloc(sizeof(double) * nn);
+    double* acc = (double*)malloc(sizeof(double) * 2 * nn);
+    double Fb[2], Tb;
+    orc_ghosts(ng, gB, body, gpos, gvel);                                  /* l.1-3 */
+    orc_density(p, n, pos, ng, gpos, rho, P);                              /* l.5-6 */
+    orc_forces(p, n, pos, vel, rho, P, ng, gpos, gvel, body, acc, Fb, &Tb); /* l.7-9 */
+    for (int i = 0; i < 2 * n; i++) {
+        xdot[i] = vel[i];
+        xdot[2 * (size_t)n + i] = acc[i];
+    }
+    double* bd = xdot + 4 * (size_t)n;
+    bd[0] = body[3];
+    bd[1] = body[4];
+    bd[2] = body[5];
+    bd[3] = (Fb[0] + u[0]) / p->m_body;
+    bd[4] = (Fb[1] + u[1]) / p->m_body;
+    bd[5] = (Tb + u[2]) / p->J_body;
+    free(gpos);
+    free(gvel);
+    free(rho);
+    free(P);
+    free(acc);
+}
+
+/* Central finite-difference Jacobian of f (the definition of the derivative, written out):
+ * column j of A = (f(x + e_j h_j, u) - f(x - e_j h_j, u)) / (2 h_j), h_j = h_rel max(1, |x_j|);
+ * B likewise for u.  A is n_x x n_x and B n_x x 3, row-major.  Truncation error O(h^2 f^(3)),
+ * rounding O(eps |f| / h). */
+void orc_jacobian_fd(const orc_params* p, int n, const double* x, int ng, const double* gB,
+                     const double* u, double h_rel, double* A, double* B) {
+    const int nx = 4 * n + 6;
+    double* xp = (double*)malloc(sizeof(double) * (size_t)nx);
+    double* fp = (double*)malloc(sizeof(double) * (size_t)nx);
+    double* fm = (double*)malloc(sizeof(double) * (size_t)nx);
+    double up[3], um[3];
+    for (int j = 0; j < nx + 3; j++) {
+        memcpy(xp, x, sizeof(double) * (size_t)nx);
+        for (int c = 0; c < 3; c++) up[c] = um[c] = u[c];
+        double hj;
+        if (j < nx) {
+            hj = h_rel * fmax(1.0, fabs(x[j]));
+            xp[j] = x[j] + hj;
+            orc_deriv(p, n, xp, ng, gB, u, fp);
+            xp[j] = x[j] - hj;
+            orc_deriv(p, n, xp, ng, gB, u, fm);
+        } else {
+            const int c = j - nx;
+            hj = h_rel * fmax(1.0, fabs(u[c]));
+            up[c] = u[c] + hj;
+            um[c] = u[c] - hj;
+            orc_deriv(p, n, x, ng, gB, up, fp);
+            orc_deriv(p, n, x, ng, gB, um, fm);
+        }
+        for (int r = 0; r < nx; r++) {
+            const double d = (fp[r] - fm[r]) / (2.0 * hj);
+            if (j < nx) A[(size_t)r * nx + j] = d;
+            else B[(size_t)r * 3 + (j - nx)] = d;
+        }
+    }
+    free(xp);
+    free(fp);
+    free(fm);
+}

@@ -66,6 +66,16 @@ int orc_rollout(const orc_params* p, int n, double* pos, double* vel, int ng, co
                 double* body, int K, int n_sub, const double* u_seq, const double* theta_ref,
                 double Kp, double Kd, double* y_out, double* u_applied, int64_t* bad_step);
 
+/* ---- linearization -------------------------------- */
+/* Continuous-time f(x, u) of Sigma: x = [pos (n x 2), vel (n x 2), r_x, r_y, theta,
+ * rd_x, rd_y, thd] (n_x = 4n + 6), u = (u_x, u_y, tau); xdot[n_x]. */
+void orc_deriv(const orc_params* p, int n, const double* x, int ng, const double* gB,
+               const double* u, double* xdot);
+/* Central-difference Jacobian A = df/dx (n_x x n_x), B = df/du (n_x x 3), row-major, step
+ * h_j = h_rel max(1, |x_j|) (SPEC linearization: h_rel = 1e-6). */
+void orc_jacobian_fd(const orc_params* p, int n, const double* x, int ng, const double* gB,
+                     const double* u, double h_rel, double* A, double* B);
+
 /* ---- float32 parity predicates (reading A19), evaluated on given float32 values ----- */
 /* Cell of each point: c_x = floor((x - o_x) * inv) with IEEE float32 ops, no contraction.
  * o = (float)body_r - half.  cells[n][2]. */

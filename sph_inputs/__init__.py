@@ -174,6 +174,22 @@ def make_tank(ell: float = 1.0, fill: float | None = 0.5, n_first: int | None = 
     return Tank(p, pos, np.zeros_like(pos), ghost_ring(ng, p.R))
 
 
+def moving_tank(ell: float = 1.0, seed: int = 1, jitter: float = 0.05, vel: float = 0.01,
+                body=None) -> Tank:
+    """Jittered lattice with random velocities (an unsettled, fully active state: one-step and
+    linearization parity), rigidly placed at the body pose ``body`` = (r_x, r_y, th, rd_x,
+    rd_y, thd) when given; snapped to float32-representable values."""
+    t = make_tank(ell, jitter=jitter, seed=seed)
+    t.vel = np.random.Generator(np.random.Philox(seed + 100)).normal(0, vel, t.pos.shape)
+    if body is not None:
+        th = body[2]
+        c, s = math.cos(th), math.sin(th)
+        p = t.pos.copy()
+        t.pos = np.stack([c * p[:, 0] - s * p[:, 1] + body[0], s * p[:, 0] + c * p[:, 1] + body[1]], 1)
+        t.body = np.asarray(body, np.float64)
+    return t.snapped()
+
+
 def random_tank(n_fluid: int, n_ghost: int, seed: int, h: float = H_PAPER, R: float = 0.03,
                 vel_scale: float = 0.02, **over) -> Tank:
     """Small random (non-lattice) tank for parity edge cases: uniform points in the disk."""
