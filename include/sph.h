@@ -183,6 +183,25 @@ enum { SPH_LIVE_DENSITY = 0, SPH_LIVE_FORCE = 1, SPH_LIVE_SUBSTEP = 2, SPH_NUM_L
 sph_status sph_set_live_timing(sph_ctx* ctx, int every);
 sph_status sph_get_live_timing(sph_ctx* ctx, double* ms_sum, int64_t* n_samples, int reset);
 
+/* Linearization (P:259 item 2 "exact and efficient computation of the Jacobian
+ * of the state transition function", P:408-413 eigenvalues of the linearized open-loop system).
+ * Jacobians of the continuous-time model f(x, u) (Eq. NLmodel; Algorithm 1 l.1-8,
+ * Eq. tankdynamics) at rollout `rollout`'s current state:
+ *   x = [pos (n_fluid x 2, canonical id order), vel (n_fluid x 2), r_x, r_y, theta, rd_x, rd_y,
+ *        thd], n_x = 4 n_fluid + 6;  u = (u_x, u_y, tau);
+ *   f = [vel, a, rd, thd, (F_b + u_xy) / m_B, (T_b + tau) / J].
+ * f is affine in u, so A and B do not depend on the input.  Forward-mode (tangent-linear)
+ * differentiation in float64 on the GPU, one unit seed per column; the operating point is the
+ * float32 state converted exactly to float64; neighbour sets are the float64 predicates
+ * |x_i - x_j|^2 < (2h)^2, |x_i - x_g|^2 < (2h)^2 / h^2 at that point (held fixed: kernel values
+ * and gradients vanish at the support).
+ * A: n_x x n_x, B: n_x x 3, row-major float64, caller-owned; device pointers (ctx stream) if
+ * ptr_on_device, else host (the call synchronises).  Transient device scratch of
+ * ~300 MB + (host pointers) 8 n_x^2 bytes is allocated stream-ordered and released.
+ * Errors: SPH_EINVAL bad arguments; SPH_ENOMEM more than 48 fluid neighbours or ghosts around
+ * one particle; SPH_ECUDA allocation / launch failure. */
+sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr_on_device);
+
 /* Per-rollout counters (host arrays of B, nullable): substeps taken and cell-list / neighbour-
  * list rebuilds performed (with rebin_every = 0 rebuilds happen only when the displacement
  * bound requires them). */

@@ -72,6 +72,7 @@ def lib():
             "sph_set_live_timing": (i32, [vp, i32]),
             "sph_get_live_timing": (i32, [vp, vp, vp, i32]),
             "sph_launches_per_substep": (i32, [vp]),
+            "sph_jacobian": (i32, [vp, i32, vp, vp, i32]),
             "sph_get_counters": (i32, [vp, vp, vp]),
             "sph_get_sizes": (None, [vp, vp, vp, vp, vp]),
             "sph_last_error": (C.c_char_p, [vp]),
@@ -90,7 +91,7 @@ def exported_symbols():
             "sph_get_particles", "sph_get_ghosts", "sph_step", "sph_rollout_batch",
             "sph_get_body_state", "sph_settle", "sph_get_status", "sph_debug_cells",
             "sph_debug_neighbours", "sph_profile_substeps", "sph_set_live_timing", "sph_get_live_timing",
-            "sph_launches_per_substep", "sph_get_counters",
+            "sph_launches_per_substep", "sph_get_counters", "sph_jacobian",
             "sph_get_sizes", "sph_last_error", "sph_destroy"]
 
 
@@ -306,6 +307,26 @@ class SphContext:
         out = {name: (float(v) / k if k else None) for name, v in zip(LIVE_NAMES, ms)}
         out["samples"] = k
         return out
+
+    def jacobian(self, rollout: int = 0, device: bool = False):
+        """Linearization of the continuous-time model at the rollout's current state
+        (sph_jacobian): returns (A [n_x, n_x], B [n_x, 3]) float64, x = [pos, vel, r, theta,
+        rd, thd].  device=True: CUDA tensors (no host round trip), else numpy arrays."""
+        nx = 4 * self.N + 6
+        if device:
+            torch = self.torch
+            A = torch.empty((nx, nx), dtype=torch.float64, device=self.device)
+            B = torch.empty((nx, 3), dtype=torch.float64, device=self.device)
+            self._dev_in(A)
+            self._check(self.L.sph_jacobian(self.ctx, int(rollout), A.data_ptr(), B.data_ptr(), 1),
+                        "sph_jacobian")
+            self._dev_out()
+            return A, B
+        A = np.empty((nx, nx), np.float64)
+        B = np.empty((nx, 3), np.float64)
+        self._check(self.L.sph_jacobian(self.ctx, int(rollout), A.ctypes.data, B.ctypes.data, 0),
+                    "sph_jacobian")
+        return A, B
 
     def counters(self):
         steps = np.zeros(self.B, np.int64)

@@ -14,12 +14,15 @@
 
 #include "../../include/sph.h"
 #include "sph_kernels.cuh"
+#include "sph_jac.cuh"
 
 using namespace sph;
 
 struct sph_ctx {
     DevParams P;
     DevPtrs D;
+    sph_fluid_params fp;   // float64 parameters as given (linearization works in float64)
+    sph_body_params bp;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     float ghost_angle0 = 0.f;
@@ -494,6 +497,8 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
     }
     sph_ctx* ctx = new sph_ctx();
     ctx->P = P;
+    ctx->fp = *fp;
+    ctx->bp = *bp;
     ctx->n_sub = tp->substeps_per_sample;
     ctx->ghost_angle0 = (float)a0;
     carve(P, (char*)d_workspace, &ctx->D);
@@ -917,6 +922,100 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
 }
 
 int sph_launches_per_substep(const sph_ctx* ctx) { return ctx ? launches_per_substep(ctx) : 0; }
+
+sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr_on_device) {
+    if (!ctx || !A || !B) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    if (rollout < 0 || rollout >= P.B) return fail(ctx, SPH_EINVAL, "rollout out of range");
+    cudaStream_t s = ctx->stream;
+    const int N = P.N, G = P.G, nx = 4 * N + 6, nd = nx + 3;
+    JacParams J;
+    J.N = N;
+    J.G = G;
+    J.nx = nx;
+    J.h = ctx->fp.h;
+    J.m = ctx->fp.mass;
+    J.rho0 = ctx->fp.rho0;
+    J.k = ctx->fp.k;
+    J.gamma1 = ctx->fp.gamma1;
+    J.alpha2h = 2.0 * ctx->fp.alpha * ctx->fp.h;
+    J.beta = ctx->fp.beta;
+    J.eps_h2 = ctx->fp.eps * ctx->fp.h * ctx->fp.h;
+    J.m2 = ctx->fp.mass * ctx->fp.mass;
+    J.sgn2m2 = ctx->fp.ghost_pressure_sign * 2.0 * J.m2;
+    J.mB = ctx->bp.m;
+    J.J = ctx->bp.J;
+    J.H2 = 4.0 * J.h * J.h;
+    J.h2 = J.h * J.h;
+    J.wc = ctx->fp.w_cb_const;
+    J.ws = 10.0 / M_PI;
+    // seeds per chunk: tangent densities + columns within ~256 MB of scratch
+    const size_t per_seed = 8 * ((size_t)N + (size_t)nx);
+    const int Dc = (int)std::max<size_t>(1, std::min<size_t>((size_t)nd, (256u << 20) / per_seed));
+    const size_t n1 = (size_t)std::max(N, 1), g1 = (size_t)std::max(G, 1);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off += (bytes + 255) & ~(size_t)255;
+        return o;
+    };
+    const size_t o_pos = take(16 * n1), o_vel = take(16 * n1), o_body = take(48), o_gB = take(16 * g1),
+                 o_gp = take(16 * g1), o_gv = take(16 * g1), o_ga = take(16 * g1),
+                 o_nfc = take(4 * n1), o_nf = take(4 * n1 * JAC_NCAP), o_g2c = take(4 * n1),
+                 o_g2 = take(4 * n1 * JAC_GCAP), o_g1c = take(4 * n1), o_g1 = take(4 * n1 * JAC_GCAP),
+                 o_rho = take(8 * n1), o_P = take(8 * n1), o_Q = take(8 * n1),
+                 o_drho = take(8 * n1 * Dc), o_At = take(8 * (size_t)nx * Dc), o_ovf = take(4),
+                 o_A = ptr_on_device ? 0 : take(8 * (size_t)nx * nx), o_B = ptr_on_device ? 0 : take(24 * (size_t)nx);
+    char* scratch = nullptr;
+    CK(cudaMallocAsync((void**)&scratch, off, s));
+    JacPtrs X;
+    X.pos = (const double2*)(scratch + o_pos);
+    X.vel = (const double2*)(scratch + o_vel);
+    X.body = (const double*)(scratch + o_body);
+    X.gB = (const double2*)(scratch + o_gB);
+    X.gpos = (double2*)(scratch + o_gp);
+    X.gvel = (double2*)(scratch + o_gv);
+    X.garm = (double2*)(scratch + o_ga);
+    X.nf_cnt = (int*)(scratch + o_nfc);
+    X.nf = (int*)(scratch + o_nf);
+    X.g2_cnt = (int*)(scratch + o_g2c);
+    X.g2 = (int*)(scratch + o_g2);
+    X.g1_cnt = (int*)(scratch + o_g1c);
+    X.g1 = (int*)(scratch + o_g1);
+    X.rho = (double*)(scratch + o_rho);
+    X.P = (double*)(scratch + o_P);
+    X.Q = (double*)(scratch + o_Q);
+    X.drho = (double*)(scratch + o_drho);
+    X.At = (double*)(scratch + o_At);
+    X.overflow = (int*)(scratch + o_ovf);
+    double* dA = ptr_on_device ? A : (double*)(scratch + o_A);
+    double* dB = ptr_on_device ? B : (double*)(scratch + o_B);
+    auto release = [&]() { cudaFreeAsync(scratch, s); };
+    cudaMemsetAsync(X.overflow, 0, 4, s);
+    if (G) cudaMemcpyAsync((void*)X.gB, ctx->D.ghost_b, 16 * (size_t)G, cudaMemcpyDeviceToDevice, s);
+    k_jac_import<<<std::max(1, (std::max(N, 6) + 127) / 128), 128, 0, s>>>(
+        P, ctx->D, rollout, (double2*)X.pos, (double2*)X.vel, (double*)X.body);
+    if (G) k_jac_ghosts<<<(G + 127) / 128, 128, 0, s>>>(J, X);
+    if (N) k_jac_prep<<<(N + 127) / 128, 128, 0, s>>>(J, X);
+    for (int d0 = 0; d0 < nd; d0 += Dc) {
+        const int dc = std::min(Dc, nd - d0);
+        if (N) k_jac_drho<<<dim3((N + 127) / 128, dc), 128, 0, s>>>(J, X, d0);
+        k_jac_col<<<dc, JAC_T, 0, s>>>(J, X, d0);
+        k_jac_store<<<dim3((dc + 31) / 32, (nx + 31) / 32), dim3(32, 8), 0, s>>>(J, X.At, d0, dc, dA, dB);
+    }
+    int ovf = 0;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&ovf, X.overflow, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && !ptr_on_device) {
+        e = cudaMemcpyAsync(A, dA, 8 * (size_t)nx * nx, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(B, dB, 24 * (size_t)nx, cudaMemcpyDeviceToHost, s);
+    }
+    release();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(ctx, SPH_ECUDA, std::string("sph_jacobian: ") + cudaGetErrorString(e));
+    if (ovf) return fail(ctx, SPH_ENOMEM, "sph_jacobian: more than 48 neighbours or ghosts of one particle");
+    return SPH_OK;
+}
 
 sph_status sph_get_counters(sph_ctx* ctx, int64_t* steps, int32_t* rebuilds) {
     if (!ctx) return SPH_EINVAL;
