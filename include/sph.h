@@ -196,8 +196,8 @@ sph_status sph_get_live_timing(sph_ctx* ctx, double* ms_sum, int64_t* n_samples,
  * |x_i - x_j|^2 < (2h)^2, |x_i - x_g|^2 < (2h)^2 / h^2 at that point (held fixed: kernel values
  * and gradients vanish at the support).
  * A: n_x x n_x, B: n_x x 3, row-major float64, caller-owned; device pointers (ctx stream) if
- * ptr_on_device, else host (the call synchronises).  Transient device scratch of
- * ~300 MB + (host pointers) 8 n_x^2 bytes is allocated stream-ordered and released.
+ * ptr_on_device, else host (the call synchronises).  Device scratch of O(n_fluid) (+ 8 n_x^2
+ * bytes for host pointers) is kept by the context for later calls (freed by sph_destroy).
  * Errors: SPH_EINVAL bad arguments; SPH_ENOMEM more than 48 fluid neighbours or ghosts around
  * one particle; SPH_ECUDA allocation / launch failure. */
 sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr_on_device);

@@ -48,6 +48,9 @@ struct sph_ctx {
     std::vector<cudaEvent_t> live_ev;   // [sampled substep][LIVE_SLOTS]
     double live_ms[SPH_NUM_LIVE] = {0, 0, 0};
     int64_t live_n = 0;
+    // linearization scratch (sph_jacobian), kept between calls
+    void* jac_buf = nullptr;
+    size_t jac_bytes = 0;
 };
 
 // event slots of one sampled substep
@@ -949,10 +952,8 @@ sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr
     J.h2 = J.h * J.h;
     J.wc = ctx->fp.w_cb_const;
     J.ws = 10.0 / M_PI;
-    // seeds per chunk: tangent densities + columns within ~256 MB of scratch
-    const size_t per_seed = 8 * ((size_t)N + (size_t)nx);
-    const int Dc = (int)std::max<size_t>(1, std::min<size_t>((size_t)nd, (256u << 20) / per_seed));
     const size_t n1 = (size_t)std::max(N, 1), g1 = (size_t)std::max(G, 1);
+    const int nblk = std::max(1, (N + JAC_T - 1) / JAC_T);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -964,10 +965,18 @@ sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr
                  o_nfc = take(4 * n1), o_nf = take(4 * n1 * JAC_NCAP), o_g2c = take(4 * n1),
                  o_g2 = take(4 * n1 * JAC_GCAP), o_g1c = take(4 * n1), o_g1 = take(4 * n1 * JAC_GCAP),
                  o_rho = take(8 * n1), o_P = take(8 * n1), o_Q = take(8 * n1),
-                 o_drho = take(8 * n1 * Dc), o_At = take(8 * (size_t)nx * Dc), o_ovf = take(4),
+                 o_hc = take(4 * n1), o_hop = take(4 * n1 * JAC_HCAP),
+                 o_drho = take(8 * n1 * 9), o_ovf = take(4), o_bp = take(8 * 9 * 3 * (size_t)nblk),
                  o_A = ptr_on_device ? 0 : take(8 * (size_t)nx * nx), o_B = ptr_on_device ? 0 : take(24 * (size_t)nx);
-    char* scratch = nullptr;
-    CK(cudaMallocAsync((void**)&scratch, off, s));
+    if (ctx->jac_bytes < off) {   // grow the cached scratch (kept for the next call)
+        CK(cudaStreamSynchronize(s));
+        if (ctx->jac_buf) cudaFree(ctx->jac_buf);
+        ctx->jac_buf = nullptr;
+        ctx->jac_bytes = 0;
+        CK(cudaMalloc(&ctx->jac_buf, off));
+        ctx->jac_bytes = off;
+    }
+    char* scratch = (char*)ctx->jac_buf;
     JacPtrs X;
     X.pos = (const double2*)(scratch + o_pos);
     X.vel = (const double2*)(scratch + o_vel);
@@ -985,23 +994,34 @@ sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr
     X.rho = (double*)(scratch + o_rho);
     X.P = (double*)(scratch + o_P);
     X.Q = (double*)(scratch + o_Q);
+    X.hop_cnt = (int*)(scratch + o_hc);
+    X.hop = (int*)(scratch + o_hop);
     X.drho = (double*)(scratch + o_drho);
-    X.At = (double*)(scratch + o_At);
     X.overflow = (int*)(scratch + o_ovf);
+    X.bpart = (double*)(scratch + o_bp);
     double* dA = ptr_on_device ? A : (double*)(scratch + o_A);
     double* dB = ptr_on_device ? B : (double*)(scratch + o_B);
-    auto release = [&]() { cudaFreeAsync(scratch, s); };
+    X.A = dA;
+    X.B = dB;
+    cudaMemsetAsync(dA, 0, 8 * (size_t)nx * nx, s);   // A is sparse: seeds write only their rows
+    cudaMemsetAsync(dB, 0, 24 * (size_t)nx, s);
     cudaMemsetAsync(X.overflow, 0, 4, s);
     if (G) cudaMemcpyAsync((void*)X.gB, ctx->D.ghost_b, 16 * (size_t)G, cudaMemcpyDeviceToDevice, s);
     k_jac_import<<<std::max(1, (std::max(N, 6) + 127) / 128), 128, 0, s>>>(
         P, ctx->D, rollout, (double2*)X.pos, (double2*)X.vel, (double*)X.body);
     if (G) k_jac_ghosts<<<(G + 127) / 128, 128, 0, s>>>(J, X);
-    if (N) k_jac_prep<<<(N + 127) / 128, 128, 0, s>>>(J, X);
-    for (int d0 = 0; d0 < nd; d0 += Dc) {
-        const int dc = std::min(Dc, nd - d0);
+    if (N) {
+        k_jac_prep<<<(32 * N + 127) / 128, 128, 0, s>>>(J, X);   // one warp per particle
+        k_jac_hops<<<(N + JAC_HOPS_WARPS - 1) / JAC_HOPS_WARPS, 32 * JAC_HOPS_WARPS,
+                     sizeof(int) * JAC_HOPS_WARPS * JAC_CAND, s>>>(J, X);
+    }
+    // particle seeds (columns 0 .. 4N-1): one CTA each, writes its two-hop rows into A
+    if (N) k_jac_pseed<<<4 * N, JAC_PT, 0, s>>>(J, X, 0);
+    {   // body and input seeds (6 + 3 columns): every particle may respond, dense columns
+        const int d0 = 4 * N, dc = 9;
         if (N) k_jac_drho<<<dim3((N + 127) / 128, dc), 128, 0, s>>>(J, X, d0);
-        k_jac_col<<<dc, JAC_T, 0, s>>>(J, X, d0);
-        k_jac_store<<<dim3((dc + 31) / 32, (nx + 31) / 32), dim3(32, 8), 0, s>>>(J, X.At, d0, dc, dA, dB);
+        k_jac_col<<<dim3(nblk, dc), JAC_T, 0, s>>>(J, X, d0);
+        k_jac_body<<<dc, 32, 0, s>>>(J, X, d0, nblk);
     }
     int ovf = 0;
     cudaError_t e = cudaGetLastError();
@@ -1010,10 +1030,9 @@ sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr
         e = cudaMemcpyAsync(A, dA, 8 * (size_t)nx * nx, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaMemcpyAsync(B, dB, 24 * (size_t)nx, cudaMemcpyDeviceToHost, s);
     }
-    release();
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return fail(ctx, SPH_ECUDA, std::string("sph_jacobian: ") + cudaGetErrorString(e));
-    if (ovf) return fail(ctx, SPH_ENOMEM, "sph_jacobian: more than 48 neighbours or ghosts of one particle");
+    if (ovf) return fail(ctx, SPH_ENOMEM, "sph_jacobian: more than 48 neighbours or ghosts, or 192 two-hop neighbours, of one particle");
     return SPH_OK;
 }
 
@@ -1049,6 +1068,7 @@ void sph_destroy(sph_ctx* ctx) {
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     for (auto e : ctx->live_ev) cudaEventDestroy(e);
+    if (ctx->jac_buf) cudaFree(ctx->jac_buf);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

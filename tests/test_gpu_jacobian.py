@@ -50,9 +50,10 @@ def test_jacobian_matches_oracle_fd(case):
     Ao, Bo = O.jacobian_fd(t.params, x, t.ghost_b, (5.0, 2.0, 1.0))
     n = t.n_fluid
     assert A.shape == (4 * n + 6, 4 * n + 6) and B.shape == (4 * n + 6, 3)
-    assert _block_err(A, Ao, n) <= 1e-6
+    # the oracle's central differences are accurate to ~2e-9 of max|A| (its step-convergence
+    # pin); the analytic float64 Jacobian agrees to that level
+    assert _block_err(A, Ao, n) <= 5e-7       # per block: FD rounding floor of small blocks
     assert np.abs(B - Bo).max() <= 1e-9 * np.abs(Bo).max()
-    # the FD step halves the stencil error: the analytic Jacobian sits inside it
     ctx.close()
 
 
