@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN"],
+                    help="LIN: linearization (SURVEY 8(f) f1) of the paper's P0 tank, not the north star")
     ap.add_argument("--rollouts", type=int, default=0, help="override rollouts per GPU")
     ap.add_argument("--rebin-every", type=int, default=0,
                     help="1: rebuild cell list + neighbour lists every substep; 0: adaptive (skin)")
@@ -443,8 +444,97 @@ def ctx_bytes_gb(t, B):
     return B * t.n_fluid * 64 / 1e9
 
 
+# ------------------------------------------------------------------------------------------
+# Linearization: full Jacobians of the continuous-time model
+# ------------------------------------------------------------------------------------------
+LIN_METRIC = "Jacobians/s (A = df/dx, B = df/du, float64 forward mode) of the P0 tank"
+
+
+def lin_point(device):
+    """P0 tank (the paper's 666-particle benchmark) after 0.2 s of actuation
+    u = (5 N, 2 N, 1 N m) from the lattice: an active operating point (GPU product path)."""
+    from paper_2604_12505_b200 import SphContext
+    t = si.make_tank(1.0, n_first=666)
+    ctx = SphContext(t.params, t.pv32(), t.ghost_b, n_rollouts=1, device=device)
+    ctx.step(np.array([[5.0, 2.0, 1.0]], np.float32), 200)
+    return t, ctx
+
+
+def run_linearize(a):
+    import torch
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    t, ctx = lin_point(local)
+    nx = 4 * t.n_fluid + 6
+    for _ in range(max(a.warmup, 1)):
+        A, B = ctx.jacobian(0, device=True)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    for _ in range(a.steps):
+        A, B = ctx.jacobian(0, device=True)
+    e1.record(ctx.stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    # e2e: host buffers through the C ABI (D2H of A and B inside)
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record(ctx.stream)
+    for _ in range(2):
+        Ah, Bh = ctx.jacobian(0)
+    x1.record(ctx.stream)
+    torch.cuda.synchronize()
+    e2e_ms = x0.elapsed_time(x1) / 2
+    # eigenvalues of the device matrix (sph_eigenvalues: cuSOLVER Xgeev, a library call)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev = ctx.eigenvalues(A)
+    torch.cuda.synchronize()
+    eig_ms = (time.perf_counter() - t0) * 1e3
+    out_bytes = 8.0 * (nx * nx + 3 * nx)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    achieved = out_bytes / (ms / 1e3) / 1e9
+    cpu = None
+    if not a.no_cpu_baseline:
+        import oracle as O
+        pv = ctx.get_particles(0).astype(np.float64)
+        x = O.state_vector(pv[:, :2], pv[:, 2:], ctx.get_body_state()[0])
+        c0 = time.perf_counter()
+        O.jacobian_fd(t.params, x, t.ghost_b)
+        dt = time.perf_counter() - c0
+        cpu = {"value": 1.0 / dt, "unit": "Jacobians/s", "cores": 1, "kind": "oracle",
+               "sample": f"1 central-difference Jacobian of the same P0 point (2 x {nx + 3} evaluations of f), float64 C oracle, 1 thread, {dt:.1f} s"}
+    ctx.close()
+    line = {
+        "metric": LIN_METRIC, "value": 1e3 / ms, "unit": "Jacobians/s", "n_gpus": 1, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "none",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (P0 lattice tank, 0.2 s actuated)",
+        "config": {"workload": f"LIN: P0 tank (666 fluid + 236 ghosts), n_x = {nx}, columns {nx + 3}",
+                   "columns_per_s": (nx + 3) * 1e3 / ms, "eig_ms_cusolver_xgeev": eig_ms,
+                   "spectral_radius": float(ev.abs().max())},
+        "e2e": {"value": 1e3 / e2e_ms, "unit": "Jacobians/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": int(out_bytes)},
+        "gpu_launches": a.steps * 6,
+        "clocks": ck,
+        "roofline": {"bound": "hbm", "kernel": "sph_jacobian (all launches)", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "note": "algorithmic bytes = the dense float64 A and B written once; at P0 size the call is launch/latency bound"},
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     a = parse()
+    if a.workload == "LIN":
+        run_linearize(a)
+        return
     if a.impl == "reference":
         run_reference(a)
     else:

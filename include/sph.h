@@ -202,6 +202,14 @@ sph_status sph_get_live_timing(sph_ctx* ctx, double* ms_sum, int64_t* n_samples,
  * one particle; SPH_ECUDA allocation / launch failure. */
 sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr_on_device);
 
+/* Eigenvalues of a dense real n x n float64 matrix (Figs. 5-6: spectra of the
+ * linearized systems), by the GPU library eigensolver (cuSOLVER Xgeev, no eigenvectors) on the
+ * context stream.  A: column- or row-major does not matter for eigenvalues (A and A^T share
+ * them); it is overwritten.  w: n complex values as (re, im) double pairs.  A and w are device
+ * pointers if ptr_on_device, else host (copied in / out; the call synchronises).
+ * Errors: SPH_EINVAL bad arguments; SPH_ECUDA solver failure (message in sph_last_error). */
+sph_status sph_eigenvalues(sph_ctx* ctx, int n, double* A, double* w, int ptr_on_device);
+
 /* Per-rollout counters (host arrays of B, nullable): substeps taken and cell-list / neighbour-
  * list rebuilds performed (with rebin_every = 0 rebuilds happen only when the displacement
  * bound requires them). */

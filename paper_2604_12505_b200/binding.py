@@ -73,6 +73,7 @@ def lib():
             "sph_get_live_timing": (i32, [vp, vp, vp, i32]),
             "sph_launches_per_substep": (i32, [vp]),
             "sph_jacobian": (i32, [vp, i32, vp, vp, i32]),
+            "sph_eigenvalues": (i32, [vp, i32, vp, vp, i32]),
             "sph_get_counters": (i32, [vp, vp, vp]),
             "sph_get_sizes": (None, [vp, vp, vp, vp, vp]),
             "sph_last_error": (C.c_char_p, [vp]),
@@ -91,7 +92,7 @@ def exported_symbols():
             "sph_get_particles", "sph_get_ghosts", "sph_step", "sph_rollout_batch",
             "sph_get_body_state", "sph_settle", "sph_get_status", "sph_debug_cells",
             "sph_debug_neighbours", "sph_profile_substeps", "sph_set_live_timing", "sph_get_live_timing",
-            "sph_launches_per_substep", "sph_get_counters", "sph_jacobian",
+            "sph_launches_per_substep", "sph_get_counters", "sph_jacobian", "sph_eigenvalues",
             "sph_get_sizes", "sph_last_error", "sph_destroy"]
 
 
@@ -327,6 +328,25 @@ class SphContext:
         self._check(self.L.sph_jacobian(self.ctx, int(rollout), A.ctypes.data, B.ctypes.data, 0),
                     "sph_jacobian")
         return A, B
+
+    def eigenvalues(self, A):
+        """Eigenvalues of a square float64 matrix (sph_eigenvalues, cuSOLVER Xgeev on the
+        context stream).  A: CUDA tensor (copied; the result stays on the device) or numpy."""
+        torch = self.torch
+        if hasattr(A, "is_cuda") and A.is_cuda:
+            n = int(A.shape[0])
+            work = self._dev_in(A.to(torch.float64).contiguous().clone())
+            w = torch.empty((n, 2), dtype=torch.float64, device=self.device)
+            self._check(self.L.sph_eigenvalues(self.ctx, n, work.data_ptr(), w.data_ptr(), 1),
+                        "sph_eigenvalues")
+            self._dev_out()
+            return torch.complex(w[:, 0], w[:, 1])
+        a = np.array(A, dtype=np.float64, order="C", copy=True)
+        n = a.shape[0]
+        w = np.empty((n, 2), np.float64)
+        self._check(self.L.sph_eigenvalues(self.ctx, n, a.ctypes.data, w.ctypes.data, 0),
+                    "sph_eigenvalues")
+        return w[:, 0] + 1j * w[:, 1]
 
     def counters(self):
         steps = np.zeros(self.B, np.int64)

@@ -11,7 +11,8 @@ OUT = os.path.join(HERE, "libsphb200.so")
 # -ftz=true: denormals never arise in the canonical predicates (coordinates ~1e-3..1 m;
 # squared separations below 1e-38 m^2 compare below (2h)^2 either way), see DESIGN.md.
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-ftz=true", "-gencode", "arch=compute_100a,code=sm_100a",
-              "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v",
+              "-lcusolver", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
 
 
 def nvcc():

@@ -2,6 +2,7 @@
 // Validation, workspace carve-up, launch sequencing, CUDA-graph capture of a slow tick,
 // canonical-order import/export and the parity/debug entry points.
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -51,6 +52,12 @@ struct sph_ctx {
     // linearization scratch (sph_jacobian), kept between calls
     void* jac_buf = nullptr;
     size_t jac_bytes = 0;
+    // dense eigensolver (sph_eigenvalues: cuSOLVER Xgeev, library call)
+    cusolverDnHandle_t solver = nullptr;
+    cusolverDnParams_t solver_params = nullptr;
+    void* eig_dbuf = nullptr;
+    size_t eig_dbytes = 0;
+    std::vector<char> eig_hbuf;
 };
 
 // event slots of one sampled substep
@@ -1036,6 +1043,56 @@ sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr
     return SPH_OK;
 }
 
+sph_status sph_eigenvalues(sph_ctx* ctx, int n, double* A, double* w, int ptr_on_device) {
+    if (!ctx || n < 1 || !A || !w) return SPH_EINVAL;
+    cudaStream_t s = ctx->stream;
+    if (!ctx->solver) {
+        if (cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS ||
+            cusolverDnCreateParams(&ctx->solver_params) != CUSOLVER_STATUS_SUCCESS)
+            return fail(ctx, SPH_ECUDA, "cuSOLVER handle creation failed");
+    }
+    cusolverDnSetStream(ctx->solver, s);
+    const size_t An = (size_t)n * n;
+    double* dA = A;
+    double2* dW = nullptr;
+    // scratch: [A copy if host] | W (complex) | device workspace
+    size_t dws = 0, hws = 0;
+    if (cusolverDnXgeev_bufferSize(ctx->solver, ctx->solver_params, CUSOLVER_EIG_MODE_NOVECTOR,
+                                   CUSOLVER_EIG_MODE_NOVECTOR, n, CUDA_R_64F, dA, n, CUDA_C_64F,
+                                   nullptr, CUDA_R_64F, nullptr, 1, CUDA_R_64F, nullptr, 1,
+                                   CUDA_R_64F, &dws, &hws) != CUSOLVER_STATUS_SUCCESS)
+        return fail(ctx, SPH_ECUDA, "cusolverDnXgeev_bufferSize failed");
+    const size_t oA = 0, oW = ptr_on_device ? 0 : ((8 * An + 255) & ~(size_t)255);
+    const size_t oWs = oW + ((16 * (size_t)n + 255) & ~(size_t)255), need = oWs + dws + 16;
+    if (ctx->eig_dbytes < need) {
+        CK(cudaStreamSynchronize(s));
+        if (ctx->eig_dbuf) cudaFree(ctx->eig_dbuf);
+        ctx->eig_dbuf = nullptr;
+        ctx->eig_dbytes = 0;
+        CK(cudaMalloc(&ctx->eig_dbuf, need));
+        ctx->eig_dbytes = need;
+    }
+    if (ctx->eig_hbuf.size() < hws + 16) ctx->eig_hbuf.resize(hws + 16);
+    char* base = (char*)ctx->eig_dbuf;
+    if (!ptr_on_device) {
+        dA = (double*)(base + oA);
+        CK(cudaMemcpyAsync(dA, A, 8 * An, cudaMemcpyHostToDevice, s));
+    }
+    dW = ptr_on_device ? (double2*)w : (double2*)(base + oW);
+    int* dinfo = (int*)(base + oWs + dws);
+    if (cusolverDnXgeev(ctx->solver, ctx->solver_params, CUSOLVER_EIG_MODE_NOVECTOR,
+                        CUSOLVER_EIG_MODE_NOVECTOR, n, CUDA_R_64F, dA, n, CUDA_C_64F, dW, CUDA_R_64F,
+                        nullptr, 1, CUDA_R_64F, nullptr, 1, CUDA_R_64F, base + oWs, dws,
+                        ctx->eig_hbuf.data(), hws, dinfo) != CUSOLVER_STATUS_SUCCESS)
+        return fail(ctx, SPH_ECUDA, "cusolverDnXgeev failed");
+    int info = 0;
+    CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (!ptr_on_device) CK(cudaMemcpyAsync(w, dW, 16 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (info != 0) return fail(ctx, SPH_ECUDA, "cusolverDnXgeev: info = " + std::to_string(info));
+    return SPH_OK;
+}
+
 sph_status sph_get_counters(sph_ctx* ctx, int64_t* steps, int32_t* rebuilds) {
     if (!ctx) return SPH_EINVAL;
     std::vector<RolloutState> rs(ctx->P.B);
@@ -1069,6 +1126,9 @@ void sph_destroy(sph_ctx* ctx) {
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     for (auto e : ctx->live_ev) cudaEventDestroy(e);
     if (ctx->jac_buf) cudaFree(ctx->jac_buf);
+    if (ctx->eig_dbuf) cudaFree(ctx->eig_dbuf);
+    if (ctx->solver_params) cusolverDnDestroyParams(ctx->solver_params);
+    if (ctx->solver) cusolverDnDestroy(ctx->solver);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -136,3 +136,24 @@ def test_eigen_trace_spectra():
     assert np.abs(ev_g.real.max() - ev_o.real.max()) <= 1e-4 * np.abs(ev_o).max()
     assert np.abs(np.abs(ev_g).max() - np.abs(ev_o).max()) <= 1e-6 * np.abs(ev_o).max()
     ctx.close()
+
+
+def test_eigenvalues_library_solver():
+    """sph_eigenvalues (cuSOLVER Xgeev): SPEC linearization examples (zero matrix -> 0,
+    companion of xdd = -x -> +-i) and a random matrix against LAPACK (numpy)."""
+    import torch
+    t = si.make_tank(1.0)
+    ctx = _ctx(t)
+    assert np.allclose(ctx.eigenvalues(np.zeros((4, 4))), 0.0)
+    ev = np.sort_complex(ctx.eigenvalues(np.array([[0.0, 1.0], [-1.0, 0.0]])))
+    assert np.allclose(ev, [-1j, 1j], atol=1e-14)
+    rng = np.random.Generator(np.random.Philox(7))
+    M = rng.normal(size=(300, 300))
+    ev = ctx.eigenvalues(M)
+    ref = np.linalg.eigvals(M)
+    # match each LAPACK eigenvalue to its nearest GPU eigenvalue
+    d = np.abs(ref[:, None] - ev[None, :]).min(1)
+    assert d.max() <= 1e-10 * np.abs(ref).max()
+    evd = ctx.eigenvalues(torch.from_numpy(M).cuda())
+    assert evd.is_cuda and np.allclose(np.sort_complex(evd.cpu().numpy()), np.sort_complex(ev), atol=1e-12)
+    ctx.close()
