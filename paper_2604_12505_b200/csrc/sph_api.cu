@@ -175,6 +175,12 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
         P->td = pick("SPH_DTILE", 128);
         P->tf = pick("SPH_FTILE", 64);
         P->tn = pick("SPH_NTILE", 128);
+        // L2 prefetch distance: SPH_PF waves ahead (a wave = 148 SMs x resident CTAs per SM at
+        // 48 (force) / 64 (density) warps per SM); 0 disables
+        const char* e = std::getenv("SPH_PF");
+        const double waves = e ? std::atof(e) : 1.5;   // sweep: 0.5 16.7, 1 17.1, 2 17.2, 4 16.8 G/s
+        P->pf_f = (int)(waves * 148 * (48 / (P->tf / 32)));
+        P->pf_d = (int)(waves * 148 * (64 / (P->td / 32)));
     }
     // ghost-ring window (see for_ghost_candidates): only particles farther than d_min from the
     // centre can have a ghost within 2h; their ghosts lie within +-dphi of their polar angle.

@@ -59,6 +59,7 @@ struct DevParams {
     int nblk, chunk, nchunk;// ring kernels: super-tiles of SW_T slots per rollout, super-tiles
                             // per CTA, CTAs per rollout
     int td, tf, tn;         // slots (threads) per CTA of k_density / k_force / k_nlist_density
+    int pf_d, pf_f;         // L2 prefetch distance in CTAs (k_density / k_force; 0 = off)
     double dtd, m_body, J_body;
 };
 

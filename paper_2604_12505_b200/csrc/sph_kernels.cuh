@@ -329,6 +329,35 @@ __device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D,
     });
 }
 
+// L2 prefetch ahead of the wave: thread 0 of a CTA bulk-prefetches (cp.async.bulk.prefetch.L2)
+// the inputs of the tile `dist` CTAs later in launch order (same grid shape) -- the tile a CTA
+// starting about one wave later will process -- so its list rows, counts and state come from L2
+// instead of DRAM.  Issued after the thread's own work; 1x traffic (each tile once).
+template <bool FORCE>
+__device__ __forceinline__ void prefetch_ahead(const DevParams& P, const DevPtrs& D, int T, int dist) {
+    if (threadIdx.x != 0 || dist <= 0) return;
+    const long long c = (long long)blockIdx.y * gridDim.x + blockIdx.x + dist;
+    if (c >= (long long)gridDim.x * gridDim.y) return;
+    const int b = (int)(c / gridDim.x), t0 = (int)(c % gridDim.x) * T;
+    const int cnt = min(T, P.N - t0);
+    if (cnt <= 0) return;
+    const size_t o = (size_t)b * P.N;
+    auto pf = [](const void* p, size_t bytes) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+        const uintptr_t lo = a & ~(uintptr_t)15, hi = (a + bytes + 15) & ~(uintptr_t)15;
+        bulk_prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
+    };
+    for (int q = 0; q < 3; ++q)   // lists of up to 12 entries (p90 of C2: 11)
+        pf(D.nbr + (size_t)b * KQ * P.N + (size_t)q * P.N + t0, (size_t)cnt * 8);
+    pf(D.ncnt + o + t0, (size_t)cnt);
+    const RolloutState* rs = D.rs + b;
+    pf(D.pv[rs->sp ^ rs->need_rebin] + o + t0, (size_t)cnt * 16);
+    if (FORCE) {
+        pf(D.aux + (size_t)b * P.NA + t0, (size_t)cnt * 8);
+        pf(D.xb + o + t0, (size_t)cnt * 8);
+    }
+}
+
 // skip_rebuilding = 1 when rollouts that rebuild this substep get their densities from
 // k_nlist_density (which runs concurrently on another branch of the graph).
 // Plain variant: neighbour positions gathered from global memory through L1.
@@ -342,6 +371,7 @@ __global__ void __launch_bounds__(TD) k_density(DevParams P, DevPtrs D, int skip
     const int i = blockIdx.x * TD + threadIdx.x;
     const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
     if (i < P.N) density_at<true>(P, D, b, i, pv);
+    prefetch_ahead<false>(P, D, TD, P.pf_d);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -978,6 +1008,7 @@ __global__ void __launch_bounds__(TF, SPH_FORCE_MINB * TILE / TF) k_force(DevPar
     const int b = blockIdx.y;
     if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
     force_tile<TF>(P, D, damping, b, blockIdx.x);
+    prefetch_ahead<true>(P, D, TF, P.pf_f);
 }
 
 // Ring variant: CTA (x, y) walks super-tiles [x chunk, (x + 1) chunk) of rollout y (modes 0/1)
