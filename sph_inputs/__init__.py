@@ -175,11 +175,11 @@ def make_tank(ell: float = 1.0, fill: float | None = 0.5, n_first: int | None = 
 
 
 def moving_tank(ell: float = 1.0, seed: int = 1, jitter: float = 0.05, vel: float = 0.01,
-                body=None) -> Tank:
+                body=None, **over) -> Tank:
     """Jittered lattice with random velocities (an unsettled, fully active state: one-step and
     linearization parity), rigidly placed at the body pose ``body`` = (r_x, r_y, th, rd_x,
     rd_y, thd) when given; snapped to float32-representable values."""
-    t = make_tank(ell, jitter=jitter, seed=seed)
+    t = make_tank(ell, jitter=jitter, seed=seed, **over)
     t.vel = np.random.Generator(np.random.Philox(seed + 100)).normal(0, vel, t.pos.shape)
     if body is not None:
         th = body[2]

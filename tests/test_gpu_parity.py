@@ -442,3 +442,28 @@ def test_damped_settle_statistics_match_oracle(path, skin):
     assert abs(vg - vo) < 0.05 * vo, (vg, vo)
     assert abs(rho.min() - rho_ref.min()) < 1e-4 * sp.rho0
     assert abs(rho.max() - rho_ref.max()) < 1e-4 * sp.rho0
+
+
+@pytest.mark.parametrize("over", [dict(w_cb_const=si.W_CB_CONST_PRINTED),
+                                  dict(ghost_pressure_sign=1.0),
+                                  dict(gy=-0.05)],
+                         ids=["printed_cubic_constant", "literal_wall_pressure_sign", "gravity"])
+def test_reading_switches_one_step_parity(over):
+    """The readings' switches (A1 printed constant, A4 literal sign, external acceleration) take
+    the same path on both sides: one-step parity at 1e-5 on a moving, rotated C1 tank."""
+    t = si.moving_tank(1.0, seed=2, vel=0.02, body=[0.02, -0.01, 0.3, 0.01, 0.0, 0.03], **over)
+    ctx = _ctx(t)
+    ctx.set_body_state(np.array([t.body]))
+    u = (5.0, 2.0, 1.0)
+    ctx.step(np.array([u], np.float32), 1)
+    pv, rho = ctx.get_particles(0, with_rho=True)
+    ref = O.State.from_tank(t)
+    rho_ref = ref.step(u, want_rho=True)
+    sp = t.params
+    assert _rel(pv[:, :2], ref.pos) <= 1e-5
+    assert _rel(pv[:, 2:], ref.vel, sp.dt * sp.k / sp.h) <= 1e-5
+    assert _rel(rho, rho_ref) <= 1e-5
+    bg = ctx.get_body_state()[0]
+    for sl in (slice(0, 2), slice(2, 3), slice(3, 5), slice(5, 6)):
+        assert _rel(bg[sl], ref.body[sl], 1e-12) <= 1e-5
+    ctx.close()
