@@ -122,6 +122,7 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->half = (float)half_cells * P->C;
     P->ntile = std::max(1, (N + TILE - 1) / TILE);
     P->npart = P->ntile * (TILE / 32);
+    P->bsplit = P->npart > 8192 ? (P->npart + 511) / 512 : 1;
     P->nscan = (P->ncell + 1 + SCAN_TILE - 1) / SCAN_TILE;
     if ((P->nscan + SCAN_T - 1) / SCAN_T > SCAN_V) return *why = "cell grid too large for the scan", false;
     P->h = (float)h;
@@ -236,6 +237,7 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     put(d.body, (size_t)P.B * 48);
     put(d.u_cur, (size_t)P.B * 12);
     put(d.part, (size_t)P.B * P.npart * 32);
+    put(d.part2, (size_t)P.B * P.bsplit * 32);
     put(d.rs, (size_t)P.B * sizeof(RolloutState));
     put(d.geom, (size_t)P.B * sizeof(Geom));
     put(d.xfer, (size_t)std::max(P.N, 1) * 16);
@@ -283,6 +285,7 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
 }
 
 static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0) {
+    if (ctx->P.bsplit > 1) k_body_reduce<<<dim3(ctx->P.bsplit, ctx->P.B), BRED_T, 0, s>>>(ctx->P, ctx->D);
     k_body<<<ctx->P.B, ctx->body_threads, (size_t)ctx->body_threads * sizeof(double4), s>>>(
         ctx->P, ctx->D, pin, ghost_angle0);
 }
@@ -439,7 +442,9 @@ static int live_samples(const sph_ctx* ctx) {
 
 // kernels per substep: small path 5 (plan, rebuild_small, density, force, body); multi-kernel
 // path 4 + 8 rebuild kernels (the 8 run only in substeps where some rollout rebuilds).
-static int launches_per_substep(const sph_ctx* ctx) { return ctx->small ? (ctx->fork ? 7 : 6) : 12; }
+static int launches_per_substep(const sph_ctx* ctx) {
+    return (ctx->small ? (ctx->fork ? 7 : 6) : 12) + (ctx->P.bsplit > 1 ? 1 : 0);
+}
 
 static sph_status check_launch(sph_ctx* ctx) {
     cudaError_t e = cudaGetLastError();

@@ -59,6 +59,9 @@ struct DevParams {
     int nblk, chunk, nchunk;// ring kernels: super-tiles of SW_T slots per rollout, super-tiles
                             // per CTA, CTAs per rollout
     int td, tf, tn;         // slots (threads) per CTA of k_density / k_force / k_nlist_density
+    int bsplit;             // body reduction: 1 = k_body sums the npart partials itself;
+                            // > 1 = k_body_reduce first sums bsplit fixed chunks (large tanks;
+                            // chosen from N only, so bits never depend on B)
     int pf_d, pf_f;         // L2 prefetch distance in CTAs (k_density / k_force; 0 = off)
     double dtd, m_body, J_body;
 };
@@ -109,6 +112,7 @@ struct DevPtrs {
     double* body;        // [B][6] r_x r_y theta rd_x rd_y thd
     float* u_cur;        // [B][3] current ZOH input
     double4* part;       // [B][npart] per-warp (F_x, F_y, T, max relative speed) partials
+    double4* part2;      // [B][bsplit] chunk sums of part (bsplit > 1)
     RolloutState* rs;    // [B]
     Geom* geom;          // [B]
     float4* xfer;        // [N] canonical-order export / import staging

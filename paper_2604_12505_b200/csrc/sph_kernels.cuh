@@ -1089,6 +1089,35 @@ __device__ __forceinline__ void ghost_update(const DevParams& P, const DevPtrs& 
     }
 }
 
+// First stage of the body reduction of large tanks: CTA (s, b) sums the fixed chunk s of rollout
+// b's per-warp partials (thread-strided, then a fixed-order tree) into part2[b][s].
+constexpr int BRED_T = 256;
+__global__ void __launch_bounds__(BRED_T) k_body_reduce(DevParams P, DevPtrs D) {
+    __shared__ double4 red[BRED_T];
+    const int b = blockIdx.y, sidx = blockIdx.x;
+    if (D.rs[b].frozen) return;   // CTA-uniform
+    const int chunk = (P.npart + P.bsplit - 1) / P.bsplit;
+    const int t0 = sidx * chunk, t1 = min(t0 + chunk, P.npart);
+    double4 s = make_double4(0, 0, 0, 0);
+    for (int t = t0 + threadIdx.x; t < t1; t += BRED_T) {
+        const double4 q = D.part[(size_t)b * P.npart + t];
+        s.x += q.x;
+        s.y += q.y;
+        s.z += q.z;
+        s.w = fmax(s.w, q.w);
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = BRED_T / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            const double4 a = red[threadIdx.x], c = red[threadIdx.x + w];
+            red[threadIdx.x] = make_double4(a.x + c.x, a.y + c.y, a.z + c.z, fmax(a.w, c.w));
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) D.part2[(size_t)b * P.bsplit + sidx] = red[0];
+}
+
 // ---------------------------------------------------------------------------------------
 // Body: fixed-order fp64 reduction of the CTA partials, Eq. tankdynamics
 //   m rddot = -sum G + (u_x, u_y),  J thddot = sum (r_g - r) x (-G) + tau,
@@ -1108,8 +1137,10 @@ __global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
     __syncthreads();
     if (sdead) return;
     double4 s = make_double4(0, 0, 0, 0);
-    for (int t = threadIdx.x; t < P.npart; t += nt) {
-        const double4 q = D.part[(size_t)b * P.npart + t];
+    const int np = P.bsplit > 1 ? P.bsplit : P.npart;
+    const double4* part = P.bsplit > 1 ? D.part2 + (size_t)b * P.bsplit : D.part + (size_t)b * P.npart;
+    for (int t = threadIdx.x; t < np; t += nt) {
+        const double4 q = part[t];
         s.x += q.x;
         s.y += q.y;
         s.z += q.z;
