@@ -370,7 +370,7 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
     dim3 gp(P.ntile, P.B);
     if (ctx->small && !ctx->fork) {   // serial: sort + lists/densities of the rebuilt rollouts first
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
-        k_rebuild_small<false><<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
+        k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
         launch_nlist_density(ctx, s);
         live_mark(ev, LV_DEN0, s);
         launch_density(ctx, s, 1);
@@ -381,7 +381,7 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
         cudaEventRecord(ctx->ev_fork, s);
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
-        k_rebuild_small<false><<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
+        k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
         launch_nlist_density(ctx, ctx->side);
         cudaEventRecord(ctx->ev_join, ctx->side);
         live_mark(ev, LV_DEN0, s);
@@ -565,7 +565,7 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             sph_destroy(ctx);
             return fail(nullptr, SPH_EINVAL, "rebuild_path = 1 but the rollout does not fit in shared memory");
         }
-        if (want && cudaFuncSetAttribute(k_rebuild_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (want && cudaFuncSetAttribute(k_rebuild_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem) != cudaSuccess) {
             cudaGetLastError();
             want = false;
@@ -583,6 +583,10 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             return bail("side stream", e);
         // k_body: enough threads to reduce the per-warp partials of big tanks (N only)
         while (ctx->body_threads < 1024 && ctx->body_threads * 4 < P.npart) ctx->body_threads *= 2;
+        if (const char* bt = std::getenv("SPH_BODY_T")) {   // sweep override (power of two)
+            const int v = std::atoi(bt);
+            if (v >= 32 && v <= 1024 && (v & (v - 1)) == 0) ctx->body_threads = v;
+        }
     }
     if ((e = cudaMemsetAsync(d_workspace, 0, total, s)) != cudaSuccess) return bail("memset", e);
     std::vector<double2> gb(std::max(n_ghost, 1));
@@ -915,7 +919,7 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
     for (int it = 0; it < n_substeps; ++it) {
         cudaEventRecord(ev[0], s);
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
-        if (ctx->small) k_rebuild_small<false><<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
+        if (ctx->small) k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
         else launch_rebin(ctx);
         launch_nlist_density(ctx, s);   // (runs after k_density in the step; same work)
         cudaEventRecord(ev[1], s);

@@ -631,12 +631,8 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
 }
 
 // dynamic shared memory: start[ncell + 1] u32 | key[N] u32 | perm[N] u32 | rank[N] u16
-// After the gather, key|perm (8N bytes) is reused for the rollout's positions (float2[N]) and
-// rank for each slot's cell (u16; host guarantees ncell < 65536), so list building and the
-// densities read positions from shared memory.
-// LISTS = false: sort only (production path: lists + densities then run grid-wide in
-// k_nlist_density); LISTS = true: the whole rebuild + densities in this CTA.
-template <bool LISTS>
+// (host guarantees N < 65536).  Sort only: the lists and the densities of the rebuilt rollouts
+// follow grid-wide in k_nlist_density.
 __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) {
     extern __shared__ uint32_t smem[];
     __shared__ uint32_t wt[RB_T / 32];
@@ -644,8 +640,6 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
     uint32_t* s_key = s_start + ((P.ncell + 1 + 3) & ~3);   // 16-byte aligned (float2 alias)
     uint32_t* s_perm = s_key + P.N;
     uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_perm + P.N);
-    float2* s_pos = reinterpret_cast<float2*>(s_key);   // aliases key|perm after the gather
-    uint16_t* s_cell = s_rank;                           // aliases rank after the scatter
     const int count = *D.rcount;
     const int T = RB_T, tid = threadIdx.x;
     for (int w = blockIdx.x; w < count; w += gridDim.x) {
@@ -712,7 +706,7 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
             }
         }
         __syncthreads();
-        // 5. gather into cell order (slot cells kept as u16 in the rank area)
+        // 5. gather into cell order
         for (int d = tid; d < P.N; d += T) {
             const uint32_t src = s_perm[d];
             const float4 v = pv0[src];
@@ -721,48 +715,21 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
             const uint32_t c = s_key[src];
             D.skey[o + d] = c;
             D.xb[o + d] = make_float2(v.x, v.y);   // positions at this rebuild (Verlet)
-            s_cell[d] = (uint16_t)c;
         }
         __syncthreads();
-        if constexpr (!LISTS) {      // lists + densities follow in k_nlist_density (grid-wide)
-            if (tid == 0) {
-                rs->span = 0;
-                rs->rbx = gm.rx;     // body position at this rebuild (Verlet criterion)
-                rs->rby = gm.ry;
-            }
-            __syncthreads();
-            continue;
-        }
-        // positions of the new order into shared memory (key|perm are dead now)
-        for (int d = tid; d < P.N; d += T) {
-            const float4 v = pv1[d];
-            s_pos[d] = make_float2(v.x, v.y);
-        }
-        __syncthreads();
-        // 6. neighbour lists (cell starts and positions from shared memory)
-        int span = 0;
-        for (int i = tid; i < P.N; i += T)
-            span = max(span, build_list_core(P, D, b, i, s_start, (uint32_t)s_cell[i],
-                                             [&](uint32_t j) { return s_pos[j]; }));
-        span = __reduce_max_sync(0xffffffffu, span);
-        if ((tid & 31) == 0) wt[tid >> 5] = (uint32_t)span;
-        __syncthreads();
+        // lists + densities follow in k_nlist_density (grid-wide)
         if (tid == 0) {
-            uint32_t m = 0;
-            for (int q = 0; q < RB_T / 32; ++q) m = max(m, wt[q]);
-            rs->span = (int)m;
+            rs->span = 0;
+            rs->rbx = gm.rx;     // body position at this rebuild (Verlet criterion)
+            rs->rby = gm.ry;
         }
-        __syncthreads();
-        // 7. densities of the rebuilt rollout (lists just written: coherent loads)
-        for (int i = tid; i < P.N; i += T)
-            density_core<false>(P, D, b, i, [&](uint32_t j) { return s_pos[j]; });
         __syncthreads();
     }
 }
 
 // Neighbour lists + densities of the rollouts in the rebuild work list, grid-wide:
 // grid = (tiles, Y); CTA (x, y) handles tile x of work items y, y + Y, ...  The cell table,
-// slot cells and sorted state come from the sort (k_rebuild_small<false> or the grid-wide
+// slot cells and sorted state come from the sort (k_rebuild_small or the grid-wide
 // rebuild kernels); the list just written by a thread is read back by the same thread.
 template <int TN>
 __global__ void __launch_bounds__(TN) k_nlist_density(DevParams P, DevPtrs D) {
