@@ -43,6 +43,7 @@ struct sph_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool fork = true;   // small path: rebuild branch concurrent with density/forces (SPH_FORK=0: serial)
+    bool pdl = true;    // programmatic dependent launch on the substep chain (SPH_PDL=0: off)
     // live kernel timing inside the tick graph (sph_set_live_timing): event-record nodes around
     // the density / force launches of every live_every-th substep, read after each tick
     int live_every = 0;
@@ -82,6 +83,29 @@ static sph_status fail(sph_ctx* ctx, sph_status s, const std::string& m) {
     if (ctx) ctx->err = m;
     else g_init_err = m;
     return s;
+}
+
+// Kernel launch, optionally with programmatic dependent launch (PDL): the kernel may start
+// launching while its in-stream predecessor still runs; it waits (griddepcontrol.wait) before
+// touching the predecessor's results.
+template <typename... KArgs, typename... Args>
+static void launch_k(bool pdl, void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s,
+                     Args... args) {
+    if (!pdl) {
+        kern<<<g, b, smem, s>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -253,41 +277,47 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
 // ---------------------------------------------------------------------------------------
 // Launch sequencing
 // ---------------------------------------------------------------------------------------
-static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding) {
+static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding, bool pdl = false) {
+    pdl = pdl && ctx->pdl;
     const DevParams& P = ctx->P;
     dim3 gp(P.ntile, P.B);
     if (P.ring)
         k_density_ring<<<dim3(P.nchunk, P.B), SW_T, kDensityRingSmem, s>>>(P, ctx->D, skip_rebuilding);
     else
         switch (P.td) {
-            case 1024: k_density<1024><<<dim3(std::max(1, (P.N + 1023) / 1024), P.B), 1024, 0, s>>>(P, ctx->D, skip_rebuilding); break;
-            case 512: k_density<512><<<dim3(std::max(1, (P.N + 511) / 512), P.B), 512, 0, s>>>(P, ctx->D, skip_rebuilding); break;
-            case 128: k_density<128><<<dim3(std::max(1, (P.N + 127) / 128), P.B), 128, 0, s>>>(P, ctx->D, skip_rebuilding); break;
-            case 64: k_density<64><<<dim3(std::max(1, (P.N + 63) / 64), P.B), 64, 0, s>>>(P, ctx->D, skip_rebuilding); break;
-            default: k_density<256><<<dim3(std::max(1, (P.N + 255) / 256), P.B), 256, 0, s>>>(P, ctx->D, skip_rebuilding); break;
+            case 1024: launch_k(pdl, k_density<1024>, dim3(std::max(1, (P.N + 1023) / 1024), P.B), dim3(1024), 0, s, P, ctx->D, skip_rebuilding); break;
+            case 512: launch_k(pdl, k_density<512>, dim3(std::max(1, (P.N + 511) / 512), P.B), dim3(512), 0, s, P, ctx->D, skip_rebuilding); break;
+            case 128: launch_k(pdl, k_density<128>, dim3(std::max(1, (P.N + 127) / 128), P.B), dim3(128), 0, s, P, ctx->D, skip_rebuilding); break;
+            case 64: launch_k(pdl, k_density<64>, dim3(std::max(1, (P.N + 63) / 64), P.B), dim3(64), 0, s, P, ctx->D, skip_rebuilding); break;
+            default: launch_k(pdl, k_density<256>, dim3(std::max(1, (P.N + 255) / 256), P.B), dim3(256), 0, s, P, ctx->D, skip_rebuilding); break;
         }
 }
 
 // mode: 0 all rollouts, 1 non-rebuilding rollouts, 2 rebuilt rollouts (work list)
-static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode = 0) {
+static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode = 0, bool pdl = false) {
+    pdl = pdl && ctx->pdl;
     const DevParams& P = ctx->P;
     const int gy = mode == 2 ? std::min(P.B, 64) : P.B;
     if (P.ring)
         k_force_ring<<<dim3(P.nchunk, gy), SW_T, kForceRingSmem, s>>>(P, ctx->D, damping, mode);
     else
         switch (P.tf) {
-            case 1024: k_force<1024><<<dim3(std::max(1, (P.N + 1023) / 1024), gy), 1024, 0, s>>>(P, ctx->D, damping, mode); break;
-            case 512: k_force<512><<<dim3(std::max(1, (P.N + 511) / 512), gy), 512, 0, s>>>(P, ctx->D, damping, mode); break;
-            case 128: k_force<128><<<dim3(std::max(1, (P.N + 127) / 128), gy), 128, 0, s>>>(P, ctx->D, damping, mode); break;
-            case 64: k_force<64><<<dim3(std::max(1, (P.N + 63) / 64), gy), 64, 0, s>>>(P, ctx->D, damping, mode); break;
-            default: k_force<256><<<dim3(std::max(1, (P.N + 255) / 256), gy), 256, 0, s>>>(P, ctx->D, damping, mode); break;
+            case 1024: launch_k(pdl, k_force<1024>, dim3(std::max(1, (P.N + 1023) / 1024), gy), dim3(1024), 0, s, P, ctx->D, damping, mode); break;
+            case 512: launch_k(pdl, k_force<512>, dim3(std::max(1, (P.N + 511) / 512), gy), dim3(512), 0, s, P, ctx->D, damping, mode); break;
+            case 128: launch_k(pdl, k_force<128>, dim3(std::max(1, (P.N + 127) / 128), gy), dim3(128), 0, s, P, ctx->D, damping, mode); break;
+            case 64: launch_k(pdl, k_force<64>, dim3(std::max(1, (P.N + 63) / 64), gy), dim3(64), 0, s, P, ctx->D, damping, mode); break;
+            default: launch_k(pdl, k_force<256>, dim3(std::max(1, (P.N + 255) / 256), gy), dim3(256), 0, s, P, ctx->D, damping, mode); break;
         }
 }
 
-static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0) {
-    if (ctx->P.bsplit > 1) k_body_reduce<<<dim3(ctx->P.bsplit, ctx->P.B), BRED_T, 0, s>>>(ctx->P, ctx->D);
-    k_body<<<ctx->P.B, ctx->body_threads, (size_t)ctx->body_threads * sizeof(double4), s>>>(
-        ctx->P, ctx->D, pin, ghost_angle0);
+static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0, bool pdl = false) {
+    pdl = pdl && ctx->pdl;
+    if (ctx->P.bsplit > 1) {
+        k_body_reduce<<<dim3(ctx->P.bsplit, ctx->P.B), BRED_T, 0, s>>>(ctx->P, ctx->D);
+        pdl = false;
+    }
+    launch_k(pdl, k_body, dim3(ctx->P.B), dim3(ctx->body_threads), (size_t)ctx->body_threads * sizeof(double4),
+             s, ctx->P, ctx->D, pin, ghost_angle0);
 }
 
 // Grid-wide counting sort by cell of every rollout with need_rebin (7 kernels); with_nlist adds
@@ -307,13 +337,14 @@ static void launch_rebin(sph_ctx* ctx, cudaStream_t s = nullptr, bool with_nlist
 }
 
 // lists + densities of the rebuilt rollouts (work list), spread over the whole GPU
-static void launch_nlist_density(sph_ctx* ctx, cudaStream_t s) {
+static void launch_nlist_density(sph_ctx* ctx, cudaStream_t s, bool pdl = false) {
     const DevParams& P = ctx->P;
     const int gy = std::min(P.B, 64);
+    pdl = pdl && ctx->pdl;
     switch (P.tn) {
-        case 256: k_nlist_density<256><<<dim3(std::max(1, (P.N + 255) / 256), gy), 256, 0, s>>>(P, ctx->D); break;
-        case 64: k_nlist_density<64><<<dim3(std::max(1, (P.N + 63) / 64), gy), 64, 0, s>>>(P, ctx->D); break;
-        default: k_nlist_density<128><<<dim3(std::max(1, (P.N + 127) / 128), gy), 128, 0, s>>>(P, ctx->D); break;
+        case 256: launch_k(pdl, k_nlist_density<256>, dim3(std::max(1, (P.N + 255) / 256), gy), dim3(256), 0, s, P, ctx->D); break;
+        case 64: launch_k(pdl, k_nlist_density<64>, dim3(std::max(1, (P.N + 63) / 64), gy), dim3(64), 0, s, P, ctx->D); break;
+        default: launch_k(pdl, k_nlist_density<128>, dim3(std::max(1, (P.N + 127) / 128), gy), dim3(128), 0, s, P, ctx->D); break;
     }
 }
 
@@ -364,10 +395,14 @@ static void live_mark(cudaEvent_t* ev, int slot, cudaStream_t s) {
     if (ev) cudaEventRecordWithFlags(ev[slot], s, cudaEventRecordExternal);
 }
 
-static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cudaEvent_t* ev) {
+// first: the substep's first kernel has an in-stream kernel predecessor (PDL allowed); timing
+// nodes (ev) between kernels disable PDL for the kernels after them.
+static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cudaEvent_t* ev,
+                                              bool first_pdl) {
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
     dim3 gp(P.ntile, P.B);
+    const bool np = ev == nullptr;   // no timing nodes in this substep
     if (ctx->small && !ctx->fork) {   // serial: sort + lists/densities of the rebuilt rollouts first
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
         k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
@@ -378,14 +413,15 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
         return cudaSuccess;
     }
     if (ctx->small) {   // (forces are launched by launch_substep, see there)
-        k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
+        launch_k(first_pdl && np && ctx->pdl, k_rebuild_plan, dim3(1), dim3(RB_T), 0, s, P, ctx->D,
+                 (cudaGraphConditionalHandle)0, 0);
         cudaEventRecord(ctx->ev_fork, s);
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
         k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
-        launch_nlist_density(ctx, ctx->side);
+        launch_nlist_density(ctx, ctx->side, true);
         cudaEventRecord(ctx->ev_join, ctx->side);
         live_mark(ev, LV_DEN0, s);
-        launch_density(ctx, s, 1);
+        launch_density(ctx, s, 1, np);
         live_mark(ev, LV_DEN1, s);
         return cudaSuccess;
     } else {
@@ -397,10 +433,10 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
             launch_rebin(ctx);
         }
         live_mark(ev, LV_DEN0, s);
-        launch_density(ctx, s, 1);
+        launch_density(ctx, s, 1, false);   // (follows the IF node / the rebuild kernels)
         live_mark(ev, LV_DEN1, s);
     }
-    launch_nlist_density(ctx, s);
+    launch_nlist_density(ctx, s, np);
     return cudaSuccess;
 }
 
@@ -414,24 +450,27 @@ static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool cap
     if (capturing && ctx->live_every > 0 && k >= 0 && k % ctx->live_every == 0)
         ev = ctx->live_ev.data() + (size_t)(k / ctx->live_every) * LIVE_SLOTS;
     live_mark(ev, LV_SUB0, s);
-    cudaError_t e = launch_rebuild_and_density(ctx, capturing, ev);
+    const bool np = ev == nullptr;
+    // PDL on the first kernel only when an in-stream kernel precedes it (not the first substep
+    // of a captured graph)
+    cudaError_t e = launch_rebuild_and_density(ctx, capturing, ev, !(capturing && k == 0));
     if (ctx->small && ctx->fork) {
         // The rebuild branch (sort -> lists + densities of the rebuilt rollouts) runs on the side
         // stream concurrently with density AND forces of every other rollout; only the forces
         // of the rebuilt rollouts wait for it.
         live_mark(ev, LV_F1_0, s);
-        launch_force(ctx, s, damping, 1);
+        launch_force(ctx, s, damping, 1, np);
         live_mark(ev, LV_F1_1, s);
         cudaStreamWaitEvent(s, ctx->ev_join, 0);
         live_mark(ev, LV_F2_0, s);
-        launch_force(ctx, s, damping, 2);
+        launch_force(ctx, s, damping, 2, false);
         live_mark(ev, LV_F2_1, s);
     } else {
         live_mark(ev, LV_F1_0, s);
-        launch_force(ctx, s, damping, 0);
+        launch_force(ctx, s, damping, 0, np);
         live_mark(ev, LV_F1_1, s);
     }
-    launch_body(ctx, s, pin, ctx->ghost_angle0);
+    launch_body(ctx, s, pin, ctx->ghost_angle0, np);
     live_mark(ev, LV_SUB1, s);
     return e;
 }
@@ -520,6 +559,12 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
     ctx->P = P;
     ctx->fp = *fp;
     ctx->bp = *bp;
+    {   // PDL pays for latency-bound small batches (C1 / C2 single tank +4 %); at C3 it is
+        // neutral to -1 %, so it is on below the per-rollout rebuild threshold only.
+        // SPH_PDL=0/1 forces it.
+        const char* e = std::getenv("SPH_PDL");
+        ctx->pdl = e ? (e[0] == '1') : (P.B < kSmallMinBatch);
+    }
     ctx->n_sub = tp->substeps_per_sample;
     ctx->ghost_angle0 = (float)a0;
     carve(P, (char*)d_workspace, &ctx->D);

@@ -153,6 +153,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// Programmatic dependent launch (the substep chain on the main stream): a kernel waits for its
+// predecessor's completion (and memory) before reading anything it produced, and lets its own
+// dependents start launching right away, so kernel launch and prologue overlap the tail of the
+// previous kernel.  Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 // L2 prefetch of a global range (address and size multiples of 16)
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");

@@ -365,6 +365,8 @@ __device__ __forceinline__ void prefetch_ahead(const DevParams& P, const DevPtrs
 // window lines per own slot (fewer compulsory L1 misses); TD is chosen on the host.
 template <int TD>
 __global__ void __launch_bounds__(TD) k_density(DevParams P, DevPtrs D, int skip_rebuilding) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.y;
     const RolloutState* rs = D.rs + b;
     if (rs->frozen || (skip_rebuilding && rs->need_rebin)) return;   // CTA-uniform
@@ -531,6 +533,8 @@ __device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t v, uint32_t* tota
 __global__ void __launch_bounds__(RB_T) k_rebuild_plan(DevParams P, DevPtrs D,
                                                        cudaGraphConditionalHandle cond,
                                                        int set_cond) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ uint32_t wt[RB_T / 32];
     uint32_t base = 0;
     for (int b0 = 0; b0 < P.B; b0 += RB_T) {
@@ -733,6 +737,8 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
 // rebuild kernels); the list just written by a thread is read back by the same thread.
 template <int TN>
 __global__ void __launch_bounds__(TN) k_nlist_density(DevParams P, DevPtrs D) {
+    pdl_wait();
+    pdl_trigger();
     const int count = *D.rcount;
     const int i = blockIdx.x * TN + threadIdx.x;
     for (int w = blockIdx.y; w < count; w += gridDim.y) {
@@ -966,6 +972,8 @@ __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D,
 template <int TF>
 __global__ void __launch_bounds__(TF, SPH_FORCE_MINB * TILE / TF) k_force(DevParams P, DevPtrs D,
                                                                           float damping, int mode) {
+    pdl_wait();
+    pdl_trigger();
     if (mode == 2) {
         const int count = *D.rcount;
         for (int w = blockIdx.y; w < count; w += gridDim.y)
@@ -1094,6 +1102,8 @@ __global__ void __launch_bounds__(BRED_T) k_body_reduce(DevParams P, DevPtrs D) 
 // the bits, never depend on the batch size).
 __global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
                                                float ghost_angle0) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.x;
     const int nt = blockDim.x;
     RolloutState* rs = D.rs + b;
