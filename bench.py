@@ -387,7 +387,8 @@ def run_ours(a):
             "kernel_share_of_substep": kms / live["substep"] if live["samples"] else kms / prof["substep"],
             "live_ms": {k: live[k] for k in ("density", "force", "substep")},
             "isolated_ms": kern, "substep_ms_isolated": prof["substep"]}
-    launches = a.steps * (1 + sp.n_sub * ctx.launches_per_substep())
+    lps = ctx.launches_per_substep()
+    launches = a.steps * (1 + (sp.n_sub * lps if lps > 0 else 1))   # 0: one cooperative launch per tick
     ctx.close()
     del ctx
     # ---- e2e: the same ticks through the public API with HOST buffers ----------------------

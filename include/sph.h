@@ -215,7 +215,9 @@ sph_status sph_eigenvalues(sph_ctx* ctx, int n, double* A, double* w, int ptr_on
  * bound requires them). */
 sph_status sph_get_counters(sph_ctx* ctx, int64_t* steps, int32_t* rebuilds);
 
-/* Number of our kernel launches one substep issues (for the bench's gpu_launches count). */
+/* Number of our kernel launches one substep issues (for the bench's gpu_launches count);
+ * 0 when the context runs small batches as one cooperative launch per tick (or per sph_step /
+ * sph_settle call) instead of per-substep kernels. */
 int sph_launches_per_substep(const sph_ctx* ctx);
 
 /* Sizes of the context (any pointer may be NULL). */

@@ -44,6 +44,9 @@ struct sph_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool fork = true;   // small path: rebuild branch concurrent with density/forces (SPH_FORK=0: serial)
     bool pdl = true;    // programmatic dependent launch on the substep chain (SPH_PDL=0: off)
+    // small batches: the substep loop of a tick as one cooperative launch (k_coop)
+    bool coop = false;
+    int coop_grid = 0;
     // live kernel timing inside the tick graph (sph_set_live_timing): event-record nodes around
     // the density / force launches of every live_every-th substep, read after each tick
     int live_every = 0;
@@ -475,6 +478,17 @@ static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool cap
     return e;
 }
 
+// n substeps of the small-batch path in one cooperative launch
+static cudaError_t launch_coop(sph_ctx* ctx, int n, float damping, int pin) {
+    DevParams P = ctx->P;
+    DevPtrs D = ctx->D;
+    float ga = ctx->ghost_angle0;
+    int nt = ctx->body_threads;
+    void* args[] = {&P, &D, &n, &damping, &pin, &ga, &nt};
+    return cudaLaunchCooperativeKernel((void*)k_coop, dim3(ctx->coop_grid), dim3(COOP_T), args, 0,
+                                       ctx->stream);
+}
+
 static int live_samples(const sph_ctx* ctx) {
     return ctx->live_every > 0 ? (ctx->n_sub + ctx->live_every - 1) / ctx->live_every : 0;
 }
@@ -632,6 +646,22 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             const int v = std::atoi(bt);
             if (v >= 32 && v <= 1024 && (v & (v - 1)) == 0) ctx->body_threads = v;
         }
+        {   // cooperative tick for latency-bound small batches (SPH_COOP=0/1 forces it)
+            const char* ce = std::getenv("SPH_COOP");
+            bool want = ce ? ce[0] == '1' : ((size_t)P.B * P.N <= 65536 && !ctx->small);
+            want = want && !P.ring && ctx->body_threads <= COOP_T && P.bsplit == 1;
+            int coop_ok = 0, per_sm = 0;
+            cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, dev);
+            if (want && coop_ok &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coop, COOP_T, 0) == cudaSuccess &&
+                per_sm > 0) {
+                const int ncb = (P.ncell + TILE - 1) / TILE;
+                const int need = std::max({P.ntile * P.B, ncb * P.B, P.nscan * P.B, P.B, 1});
+                ctx->coop_grid = std::min(per_sm * nsm, need);
+                ctx->coop = true;
+            }
+            cudaGetLastError();
+        }
     }
     if ((e = cudaMemsetAsync(d_workspace, 0, total, s)) != cudaSuccess) return bail("memset", e);
     std::vector<double2> gb(std::max(n_ghost, 1));
@@ -723,7 +753,11 @@ sph_status sph_step(sph_ctx* ctx, const float* u, int n_substeps, int ptr_on_dev
         for (int i = 0; i < 3 * P.B; ++i)
             if (!std::isfinite(u[i])) return fail(ctx, SPH_EINVAL, "non-finite input u");
     CK(cudaMemcpyAsync(ctx->D.u_cur, u, ub, ptr_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    for (int k = 0; k < n_substeps; ++k) launch_substep(ctx, 1.0f, 0);
+    if (ctx->coop) {
+        if (n_substeps > 0) CK(launch_coop(ctx, n_substeps, 1.0f, 0));
+    } else {
+        for (int k = 0; k < n_substeps; ++k) launch_substep(ctx, 1.0f, 0);
+    }
     sph_status st = check_launch(ctx);
     if (st) return st;
     if (!ptr_on_device) CK(cudaStreamSynchronize(s));
@@ -828,13 +862,17 @@ sph_status sph_rollout_batch(sph_ctx* ctx, const float* u_seq, int K, const sph_
         du = su;
         dth = pd ? sth : nullptr;
     }
-    sph_status st = capture_tick_graph(ctx);
+    sph_status st = ctx->coop ? SPH_OK : capture_tick_graph(ctx);
     if (st) return st;
     const int tb = 128, tg = (P.B + tb - 1) / tb;
     for (int k = 0; k < K; ++k) {
         k_tick<<<tg, tb, 0, s>>>(P, ctx->D, du, dth, dy, dua, K, k, pd ? 1 : 0, pd ? pd->Kp : 0.0, pd ? pd->Kd : 0.0);
+        if (ctx->coop) {
+            CK(launch_coop(ctx, ctx->n_sub, 1.0f, 0));
+            continue;
+        }
         CK(cudaGraphLaunch(ctx->tick_graph, s));
-        if (ctx->live_every > 0) {   // read this tick's timing nodes before the next launch
+        if (ctx->live_every > 0 && !ctx->coop) {   // read this tick's timing nodes before the next launch
             CK(cudaStreamSynchronize(s));
             st = accumulate_live(ctx);
             if (st) return st;
@@ -861,7 +899,11 @@ sph_status sph_get_body_state(sph_ctx* ctx, double* out) {
 sph_status sph_settle(sph_ctx* ctx, double damping, int n_steps) {
     if (!ctx || n_steps < 0 || !(damping > 0 && damping <= 1)) return SPH_EINVAL;
     CK(cudaMemsetAsync(ctx->D.u_cur, 0, sizeof(float) * 3 * ctx->P.B, ctx->stream));
-    for (int k = 0; k < n_steps; ++k) launch_substep(ctx, (float)damping, 1);
+    if (ctx->coop) {
+        if (n_steps > 0) CK(launch_coop(ctx, n_steps, (float)damping, 1));
+    } else {
+        for (int k = 0; k < n_steps; ++k) launch_substep(ctx, (float)damping, 1);
+    }
     sph_status st = check_launch(ctx);
     if (st) return st;
     CK(cudaStreamSynchronize(ctx->stream));
@@ -991,7 +1033,9 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
     return SPH_OK;
 }
 
-int sph_launches_per_substep(const sph_ctx* ctx) { return ctx ? launches_per_substep(ctx) : 0; }
+int sph_launches_per_substep(const sph_ctx* ctx) {
+    return ctx ? (ctx->coop ? 0 : launches_per_substep(ctx)) : 0;   // 0: one cooperative launch per tick
+}
 
 sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr_on_device) {
     if (!ctx || !A || !B) return SPH_EINVAL;

@@ -1,19 +1,22 @@
 // sph_kernels.cuh -- the sm_100a kernels of one substep (see sph_device.cuh for the pipeline).
 // Included once by sph_api.cu.  P:n = line n of the paper text.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "sph_device.cuh"
 
 namespace sph {
+namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------------------------------
 // Rebuild 1/8: cell key + rank inside the cell (north star: "cell-hash build").
 // Grid origin o = float(r_body) - half (reading A19), cells row-major.
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TILE) k_hash(DevParams P, DevPtrs D) {
-    const int b = blockIdx.y;
+__device__ __forceinline__ void hash_blk(const DevParams& P, const DevPtrs& D, int bx, int by) {
+    const int b = by;
     RolloutState* rs = D.rs + b;
     if (rs->frozen || !rs->need_rebin) return;
-    const int i = blockIdx.x * TILE + threadIdx.x;
+    const int i = bx * TILE + threadIdx.x;
     if (i == 0) {
         rs->span = 0;           // recomputed by k_nlist (kernel boundary orders the atomics)
         rs->rbx = D.geom[b].rx; // body position at this rebuild (Verlet criterion)
@@ -34,6 +37,7 @@ __global__ void __launch_bounds__(TILE) k_hash(DevParams P, DevPtrs D) {
     D.key[o + i] = c;
     D.rank[o + i] = atomicAdd(D.counts + (size_t)b * P.ncell + c, 1u);
 }
+__global__ void __launch_bounds__(TILE) k_hash(DevParams P, DevPtrs D) { hash_blk(P, D, blockIdx.x, blockIdx.y); }
 
 // ---------------------------------------------------------------------------------------
 // Rebuild 2-4/8: segmented exclusive scan of the cell counts of each rollout
@@ -66,11 +70,11 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total)
     return base + x - v;
 }
 
-__global__ void __launch_bounds__(SCAN_T) k_scan_reduce(DevParams P, DevPtrs D) {
-    const int b = blockIdx.y;
+__device__ __forceinline__ void scan_reduce_blk(const DevParams& P, const DevPtrs& D, int bx, int by) {
+    const int b = by;
     if (D.rs[b].frozen || !D.rs[b].need_rebin) return;
     const uint32_t* cnt = D.counts + (size_t)b * P.ncell;
-    const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_V;
+    const int base = bx * SCAN_TILE + threadIdx.x * SCAN_V;
     uint32_t s = 0;
 #pragma unroll
     for (int v = 0; v < SCAN_V; ++v) {
@@ -79,11 +83,12 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_reduce(DevParams P, DevPtrs D) 
     }
     uint32_t tot;
     block_excl_scan(s, &tot);
-    if (threadIdx.x == 0) D.tsum[(size_t)b * P.nscan + blockIdx.x] = tot;
+    if (threadIdx.x == 0) D.tsum[(size_t)b * P.nscan + bx] = tot;
 }
+__global__ void __launch_bounds__(SCAN_T) k_scan_reduce(DevParams P, DevPtrs D) { scan_reduce_blk(P, D, blockIdx.x, blockIdx.y); }
 
-__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(DevParams P, DevPtrs D) {
-    const int b = blockIdx.x;
+__device__ __forceinline__ void scan_tiles_blk(const DevParams& P, const DevPtrs& D, int bx, int by) {
+    const int b = bx;
     if (D.rs[b].frozen || !D.rs[b].need_rebin) return;
     uint32_t* ts = D.tsum + (size_t)b * P.nscan;
     const int per = (P.nscan + SCAN_T - 1) / SCAN_T;   // host guarantees per <= SCAN_V
@@ -103,13 +108,14 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_tiles(DevParams P, DevPtrs D) {
         run += v[k];
     }
 }
+__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(DevParams P, DevPtrs D) { scan_tiles_blk(P, D, blockIdx.x, blockIdx.y); }
 
-__global__ void __launch_bounds__(SCAN_T) k_scan_down(DevParams P, DevPtrs D) {
-    const int b = blockIdx.y;
+__device__ __forceinline__ void scan_down_blk(const DevParams& P, const DevPtrs& D, int bx, int by) {
+    const int b = by;
     if (D.rs[b].frozen || !D.rs[b].need_rebin) return;
     uint32_t* cnt = D.counts + (size_t)b * P.ncell;
     uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
-    const int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_V;
+    const int base = bx * SCAN_TILE + threadIdx.x * SCAN_V;
     uint32_t v[SCAN_V];
     uint32_t s = 0;
 #pragma unroll
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_down(DevParams P, DevPtrs D) {
         v[k] = c < P.ncell ? cnt[c] : 0u;
         s += v[k];
     }
-    uint32_t run = block_excl_scan(s, nullptr) + D.tsum[(size_t)b * P.nscan + blockIdx.x];
+    uint32_t run = block_excl_scan(s, nullptr) + D.tsum[(size_t)b * P.nscan + bx];
 #pragma unroll
     for (int k = 0; k < SCAN_V; ++k) {
         int c = base + k;
@@ -127,30 +133,32 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_down(DevParams P, DevPtrs D) {
         run += v[k];
     }
 }
+__global__ void __launch_bounds__(SCAN_T) k_scan_down(DevParams P, DevPtrs D) { scan_down_blk(P, D, blockIdx.x, blockIdx.y); }
 
 // ---------------------------------------------------------------------------------------
 // Rebuild 5/8: scatter old slot -> new slot (cell start + rank).
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TILE) k_scatter(DevParams P, DevPtrs D) {
-    const int b = blockIdx.y;
+__device__ __forceinline__ void scatter_blk(const DevParams& P, const DevPtrs& D, int bx, int by) {
+    const int b = by;
     if (D.rs[b].frozen || !D.rs[b].need_rebin) return;
-    const int i = blockIdx.x * TILE + threadIdx.x;
+    const int i = bx * TILE + threadIdx.x;
     if (i >= P.N) return;
     const size_t o = (size_t)b * P.N;
     const uint32_t c = D.key[o + i];
     D.perm[o + D.cstart[(size_t)b * (P.ncell + 1) + c] + D.rank[o + i]] = (uint32_t)i;
 }
+__global__ void __launch_bounds__(TILE) k_scatter(DevParams P, DevPtrs D) { scatter_blk(P, D, blockIdx.x, blockIdx.y); }
 
 // ---------------------------------------------------------------------------------------
 // Rebuild 6/8: make the order inside every cell ascending in canonical id (the atomic ranks
 // are not deterministic; this makes the whole sort deterministic and history independent,
 // reading A20).  One thread per cell.
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TILE) k_cellsort(DevParams P, DevPtrs D) {
-    const int b = blockIdx.y;
+__device__ __forceinline__ void cellsort_blk(const DevParams& P, const DevPtrs& D, int bx, int by) {
+    const int b = by;
     const RolloutState* rs = D.rs + b;
     if (rs->frozen || !rs->need_rebin) return;
-    const int c = blockIdx.x * TILE + threadIdx.x;
+    const int c = bx * TILE + threadIdx.x;
     if (c >= P.ncell) return;
     const uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
     const uint32_t s = cs[c], e = cs[c + 1];
@@ -189,16 +197,17 @@ __global__ void __launch_bounds__(TILE) k_cellsort(DevParams P, DevPtrs D) {
         }
     }
 }
+__global__ void __launch_bounds__(TILE) k_cellsort(DevParams P, DevPtrs D) { cellsort_blk(P, D, blockIdx.x, blockIdx.y); }
 
 // ---------------------------------------------------------------------------------------
 // Rebuild 7/8: gather the state into cell order (coalesced writes; reads are nearly sequential
 // because particles move little between rebuilds).
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) {
-    const int b = blockIdx.y;
+__device__ __forceinline__ void gather_blk(const DevParams& P, const DevPtrs& D, int bx, int by) {
+    const int b = by;
     const RolloutState* rs = D.rs + b;
     if (rs->frozen || !rs->need_rebin) return;
-    const int d = blockIdx.x * TILE + threadIdx.x;
+    const int d = bx * TILE + threadIdx.x;
     if (d >= P.N) return;
     const size_t o = (size_t)b * P.N;
     const int sp = rs->sp, ip = rs->ip;
@@ -209,6 +218,7 @@ __global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) {
     const float4 x = D.pv[sp ^ 1][o + d];
     D.xb[o + d] = make_float2(x.x, x.y);   // positions at this rebuild (Verlet criterion)
 }
+__global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) { gather_blk(P, D, blockIdx.x, blockIdx.y); }
 
 // ---------------------------------------------------------------------------------------
 // Rebuild 8/8: neighbour candidate list of every slot: all j != i of the 3x3 rebuild-time
@@ -615,11 +625,11 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
     return ovf ? -1 : max(-first, last);   // entries ascend in j: first = min, last = max
 }
 
-__global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
-    const int b = blockIdx.y;
+__device__ __forceinline__ void nlist_blk(const DevParams& P, const DevPtrs& D, int bx, int by) {
+    const int b = by;
     RolloutState* rs = D.rs + b;
     if (rs->frozen || !rs->need_rebin) return;
-    const int i = blockIdx.x * TILE + threadIdx.x;
+    const int i = bx * TILE + threadIdx.x;
     int span = 0;
     if (i < P.N) {
         const size_t o = (size_t)b * P.N;
@@ -633,6 +643,7 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) {
     span = __reduce_max_sync(0xffffffffu, span);
     if ((threadIdx.x & 31) == 0 && span > 0) atomicMax(&rs->span, span);
 }
+__global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) { nlist_blk(P, D, blockIdx.x, blockIdx.y); }
 
 // dynamic shared memory: start[ncell + 1] u32 | key[N] u32 | perm[N] u32 | rank[N] u16
 // (host guarantees N < 65536).  Sort only: the lists and the densities of the rebuilt rollouts
@@ -735,32 +746,34 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
 // grid = (tiles, Y); CTA (x, y) handles tile x of work items y, y + Y, ...  The cell table,
 // slot cells and sorted state come from the sort (k_rebuild_small or the grid-wide
 // rebuild kernels); the list just written by a thread is read back by the same thread.
+// lists + density of slot i of the rebuilt rollout b (every lane of the warp calls it)
+__device__ __forceinline__ void nlist_density_at(const DevParams& P, const DevPtrs& D, int b, int i) {
+    RolloutState* rs = D.rs + b;
+    const size_t o = (size_t)b * P.N;
+    const float4* __restrict__ pv = opaque(D.pv[rs->sp ^ 1] + o);   // sorted (rebuilt) buffer
+    auto pos = [&](uint32_t j) {
+        const float4 v = __ldg(pv + j);
+        return make_float2(v.x, v.y);
+    };
+    int span = 0;
+    if (i < P.N) {
+        float wf;
+        span = build_list_core<true>(P, D, b, i, D.cstart + (size_t)b * (P.ncell + 1),
+                                     D.skey[o + i], pos, &wf);
+        if (span >= 0) finish_density(P, D, b, i, pos((uint32_t)i), wf);
+        else density_core<false>(P, D, b, i, pos);   // list overflow: cell-scan density
+    }
+    span = __reduce_max_sync(0xffffffffu, span);
+    if ((threadIdx.x & 31) == 0 && span > 0) atomicMax(&rs->span, span);
+}
+
 template <int TN>
 __global__ void __launch_bounds__(TN) k_nlist_density(DevParams P, DevPtrs D) {
     pdl_wait();
     pdl_trigger();
     const int count = *D.rcount;
     const int i = blockIdx.x * TN + threadIdx.x;
-    for (int w = blockIdx.y; w < count; w += gridDim.y) {
-        const int b = D.rlist[w];
-        RolloutState* rs = D.rs + b;
-        const size_t o = (size_t)b * P.N;
-        const float4* __restrict__ pv = opaque(D.pv[rs->sp ^ 1] + o);   // sorted (rebuilt) buffer
-        auto pos = [&](uint32_t j) {
-            const float4 v = __ldg(pv + j);
-            return make_float2(v.x, v.y);
-        };
-        int span = 0;
-        if (i < P.N) {
-            float wf;
-            span = build_list_core<true>(P, D, b, i, D.cstart + (size_t)b * (P.ncell + 1),
-                                         D.skey[o + i], pos, &wf);
-            if (span >= 0) finish_density(P, D, b, i, pos((uint32_t)i), wf);
-            else density_core<false>(P, D, b, i, pos);   // list overflow: cell-scan density
-        }
-        span = __reduce_max_sync(0xffffffffu, span);
-        if ((threadIdx.x & 31) == 0 && span > 0) atomicMax(&rs->span, span);
-    }
+    for (int w = blockIdx.y; w < count; w += gridDim.y) nlist_density_at(P, D, D.rlist[w], i);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1100,30 +1113,26 @@ __global__ void __launch_bounds__(BRED_T) k_body_reduce(DevParams P, DevPtrs D) 
 // ---------------------------------------------------------------------------------------
 // blockDim.x = a power of two <= 1024, chosen from N only (so the reduction order, and hence
 // the bits, never depend on the batch size).
-__global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
-                                               float ghost_angle0) {
-    pdl_wait();
-    pdl_trigger();
-    const int b = blockIdx.x;
-    const int nt = blockDim.x;
+// Body step of rollout b by the CTA: fixed-order fp64 reduction of the per-warp partials over
+// the first nt threads (nt = k_body's block size, chosen from N only, so the bits never depend on
+// the launch shape), Newton-Euler kick-then-drift, status, parity flips, rebuild decision, then
+// the ghosts of the next substep by every thread.  red: shared memory [>= nt].  CTA-uniform.
+__device__ __forceinline__ void body_step(const DevParams& P, const DevPtrs& D, int b, int pin,
+                                          float ghost_angle0, double4* red, int nt) {
     RolloutState* rs = D.rs + b;
-    extern __shared__ double4 red[];   // [blockDim.x]
     __shared__ double sbody[8];
-    __shared__ int sdead;
-    if (threadIdx.x == 0) sdead = rs->frozen;
-    __syncthreads();
-    if (sdead) return;
     double4 s = make_double4(0, 0, 0, 0);
     const int np = P.bsplit > 1 ? P.bsplit : P.npart;
     const double4* part = P.bsplit > 1 ? D.part2 + (size_t)b * P.bsplit : D.part + (size_t)b * P.npart;
-    for (int t = threadIdx.x; t < np; t += nt) {
-        const double4 q = part[t];
-        s.x += q.x;
-        s.y += q.y;
-        s.z += q.z;
-        s.w = fmax(s.w, q.w);
-    }
-    red[threadIdx.x] = s;
+    if (threadIdx.x < nt)
+        for (int t = threadIdx.x; t < np; t += nt) {
+            const double4 q = part[t];
+            s.x += q.x;
+            s.y += q.y;
+            s.z += q.z;
+            s.w = fmax(s.w, q.w);
+        }
+    if (threadIdx.x < nt) red[threadIdx.x] = s;
     __syncthreads();
     for (int w = nt / 2; w > 0; w >>= 1) {
         if (threadIdx.x < w) {
@@ -1162,8 +1171,6 @@ __global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
         rs->sp = rs->sp ^ nr ^ 1;
         rs->ip ^= nr;
         rs->rebuilds += nr;
-        // drift of any particle relative to the body translation in this substep:
-        // dt |v_i' - rdot_n'| <= dt (|v_i' - rdot_n| + dt |rddot|)
         // max over particles of |(x_i - x_i^build) - (r_n - r^build)| (from k_force) plus the
         // body's drift in this substep: a strict bound on every particle's displacement
         // relative to the body translation since the last rebuild (Verlet criterion)
@@ -1174,7 +1181,75 @@ __global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
         if (rs->status) rs->frozen = 1;
     }
     __syncthreads();
-    ghost_update(P, D, b, sbody, threadIdx.x, nt);
+    ghost_update(P, D, b, sbody, threadIdx.x, blockDim.x);
+    __syncthreads();   // sbody / red reusable by the caller's next rollout
+}
+
+// blockDim.x = a power of two <= 1024, chosen from N only (so the reduction order, and hence
+// the bits, never depend on the batch size).
+__global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
+                                               float ghost_angle0) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ double4 red[];   // [blockDim.x]
+    const int b = blockIdx.x;
+    if (D.rs[b].frozen) return;        // CTA-uniform
+    body_step(P, D, b, pin, ghost_angle0, red, blockDim.x);
+}
+
+// ---------------------------------------------------------------------------------------
+// Small batches (latency-bound: C1, P0, a single C2 tank): the whole substep loop of a slow
+// tick in ONE cooperative launch.  Every phase of the multi-kernel path runs as a loop over
+// virtual blocks of TILE threads separated by grid-wide barriers (cooperative groups), with
+// the same per-particle, per-warp and per-rollout arithmetic -- so results are bitwise equal to
+// the multi-kernel path (and independent of B).  No launch gaps, no per-kernel tails.
+// ---------------------------------------------------------------------------------------
+constexpr int COOP_T = TILE;
+__global__ void __launch_bounds__(COOP_T, 2) k_coop(DevParams P, DevPtrs D, int n_sub,
+                                                     float damping, int pin, float ghost_angle0,
+                                                     int body_nt) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double4 red[COOP_T];
+    const int G = gridDim.x;
+    const int nt = P.ntile * P.B;                          // (tile, rollout) virtual blocks
+    const int ncb = (P.ncell + TILE - 1) / TILE;
+    for (int it = 0; it < n_sub; ++it) {
+        int any = 0;
+        for (int b = 0; b < P.B; ++b) any |= D.rs[b].need_rebin & (D.rs[b].frozen ^ 1);
+        if (any) {   // grid-uniform: the counting sort of every rollout that needs it
+            for (int v = blockIdx.x; v < nt; v += G) hash_blk(P, D, v % P.ntile, v / P.ntile);
+            grid.sync();
+            for (int v = blockIdx.x; v < P.nscan * P.B; v += G) scan_reduce_blk(P, D, v % P.nscan, v / P.nscan);
+            grid.sync();
+            for (int v = blockIdx.x; v < P.B; v += G) scan_tiles_blk(P, D, v, 0);
+            grid.sync();
+            for (int v = blockIdx.x; v < P.nscan * P.B; v += G) scan_down_blk(P, D, v % P.nscan, v / P.nscan);
+            grid.sync();
+            for (int v = blockIdx.x; v < nt; v += G) scatter_blk(P, D, v % P.ntile, v / P.ntile);
+            grid.sync();
+            for (int v = blockIdx.x; v < ncb * P.B; v += G) cellsort_blk(P, D, v % ncb, v / ncb);
+            grid.sync();
+            for (int v = blockIdx.x; v < nt; v += G) gather_blk(P, D, v % P.ntile, v / P.ntile);
+            grid.sync();
+        }
+        // lists + densities of the rebuilt rollouts, densities of the others (disjoint rollouts)
+        for (int v = blockIdx.x; v < nt; v += G) {
+            const int b = v / P.ntile, i = (v % P.ntile) * TILE + threadIdx.x;
+            const RolloutState* rs = D.rs + b;
+            if (rs->frozen) continue;                      // CTA-uniform
+            if (rs->need_rebin) {
+                nlist_density_at(P, D, b, i);
+            } else if (i < P.N) {
+                density_at<true>(P, D, b, i, D.pv[rs->sp] + (size_t)b * P.N);
+            }
+        }
+        grid.sync();
+        for (int v = blockIdx.x; v < nt; v += G) force_tile<TILE>(P, D, damping, v / P.ntile, v % P.ntile);
+        grid.sync();
+        for (int b = blockIdx.x; b < P.B; b += G)
+            if (!D.rs[b].frozen) body_step(P, D, b, pin, ghost_angle0, red, body_nt);
+        grid.sync();
+    }
 }
 
 // ---------------------------------------------------------------------------------------

@@ -209,9 +209,11 @@ def test_graph_rollout_equals_direct_steps(settled_c1):
 
 
 @pytest.mark.parametrize("path", [1, 2])
-def test_live_timing_nodes_do_not_change_results(settled_c1, path):
+def test_live_timing_nodes_do_not_change_results(settled_c1, path, monkeypatch):
     """Event-record nodes in the tick graph (bench's live kernel timing) leave the trajectory
-    bitwise unchanged, and the sampled times are consistent (parts <= whole substep)."""
+    bitwise unchanged, and the sampled times are consistent (parts <= whole substep).
+    (Graph path: the cooperative small-batch tick has no per-kernel nodes.)"""
+    monkeypatch.setenv("SPH_COOP", "0")
     t = settled_c1
     K = 2
     u = si.ensemble_inputs([3, 4], K)[0]
@@ -467,3 +469,26 @@ def test_reading_switches_one_step_parity(over):
     for sl in (slice(0, 2), slice(2, 3), slice(3, 5), slice(5, 6)):
         assert _rel(bg[sl], ref.body[sl], 1e-12) <= 1e-5
     ctx.close()
+
+
+@pytest.mark.parametrize("ell,B", [(1.0, 1), (1.0, 3), (4.0, 1)])
+def test_cooperative_tick_bitwise_equals_kernel_path(ell, B, monkeypatch):
+    """Small batches run a whole tick as one cooperative launch (k_coop); its phases use the
+    multi-kernel path's per-particle / per-warp / per-rollout arithmetic, so trajectories,
+    particle states and rebuild counts are bitwise equal to the per-substep kernels."""
+    t = si.moving_tank(ell, seed=4, vel=0.02)
+    sp = t.params
+    u = si.ensemble_inputs(list(range(B)), 3)[0] * 20.0
+    out = []
+    for coop in ("0", "1"):
+        monkeypatch.setenv("SPH_COOP", coop)
+        ctx = _ctx(t, B=B, rebin_every=0, skin=0.15 * sp.h)
+        assert (ctx.launches_per_substep() == 0) == (coop == "1")
+        y, ua = ctx.rollout(u)
+        ctx.step(u[:, 0], 7)                                   # sph_step path too
+        out.append((y, ctx.get_particles(B - 1), ctx.get_body_state(), ctx.counters()[1]))
+        assert (ctx.get_status()[0] == 0).all()
+        ctx.close()
+    assert out[0][3].min() >= 2                                  # rebuilds happened
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)

@@ -14,7 +14,7 @@ l=sys.stdin.read().strip()
 try:
   d=json.loads(l); r=d['roofline']
   print('value %.3e' % d['value'], 'chk %.9e' % d['config'].get('y_checksum',0), 'reb/sub %.1f' % d['config']['substeps_per_rebuild'],
-        'live', {k: round(v*1e3,1) for k,v in r['live_ms'].items()}, 'isolated', {k: round(v*1e3,1) for k,v in r['isolated_ms'].items()}, 'frac %.3f' % r['frac'])
+        'live', {k: (round(v*1e3,1) if v is not None else None) for k,v in r['live_ms'].items()}, 'isolated', {k: round(v*1e3,1) for k,v in r['isolated_ms'].items()}, 'ms/step %.3f' % d['ms_per_step'], 'frac %.3f' % r['frac'])
 except Exception as e: print('ERR', l[-800:])
 "
 done
