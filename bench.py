@@ -49,9 +49,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN", "P0"],
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN", "P0", "C2CL"],
                     help="LIN: linearization (SURVEY 8(f) f1) of the paper's P0 tank; P0: the paper's "
-                         "Table 3 benchmark (30 s closed loop); neither is the north-star line")
+                         "Table 3 benchmark (30 s closed loop); C2CL: the same manoeuvre on the C2 tank (configs[1]); "
+                         "none of them is the north-star line")
     ap.add_argument("--rollouts", type=int, default=0, help="override rollouts per GPU")
     ap.add_argument("--rebin-every", type=int, default=0,
                     help="1: rebuild cell list + neighbour lists every substep; 0: adaptive (skin)")
@@ -557,25 +558,30 @@ P0_METRIC = "SPH simulation time of manoeuvre profile 1, 30 s closed loop (paper
 P0_PAPER_S = 9.9093   # RTX 2000 Ada laptop GPU, JAX (context, not the target)
 
 
-def run_p0(a):
+def run_p0(a, closed_loop_c2=False):
+    """P0 (the paper's Table 3 tank) or, with closed_loop_c2, the C2 tank (configs[1]: paper
+    resolution x4, one manoeuvre, closed loop): profile 1 + PD law over 30 s."""
     import torch
     rank, world, local = dist_env()
     if rank != 0:
         return
     torch.cuda.set_device(local)
     from paper_2604_12505_b200 import SphContext
-    t = si.make_tank(1.0, n_first=666)
+    t = si.make_tank(4.0) if closed_loop_c2 else si.make_tank(1.0, n_first=666)
     sp = t.params
     K = int(round(30.0 / (sp.dt * sp.n_sub)))                # 600 slow ticks of 50 ms
     u, th = si.profile(1, K)
     u = u.astype(np.float32)[None]
     th = th.astype(np.float32)[None]
-    # damped settle (reading A17, untimed) on the GPU from the lattice
-    ctx = SphContext(sp, t.pv32(), t.ghost_b, n_rollouts=1, rebin_every=0, skin=a.skin * sp.h,
-                     device=local)
-    ctx.settle(math.exp(-10.0 * sp.dt), int(2.0 / sp.dt))
-    pv0 = ctx.get_particles(0)
-    ctx.close()
+    # damped settle (reading A17, untimed): the oracle-settled C2 snapshot, else 2 s on the GPU
+    if closed_loop_c2:
+        pv0 = settled_start(t, a.settle_seconds, local)
+    else:
+        ctx = SphContext(sp, t.pv32(), t.ghost_b, n_rollouts=1, rebin_every=0, skin=a.skin * sp.h,
+                         device=local)
+        ctx.settle(math.exp(-10.0 * sp.dt), int(2.0 / sp.dt))
+        pv0 = ctx.get_particles(0)
+        ctx.close()
     ctx = SphContext(sp, pv0, t.ghost_b, n_rollouts=1, rebin_every=0, skin=a.skin * sp.h, device=local)
     dev = torch.device("cuda", local)
     ud, thd = torch.from_numpy(u).to(dev), torch.from_numpy(th).to(dev)
@@ -596,12 +602,14 @@ def run_p0(a):
     secs = e0.elapsed_time(e1) / 1e3
     steps = K * sp.n_sub
     st = ctx.get_status()[0]
+    n_steps, n_reb = ctx.counters()
+    lps = ctx.launches_per_substep()
     theta_end = float(y[0, -1, 2])
     cpu = None
     if not a.no_cpu_baseline:
         import oracle as O
         s = O.State(sp, pv0[:, :2].astype(np.float64), pv0[:, 2:].astype(np.float64), t.ghost_b)
-        n_t = 40                                                  # 2 s of the profile, 1 thread
+        n_t = 4 if closed_loop_c2 else 40                         # a bounded sample, 1 thread
         c0 = time.perf_counter()
         s.rollout(u[0, :n_t], sp.n_sub, theta_ref=th[0, :n_t], Kp=sp.Kp, Kd=sp.Kd)
         dt = time.perf_counter() - c0
@@ -609,17 +617,27 @@ def run_p0(a):
                "sample": f"first {n_t} of {K} ticks ({n_t * sp.n_sub} steps), float64 C oracle, 1 thread, "
                          f"{dt:.1f} s, extrapolated to the 30 s horizon"}
     ctx.close()
+    if closed_loop_c2:
+        metric, vsb = "SPH simulation time of manoeuvre profile 1, 30 s closed loop, C2 tank", None
+        data = "synthetic (C2 lattice tank, oracle-settled snapshot, profile 1 + PD law)"
+        wl = f"C2CL: C2 tank (9261 fluid + 944 ghosts), dt 0.25 ms, {K} ticks x {sp.n_sub} substeps (configs[1])"
+    else:
+        metric, vsb = P0_METRIC, secs / P0_PAPER_S
+        data = "synthetic (P0 lattice tank, 2 s GPU damped settle, profile 1 + PD law)"
+        wl = "P0: paper tank, 666 fluid + 236 ghosts, dt 1 ms, 600 ticks x 50 substeps"
     line = {
-        "metric": P0_METRIC, "value": secs, "unit": "s", "n_gpus": 1, "steps": 1, "warmup": 1,
+        "metric": metric, "value": secs, "unit": "s", "n_gpus": 1, "steps": 1, "warmup": 1,
         "ms_per_step": secs * 1e3, "higher_is_better": False, "scaling": "none",
-        "vs_baseline": secs / P0_PAPER_S, "dtype": "f32 (body f64)",
-        "data": "synthetic (P0 lattice tank, 2 s GPU damped settle, profile 1 + PD law)",
-        "config": {"workload": "P0: paper tank, 666 fluid + 236 ghosts, dt 1 ms, 600 ticks x 50 substeps",
+        "vs_baseline": vsb, "dtype": "f32 (body f64)",
+        "data": data,
+        "config": {"workload": wl, "steps_per_s": steps / secs,
                    "substeps": steps, "us_per_substep": secs * 1e6 / steps,
                    "particle_updates_per_s": t.n_fluid * steps / secs,
                    "paper_seconds": P0_PAPER_S, "paper_hardware": "RTX 2000 Ada laptop GPU, JAX (P:391, P:490)",
-                   "status": int(st[0]), "theta_end_rad": theta_end},
-        "gpu_launches": K * (1 + sp.n_sub * 12),
+                   "status": int(st[0]), "theta_end_rad": theta_end,
+                   "substeps_per_rebuild": float(n_steps[0] / max(int(n_reb[0]), 1)),
+                   "path": "cooperative tick" if lps == 0 else f"{lps} kernels per substep"},
+        "gpu_launches": K * (1 + (sp.n_sub * lps if lps > 0 else 1)),
         "clocks": ck,
         "cpu_baseline": cpu,
     }
@@ -631,8 +649,8 @@ def main():
     if a.workload == "LIN":
         run_linearize(a)
         return
-    if a.workload == "P0":
-        run_p0(a)
+    if a.workload in ("P0", "C2CL"):
+        run_p0(a, closed_loop_c2=a.workload == "C2CL")
         return
     if a.impl == "reference":
         run_reference(a)

@@ -492,3 +492,37 @@ def test_cooperative_tick_bitwise_equals_kernel_path(ell, B, monkeypatch):
     assert out[0][3].min() >= 2                                  # rebuilds happened
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a, b)
+
+
+def test_closed_loop_profile1_speed_statistics_match_oracle():
+    """P0 tank, manoeuvre profile 1 + PD law from an oracle-settled start: over a
+    2 s horizon the distribution of fluid speeds relative to the body (max, p99, median) agrees
+    with the oracle's within 5 % (trajectories of the particles themselves decorrelate: the
+    flow is chaotic).  Also exercises the cooperative small-batch path under the PD law."""
+    t = si.make_tank(1.0, n_first=666)
+    sp = t.params
+    s = O.settle(t, seconds=2.0)
+    pv0 = np.concatenate([s.pos, s.vel], 1).astype(np.float32)
+    u, th = si.profile(1, 40)
+    ctx = SphContext_(t, pv0)
+    ctx.rollout(u[None].astype(np.float32), theta_ref=th[None].astype(np.float32), Kp=sp.Kp, Kd=sp.Kd)
+    ref = O.State(sp, pv0[:, :2].astype(np.float64), pv0[:, 2:].astype(np.float64), t.ghost_b)
+    ref.rollout(u.astype(np.float32).astype(np.float64), sp.n_sub,
+                theta_ref=th.astype(np.float32).astype(np.float64), Kp=sp.Kp, Kd=sp.Kd)
+
+    def stats(vel, body):
+        v = np.sqrt(((vel - body[3:5]) ** 2).sum(1))
+        return np.array([v.max(), np.percentile(v, 99), np.median(v)])
+
+    g = stats(ctx.get_particles(0)[:, 2:].astype(np.float64), ctx.get_body_state()[0])
+    o = stats(ref.vel, ref.body)
+    assert np.all(np.abs(g - o) <= 0.05 * o), (g, o)
+    # the body translation under the 5 N thrust (theta is still ~1e-6 rad noise before the 5 s
+    # reference step)
+    assert abs(ctx.get_body_state()[0][0] - ref.body[0]) <= 1e-3 * abs(ref.body[0])
+    ctx.close()
+
+
+def SphContext_(t, pv0):
+    from paper_2604_12505_b200 import SphContext
+    return SphContext(t.params, pv0, t.ghost_b, n_rollouts=1, rebin_every=0, skin=0.15 * t.params.h)
