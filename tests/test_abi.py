@@ -76,3 +76,20 @@ def test_invalid_parameters_rejected_without_gpu(libpath):
     st = L.sph_init_tank(C.byref(fp), C.byref(bp), C.byref(tp), 569, pv.ctypes.data, 236,
                          (gb * 0.9).ctypes.data, 1, None, 256, 1 << 40, C.byref(ctx))
     assert st == B.SPH_EINVAL
+
+
+def test_null_context_calls_rejected_without_gpu(libpath):
+    """Every entry point that takes a context returns SPH_EINVAL for a NULL context or NULL
+    buffers before touching the device (header: 'Argument / configuration errors return
+    SPH_EINVAL before any device work')."""
+    from paper_2604_12505_b200 import binding as B
+    L = B.lib()
+    buf = (C.c_double * 64)()
+    assert L.sph_jacobian(None, 0, buf, buf, 0) == B.SPH_EINVAL
+    assert L.sph_eigenvalues(None, 4, buf, buf, 0) == B.SPH_EINVAL
+    assert L.sph_step(None, None, 1, 0) == B.SPH_EINVAL
+    assert L.sph_get_body_state(None, buf) == B.SPH_EINVAL
+    assert L.sph_set_live_timing(None, 4) == B.SPH_EINVAL
+    assert L.sph_get_live_timing(None, buf, None, 0) == B.SPH_EINVAL
+    assert L.sph_settle(None, 0.5, 10) == B.SPH_EINVAL
+    assert L.sph_launches_per_substep(None) == 0
