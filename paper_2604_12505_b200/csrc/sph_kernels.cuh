@@ -931,11 +931,16 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
     const float2 xb = __ldg(D.xb + o + i);
     const float ddx = (xn.x - xb.x) - (gm.rx - rs->rbx), ddy = (xn.y - xb.y) - (gm.ry - rs->rby);
     acc.vmax = ddx * ddx + ddy * ddy;
-    const bool finite = isfinite(xn.x) && isfinite(xn.y) && isfinite(xn.z) && isfinite(xn.w);
-    if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || fabsf(xn.z) > 1e9f ||
-        fabsf(xn.w) > 1e9f)
-        set_status(const_cast<RolloutState*>(rs), finite ? 2 : 1,
-                   (int)D.id[rs->ip ^ rs->need_rebin][o + i]);
+    // one test for the common case: the abs-sum is NaN / inf for any non-finite element and
+    // exceeds 1e9 whenever an element does; classify only in the rare branch
+    const float mag = fabsf(xn.x) + fabsf(xn.y) + fabsf(xn.z) + fabsf(xn.w);
+    if (!(mag <= 1e9f)) {
+        const bool finite = isfinite(xn.x) && isfinite(xn.y) && isfinite(xn.z) && isfinite(xn.w);
+        if (!finite || fabsf(xn.x) > 1e9f || fabsf(xn.y) > 1e9f || fabsf(xn.z) > 1e9f ||
+            fabsf(xn.w) > 1e9f)
+            set_status(const_cast<RolloutState*>(rs), finite ? 2 : 1,
+                       (int)D.id[rs->ip ^ rs->need_rebin][o + i]);
+    }
 }
 
 // Body partials: warp butterfly (deterministic order), one fp64 partial per warp of 32 slots,
