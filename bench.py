@@ -34,7 +34,7 @@ import sph_inputs as si  # noqa: E402
 
 WORKLOADS = {
     # name: (ell, rollouts per GPU, description)
-    "C3": (4.0, 1024, "C3: 1024 rollouts x C2 tank (ell=4, 9261 fluid + 944 ghosts), open-loop excitation, 1 GPU"),
+    "C3": (4.0, 1024, "C3: 1024 rollouts per GPU x C2 tank (ell=4, 9261 fluid + 944 ghosts), open-loop excitation"),
     "C2": (4.0, 1, "C2: single C2 tank (9261 + 944), excitation, latency-bound"),
     "C4": (42.0, 1, "C4: single ell=42 tank (1,025,788 + 9,912)"),
     "C1": (1.0, 1, "C1: single ell=1 tank (569 + 236)"),
@@ -70,6 +70,10 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # control-flow check of the multi-rank path on a 1-GPU box (tools/check_multirank_bench.sh):
+    # every rank on device 0, gloo collectives; never used for a measured number
+    if os.environ.get("BENCH_SINGLE_DEVICE_CHECK") == "1":
+        local = 0
     return rank, world, local
 
 
@@ -292,7 +296,10 @@ def run_ours(a):
     import torch.distributed as dist
     rank, world, local = dist_env()
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("BENCH_SINGLE_DEVICE_CHECK") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2604_12505_b200 import SphContext
@@ -445,7 +452,9 @@ def run_ours(a):
                    "ghosts_per_rollout": t.n_ghost, "substeps_per_step": sp.n_sub,
                    "dt": sp.dt, "rebin_every": a.rebin_every, "skin_h": a.skin,
                    "parallelism": f"ensemble dp{world}",
-                   "l2": f"no flush: working set {ctx_bytes_gb(t, B):.2f} GB > 126 MB L2",
+                   "l2": (f"no flush: working set {ctx_bytes_gb(t, B):.2f} GB > 126 MB L2"
+                          if ctx_bytes_gb(t, B) > 0.126 else
+                          f"working set {ctx_bytes_gb(t, B):.3f} GB fits the 126 MB L2 (not flushed)"),
                    "failed_rollouts": n_failed, "gather_ms": gather_ms, "settle": SETTLE_INFO,
                    "substeps_per_rebuild": float(steps_done.mean() / max(rebuilds.mean(), 1)),
                    "y_checksum": y_checksum},
