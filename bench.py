@@ -56,7 +56,9 @@ def parse():
     ap.add_argument("--rollouts", type=int, default=0, help="override rollouts per GPU")
     ap.add_argument("--rebin-every", type=int, default=0,
                     help="1: rebuild cell list + neighbour lists every substep; 0: adaptive (skin)")
-    ap.add_argument("--skin", type=float, default=0.15, help="Verlet skin in units of h (adaptive)")
+    ap.add_argument("--skin", type=float, default=None,
+                    help="Verlet skin in units of h (adaptive); default 0.15 for the open-loop ensembles, "
+                         "0.5 for the closed-loop manoeuvre runs (P0, C2CL: energetic flow, see DESIGN.md)")
     ap.add_argument("--live-every", type=int, default=16,
                     help="live kernel timing: event nodes every N-th substep of the timed ticks (0 = off)")
     ap.add_argument("--settle-seconds", type=float, default=4.0,
@@ -639,7 +641,7 @@ def run_p0(a, closed_loop_c2=False):
         "ms_per_step": secs * 1e3, "higher_is_better": False, "scaling": "none",
         "vs_baseline": vsb, "dtype": "f32 (body f64)",
         "data": data,
-        "config": {"workload": wl, "steps_per_s": steps / secs,
+        "config": {"workload": wl, "steps_per_s": steps / secs, "skin_h": a.skin,
                    "substeps": steps, "us_per_substep": secs * 1e6 / steps,
                    "particle_updates_per_s": t.n_fluid * steps / secs,
                    "paper_seconds": P0_PAPER_S, "paper_hardware": "RTX 2000 Ada laptop GPU, JAX (P:391, P:490)",
@@ -655,6 +657,8 @@ def run_p0(a, closed_loop_c2=False):
 
 def main():
     a = parse()
+    if a.skin is None:
+        a.skin = 0.5 if a.workload in ("P0", "C2CL") else 0.15
     if a.workload == "LIN":
         run_linearize(a)
         return
