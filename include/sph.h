@@ -178,7 +178,9 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms);
  * sph_get_live_timing writes the sums in ms over the sampled substeps into
  * ms_sum[SPH_NUM_LIVE] (order SPH_LIVE_*) and their count into *n_samples (nullable);
  * reset != 0 zeroes the accumulators afterwards.  In the small-rollout path the density and
- * the first force launch overlap the rebuild branch, so these are in-situ durations. */
+ * the force launches overlap the rebuild branch, so these are in-situ durations; the forces of
+ * the rebuilt rollouts run on that branch concurrently with the others', and the force time is
+ * the union of the two launches' active intervals. */
 enum { SPH_LIVE_DENSITY = 0, SPH_LIVE_FORCE = 1, SPH_LIVE_SUBSTEP = 2, SPH_NUM_LIVE = 3 };
 sph_status sph_set_live_timing(sph_ctx* ctx, int every);
 sph_status sph_get_live_timing(sph_ctx* ctx, double* ms_sum, int64_t* n_samples, int reset);

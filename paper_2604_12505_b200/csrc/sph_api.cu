@@ -44,6 +44,9 @@ struct sph_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool fork = true;   // small path: rebuild branch concurrent with density/forces (SPH_FORK=0: serial)
     bool pdl = true;    // programmatic dependent launch on the substep chain (SPH_PDL=0: off)
+    bool m2side = true; // small path: forces of the rebuilt rollouts at the end of the rebuild
+                        // branch (overlapping the others' forces); SPH_M2SIDE=0: after the join
+    float damping_cur = 1.0f;
     // small batches: the substep loop of a tick as one cooperative launch (k_coop)
     bool coop = false;
     int coop_grid = 0;
@@ -422,6 +425,12 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
         k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
         launch_nlist_density(ctx, ctx->side, true);
+        if (ctx->m2side) {   // (timing nodes on the side stream: the force time is the sum
+                             // of both launches' durations)
+            live_mark(ev, LV_F2_0, ctx->side);
+            launch_force(ctx, ctx->side, ctx->damping_cur, 2, np);
+            live_mark(ev, LV_F2_1, ctx->side);
+        }
         cudaEventRecord(ctx->ev_join, ctx->side);
         live_mark(ev, LV_DEN0, s);
         launch_density(ctx, s, 1, np);
@@ -454,6 +463,7 @@ static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool cap
         ev = ctx->live_ev.data() + (size_t)(k / ctx->live_every) * LIVE_SLOTS;
     live_mark(ev, LV_SUB0, s);
     const bool np = ev == nullptr;
+    ctx->damping_cur = damping;   // (the rebuild branch launches the rebuilt rollouts' forces)
     // PDL on the first kernel only when an in-stream kernel precedes it (not the first substep
     // of a captured graph)
     cudaError_t e = launch_rebuild_and_density(ctx, capturing, ev, !(capturing && k == 0));
@@ -465,9 +475,11 @@ static cudaError_t launch_substep(sph_ctx* ctx, float damping, int pin, bool cap
         launch_force(ctx, s, damping, 1, np);
         live_mark(ev, LV_F1_1, s);
         cudaStreamWaitEvent(s, ctx->ev_join, 0);
-        live_mark(ev, LV_F2_0, s);
-        launch_force(ctx, s, damping, 2, false);
-        live_mark(ev, LV_F2_1, s);
+        if (!ctx->m2side) {
+            live_mark(ev, LV_F2_0, s);
+            launch_force(ctx, s, damping, 2, false);
+            live_mark(ev, LV_F2_1, s);
+        }
     } else {
         live_mark(ev, LV_F1_0, s);
         launch_force(ctx, s, damping, 0, np);
@@ -573,6 +585,10 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
     ctx->P = P;
     ctx->fp = *fp;
     ctx->bp = *bp;
+    {
+        const char* e = std::getenv("SPH_M2SIDE");
+        ctx->m2side = !(e && e[0] == '0');
+    }
     {   // PDL pays for latency-bound small batches (C1 / C2 single tank +4 %); at C3 it is
         // neutral to -1 %, so it is on below the per-rollout rebuild threshold only.
         // SPH_PDL=0/1 forces it.
@@ -774,8 +790,19 @@ static sph_status accumulate_live(sph_ctx* ctx) {
     for (int q = 0; q < live_samples(ctx); ++q) {
         const cudaEvent_t* ev = ctx->live_ev.data() + (size_t)q * LIVE_SLOTS;
         CK(el(ev, LV_DEN0, LV_DEN1, &ctx->live_ms[SPH_LIVE_DENSITY]));
-        CK(el(ev, LV_F1_0, LV_F1_1, &ctx->live_ms[SPH_LIVE_FORCE]));
-        if (ctx->small && ctx->fork) CK(el(ev, LV_F2_0, LV_F2_1, &ctx->live_ms[SPH_LIVE_FORCE]));
+        if (ctx->small && ctx->fork && ctx->m2side) {
+            // the two force launches overlap (main stream / rebuild branch): the force time of
+            // the substep is the union of their active intervals
+            double a = 0, b = 0, c = 0, d = 0;
+            CK(el(ev, LV_SUB0, LV_F1_0, &a));
+            CK(el(ev, LV_SUB0, LV_F1_1, &b));
+            CK(el(ev, LV_SUB0, LV_F2_0, &c));
+            CK(el(ev, LV_SUB0, LV_F2_1, &d));
+            ctx->live_ms[SPH_LIVE_FORCE] += std::max(b, d) - std::min(a, c);
+        } else {
+            CK(el(ev, LV_F1_0, LV_F1_1, &ctx->live_ms[SPH_LIVE_FORCE]));
+            if (ctx->small && ctx->fork) CK(el(ev, LV_F2_0, LV_F2_1, &ctx->live_ms[SPH_LIVE_FORCE]));
+        }
         CK(el(ev, LV_SUB0, LV_SUB1, &ctx->live_ms[SPH_LIVE_SUBSTEP]));
         ++ctx->live_n;
     }
