@@ -183,7 +183,7 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->rebin_every = tp->rebin_every;
     const float RL = (float)(2.0 * h + (tp->rebin_every ? 0.0 : tp->skin));
     P->RL2 = tp->rebin_every ? P->H2 : RL * RL;      // list radius (2h + skin)^2
-    P->rebuild_disp = (float)(0.45 * tp->skin);      // < skin / 2 with margin for rounding
+    P->rebuild_disp = (float)(0.49 * tp->skin);      // < skin / 2; float rounding of the bound ~1e-4 skin
     P->NA = (N + 1) & ~1;
     {   // TMA-fed shared-memory ring kernels: opt-in (SPH_RING=1), measured no faster than the
         // plain gather kernels on C3
