@@ -249,6 +249,35 @@ __device__ __forceinline__ float w_list(const DevParams& P, float4 xi, float4 xj
     return fmaf(-4.0f * c, c * c, a * a * a);
 }
 
+#ifndef SPH_F32X2
+#define SPH_F32X2 1   // packed FP32 (FADD2 / FMUL2 / FFMA2) list loops
+#endif
+
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+// c - a as one FFMA2 (a * -1 + c is exact up to the one rounding of the difference; an explicit
+// negation of a register operand would cost an FADD per lane under -ftz)
+__device__ __forceinline__ float2 rsub2(float2 c, float2 a) { return __ffma2_rn(a, bc2(-1.0f), c); }
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// w_list of two candidates a, b on the packed FP32 pipe (sm_100 FADD2 / FMUL2 / FFMA2): lane
+// a / b of every float2 is candidate a / b, with w_list's operations and rounding per lane; one
+// issue slot serves both candidates except for the square roots and the clamps.  Returns w_a + w_b.
+__device__ __forceinline__ float w_list2(const DevParams& P, float2 pi, float2 xa, float2 xb) {
+    const float2 da = rsub2(pi, xa), db = rsub2(pi, xb);
+    const float2 r2 = make_float2(fmaf(da.x, da.x, da.y * da.y), fmaf(db.x, db.x, db.y * db.y));
+    const float2 q = __fmul2_rn(make_float2(sqrt_approx(r2.x), sqrt_approx(r2.y)), bc2(P.inv_h));
+    const float2 a0 = rsub2(bc2(2.0f), q), c0 = rsub2(bc2(1.0f), q);
+    const float2 a = make_float2(fmaxf(a0.x, 0.0f), fmaxf(a0.y, 0.0f));
+    const float2 c = make_float2(fmaxf(c0.x, 0.0f), fmaxf(c0.y, 0.0f));
+    const float2 w = __ffma2_rn(__fmul2_rn(bc2(-4.0f), c), __fmul2_rn(c, c),
+                                __fmul2_rn(__fmul2_rn(a, a), a));
+    return w.x + w.y;
+}
+
 // cell-scan fallback: candidates include the particle itself (valid = false)
 __device__ __forceinline__ float w_masked(const DevParams& P, float4 xi, float4 xj, bool valid) {
     const float w = w_list(P, xi, xj);
@@ -306,6 +335,13 @@ __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& 
             const uint2 w = wn;
             nq += P.N;
             if (k + 4 < n) wn = ld<NC>(nq);
+#if SPH_F32X2
+            wf += w_list2(P, p, pos((uint32_t)(i + quad_offset(w, 0))),
+                          pos((uint32_t)(i + quad_offset(w, 1))));
+            if (k + 2 < n)     // pairs granularity (see force_list)
+                wf += w_list2(P, p, pos((uint32_t)(i + quad_offset(w, 2))),
+                              pos((uint32_t)(i + quad_offset(w, 3))));
+#else
             const float4 x0 = as4(pos((uint32_t)(i + quad_offset(w, 0))));
             const float4 x1 = as4(pos((uint32_t)(i + quad_offset(w, 1))));
             wf += w_list(P, xi, x0) + w_list(P, xi, x1);
@@ -314,6 +350,7 @@ __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& 
                 const float4 x3 = as4(pos((uint32_t)(i + quad_offset(w, 3))));
                 wf += w_list(P, xi, x2) + w_list(P, xi, x3);
             }
+#endif
         }
         wf -= 4.0f * (float)(((n + 1) & ~1) - n);   // padding entries (self) added W(0) = 4 each
     } else {
@@ -810,6 +847,34 @@ __device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2
     sy += s * dy;
 }
 
+// pair_force of two list pairs a, b on the packed FP32 pipe (see w_list2): lane a / b of every
+// float2 is pair a / b with pair_force's operations per lane; the accumulation s = (sx, sy) is
+// one FFMA2 per pair, in the order a then b as in two pair_force calls.
+__device__ __forceinline__ void pair_force2(const DevParams& P, float4 xi, float2 ai, float4 xa,
+                                            float2 aa, float4 xb, float2 ab, float2& s) {
+    const float2 pi = make_float2(xi.x, xi.y), vi = make_float2(xi.z, xi.w);
+    const float2 da = rsub2(pi, make_float2(xa.x, xa.y)), db = rsub2(pi, make_float2(xb.x, xb.y));
+    const float2 wa = rsub2(vi, make_float2(xa.z, xa.w)), wb = rsub2(vi, make_float2(xb.z, xb.w));
+    const float2 r2 = make_float2(fmaf(da.x, da.x, da.y * da.y), fmaf(db.x, db.x, db.y * db.y));
+    const float2 vr = make_float2(fmaf(wa.x, da.x, wa.y * da.y), fmaf(wb.x, db.x, wb.y * db.y));
+    const float2 rs = make_float2(rsqrtf(fmaxf(r2.x, 1e-30f)), rsqrtf(fmaxf(r2.y, 1e-30f)));
+    const float2 q = __fmul2_rn(__fmul2_rn(r2, rs), bc2(P.inv_h));
+    const float2 t0 = rsub2(bc2(2.0f), q), u0 = rsub2(bc2(1.0f), q);
+    const float2 t = make_float2(fmaxf(t0.x, 0.0f), fmaxf(t0.y, 0.0f));
+    const float2 u = make_float2(fmaxf(u0.x, 0.0f), fmaxf(u0.y, 0.0f));
+    // -d = t^2 - 4u^2 and -(visc - (P_i/rho_i^2 + P_j/rho_j^2)): both factors of the pair
+    // scalar negated (exact), so no negated register operand is needed
+    const float2 nd = __ffma2_rn(__fmul2_rn(bc2(-4.0f), u), u, __fmul2_rn(t, t));
+    const float2 rho = make_float2(ai.x + aa.x, ai.x + ab.x);
+    const float2 pp = make_float2(ai.y + aa.y, ai.y + ab.y);
+    const float2 den = __fmul2_rn(rho, __fadd2_rn(r2, bc2(P.eps_h2)));
+    const float2 nvisc = __fmul2_rn(__fmul2_rn(bc2(-P.alpha2h), vr),
+                                    make_float2(rcp_approx(den.x), rcp_approx(den.y)));
+    const float2 sc = __fmul2_rn(__fadd2_rn(nvisc, pp), __fmul2_rn(nd, rs));
+    s = __ffma2_rn(bc2(sc.x), da, s);
+    s = __ffma2_rn(bc2(sc.y), db, s);
+}
+
 // masked variant for the cell-scan fallback (candidates may include j == i)
 __device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2 ai, float4 xj,
                                            float2 aj, bool valid, float& sx, float& sy) {
@@ -829,6 +894,9 @@ __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __re
                                            uint2 q0, float4 xi, float2 ai, PV&& pvj, AX&& axj,
                                            float& sx, float& sy) {
     uint2 wn = q0;   // offsets stream from DRAM: keep the next quad's load in flight
+#if SPH_F32X2
+    float2 s = make_float2(sx, sy);
+#endif
     for (int k = 0; k < n; k += 4) {
         const uint2 w = wn;
         nq += P.N;
@@ -838,20 +906,32 @@ __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __re
         const int d0 = quad_offset(w, 0), d1 = quad_offset(w, 1);
         const float4 x0 = pvj(d0), x1 = pvj(d1);
         const float2 a0 = axj(d0), a1 = axj(d1);
+#if SPH_F32X2
+        pair_force2(P, xi, ai, x0, a0, x1, a1, s);
+#else
         pair_force(P, xi, ai, x0, a0, sx, sy);
         pair_force(P, xi, ai, x1, a1, sx, sy);
+#endif
         if (k + 2 < n) {
             const int d2 = quad_offset(w, 2), d3 = quad_offset(w, 3);
             const float4 x2 = pvj(d2), x3 = pvj(d3);
             const float2 a2 = axj(d2), a3 = axj(d3);
+#if SPH_F32X2
+            pair_force2(P, xi, ai, x2, a2, x3, a3, s);
+#else
             pair_force(P, xi, ai, x2, a2, sx, sy);
             pair_force(P, xi, ai, x3, a3, sx, sy);
+#endif
         }
     }
+#if SPH_F32X2
+    sx = s.x;
+    sy = s.y;
+#endif
 }
 
 #ifndef SPH_FORCE_MINB
-#define SPH_FORCE_MINB 6   // 40 registers: occupancy beats the small spill (measured sweep 3..8)
+#define SPH_FORCE_MINB 5   // 48 registers with the packed pair math (sweep 4..6: 5 best, no loop spill)
 #endif
 
 // Body partial accumulators of one thread (reaction force, torque, squared displacement).
