@@ -9,6 +9,9 @@ parity status per function:
   neighbours*           pinned (brute force vs cell list; float32 predicate vs numpy)
   ghosts                pinned (rigidity, rotation special cases, golden G2)
   density               pinned (isolated particle, square-lattice sum, golden G1/G2)
+  density_parts /
+  estimate_gamma1       pinned (completed-lattice identity gamma1 = 1, ghost-doubling halves
+                        it, density consistency, Table 2's gamma1 = 0.5 on the C1 wall layer)
   forces / step         pinned (golden G1/G2, momentum + angular momentum balance,
                         rigid-only closed form, hydrostatic identity, sign tests)
   rollout               pinned (PD gains, ZOH, sampling order vs closed forms)
@@ -62,6 +65,7 @@ def lib():
         L.orc_neighbours.restype = C.c_int64
         L.orc_ghosts.argtypes = [C.c_int, _D, _D, _D, _D]
         L.orc_density.argtypes = [P, C.c_int, _D, C.c_int, _D, _D, _D]
+        L.orc_density_parts.argtypes = [P, C.c_int, _D, C.c_int, _D, _D, _D]
         L.orc_forces.argtypes = [P, C.c_int, _D, _D, _D, _D, C.c_int, _D, _D, _D, _D, _D,
                                  C.POINTER(C.c_double)]
         L.orc_step.argtypes = [P, C.c_int, _D, _D, C.c_int, _D, _D, _D, C.c_double, C.c_int,
@@ -145,6 +149,36 @@ def density(sp, pos, gpos):
     P = np.zeros(n)
     lib().orc_density(C.byref(params(sp)), n, pos, gpos.shape[0], gpos, rho, P)
     return rho, P
+
+
+def density_parts(sp, pos, gpos):
+    """(sf, sg): the fluid (self included) and ghost kernel sums of Eq. density_update
+    (P:180-182), rho_i = m (sf_i + gamma1 sg_i)."""
+    pos = _c(pos)
+    gpos = _c(gpos).reshape(-1, 2)
+    n = pos.shape[0]
+    sf = np.zeros(n)
+    sg = np.zeros(n)
+    lib().orc_density_parts(C.byref(params(sp)), n, pos, gpos.shape[0], gpos, sf, sg)
+    return sf, sg
+
+
+def estimate_gamma1(sp, pos, gpos, rho_target=None):
+    """Analytic estimate of the wall correcting factor, Eq. gamma1:
+        gamma1_i = (rho_i / m_i - sum_f W_i,f) / sum_g W_i,g
+    with rho_i := rho_target (default rho0, the density the wall layer should have) and the
+    printed denominator subscript i_b read as the ghost sum (reading G1).  Returns
+    (gamma1_wall, gamma1_i, sf, sg): gamma1_i is NaN where no ghost is within 2h, and the single
+    calibrated value gamma1_wall applies the same equation to the whole wall layer (the sums of
+    its numerators and denominators over the particles with sg > 0: the gamma1 that gives the
+    layer its target mass, reading G1)."""
+    sf, sg = density_parts(sp, pos, gpos)
+    rt = (sp.rho0 if rho_target is None else rho_target) / sp.mass
+    w = sg > 0.0
+    g = np.full(sf.shape, np.nan)
+    g[w] = (rt - sf[w]) / sg[w]
+    wall = float((rt - sf[w]).sum() / sg[w].sum()) if w.any() else float("nan")
+    return wall, g, sf, sg
 
 
 def forces(sp, pos, vel, rho, P, gpos, gvel, body):

@@ -246,6 +246,40 @@ void orc_ghosts(int ng, const double* gB, const double* body, double* gpos, doub
 /*   rho_i = m_i ( sum_{i_f} W_cb(r_i,i_f) + gamma1 sum_{i_g} W_cb(r_i,i_g) ),            */
 /*   the fluid sum includes i itself ("all particles"), cubic kernel.       */
 /* ------------------------------------------------------------------------------------ */
+void orc_density_parts(const orc_params* p, int n, const double* pos, int ng, const double* gpos,
+                       double* sf, double* sg) {
+    /* the two sums of Eq. density_update, formed as in orc_density below with the
+     * mass and gamma1 factors left out */
+    double H = 2.0 * p->h;
+    grid_t gf, gg;
+    grid_build(&gf, n, pos, H);
+    grid_build(&gg, ng, gpos, H);
+    int cap = 64;
+    int* buf = (int*)malloc(sizeof(int) * (size_t)cap);
+    for (int i = 0; i < n; i++) {
+        double xi = pos[2 * i], yi = pos[2 * i + 1];
+        double f = orc_W_cb(p, 0.0); /* self term */
+        int m = grid_query(&gf, pos, xi, yi, H * H, i, &buf, &cap);
+        for (int t = 0; t < m; t++) {
+            int j = buf[t];
+            double dx = xi - pos[2 * j], dy = yi - pos[2 * j + 1];
+            f += orc_W_cb(p, sqrt(dx * dx + dy * dy));
+        }
+        double g = 0.0;
+        m = grid_query(&gg, gpos, xi, yi, H * H, -1, &buf, &cap);
+        for (int t = 0; t < m; t++) {
+            int k = buf[t];
+            double dx = xi - gpos[2 * k], dy = yi - gpos[2 * k + 1];
+            g += orc_W_cb(p, sqrt(dx * dx + dy * dy));
+        }
+        sf[i] = f;
+        sg[i] = g;
+    }
+    free(buf);
+    grid_free(&gf);
+    grid_free(&gg);
+}
+
 void orc_density(const orc_params* p, int n, const double* pos, int ng, const double* gpos,
                  double* rho, double* P) {
     double H = 2.0 * p->h;

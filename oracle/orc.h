@@ -40,6 +40,11 @@ int64_t orc_neighbours(const orc_params* p, int n, const double* pos, int use_ce
 void orc_ghosts(int ng, const double* gB, const double* body, double* gpos, double* gvel);
 
 /* Eqs. density_update + EOS.  rho[n], P[n]. */
+/* The two kernel sums of Eq. density_update, in units of W_cb (m = 1, gamma1 = 1
+ * kept apart): sf[i] = sum over fluid j (self included) W_cb(r_ij), sg[i] = sum over ghosts
+ * W_cb(r_ig).  Ingredients of the gamma1 estimate, Eq. gamma1. */
+void orc_density_parts(const orc_params* p, int n, const double* pos, int ng, const double* gpos,
+                       double* sf, double* sg);
 void orc_density(const orc_params* p, int n, const double* pos, int ng, const double* gpos,
                  double* rho, double* P);
 
