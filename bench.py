@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN", "P0", "C2CL"],
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN", "P0", "C2CL", "SETTLE"],
                     help="LIN: linearization (SURVEY 8(f) f1) of the paper's P0 tank; P0: the paper's "
                          "Table 3 benchmark (30 s closed loop); C2CL: the same manoeuvre on the C2 tank (configs[1]); "
                          "none of them is the north-star line")
@@ -655,15 +655,91 @@ def run_p0(a, closed_loop_c2=False):
     print(json.dumps(line), flush=True)
 
 
+def run_settle(a):
+    """--workload SETTLE: the paper's initialisation -- fluid
+    spawned at random in the C2 tank, damped settle (reading A17, body pinned) for 3 s of model
+    time until the velocities vanish -- then the gamma1 estimate (Eq. gamma1) of the
+    settled wall layer.  Both device-timed on the context stream; the oracle's settle of the
+    same spawn timed beside it on a bounded sample."""
+    import torch
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    from paper_2604_12505_b200 import SphContext
+    t = si.random_spawn(4.0, seed=0)
+    sp = t.params
+    n = int(round(3.0 / sp.dt))
+    damp = math.exp(-10.0 * sp.dt)
+    ctx = SphContext(sp, t.pv32(), t.ghost_b, n_rollouts=1, rebin_every=0, skin=a.skin * sp.h,
+                     device=local)
+    ctx.settle(damp, 8)                                   # warm-up (first-call allocations)
+    ctx.set_state(t.pv32(), rollout=0, body=np.zeros(6))
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record(ctx.stream)
+    ctx.settle(damp, n)
+    ev[1].record(ctx.stream)
+    wall, g, sums = ctx.gamma1_estimate(0)
+    ev[2].record(ctx.stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    settle_s = ev[0].elapsed_time(ev[1]) / 1e3
+    g1_ms = ev[1].elapsed_time(ev[2])
+    st = ctx.get_status()[0]
+    pv = ctx.get_particles(0)
+    n_steps, n_reb = ctx.counters()
+    lps = ctx.launches_per_substep()
+    ctx.close()
+    r = np.hypot(pv[:, 0], pv[:, 1])
+    cpu = None
+    if not a.no_cpu_baseline:
+        import oracle as O
+        s = O.State.from_tank(t)
+        m = 400                                                # a bounded sample, 1 thread
+        c0 = time.perf_counter()
+        s.step(n=m, damping=damp, pin_body=True)
+        dt = time.perf_counter() - c0
+        cpu = {"value": dt * n / m, "unit": "s", "cores": 1, "kind": "oracle",
+               "sample": f"first {m} of {n} settle substeps of the same spawn, float64 C oracle, "
+                         f"1 thread, {dt:.1f} s, extrapolated to the 3 s settle"}
+    line = {
+        "metric": "random-spawn damped settle of the C2 tank, 3 s model time (P:323-324)",
+        "value": settle_s, "unit": "s", "n_gpus": 1, "steps": 1, "warmup": 1,
+        "ms_per_step": settle_s * 1e3, "higher_is_better": False, "scaling": "none",
+        "vs_baseline": None, "dtype": "f32 (body f64)",
+        "data": "synthetic (uniform random spawn, Philox seed 0, C2 fill region)",
+        "config": {"workload": f"SETTLE: C2 tank ({t.n_fluid} fluid + {t.n_ghost} ghosts), "
+                               f"{n} damped substeps + gamma1 estimate",
+                   "substeps": n, "us_per_substep": settle_s * 1e6 / n,
+                   "particle_updates_per_s": t.n_fluid * n / settle_s,
+                   "substeps_per_rebuild": float(n_steps[0] / max(int(n_reb[0]), 1)),
+                   "status": int(st[0]), "max_speed_end": float(np.abs(pv[:, 2:]).max()),
+                   "max_r_over_R": float(r.max() / sp.R),
+                   "gamma1_estimate_wall": wall, "gamma1_estimate_ms": g1_ms,
+                   "gamma1_wall_particles": int(np.isfinite(g).sum()),
+                   "path": "cooperative tick" if lps == 0 else f"{lps} kernels per substep"},
+        "gpu_launches": (1 if lps == 0 else n * lps) + 2,
+        "clocks": ck,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     a = parse()
     if a.skin is None:
-        a.skin = 0.5 if a.workload in ("P0", "C2CL") else 0.15
+        a.skin = 0.5 if a.workload in ("P0", "C2CL", "SETTLE") else 0.15
     if a.workload == "LIN":
         run_linearize(a)
         return
     if a.workload in ("P0", "C2CL"):
         run_p0(a, closed_loop_c2=a.workload == "C2CL")
+        return
+    if a.workload == "SETTLE":
+        run_settle(a)
         return
     if a.impl == "reference":
         run_reference(a)

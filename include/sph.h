@@ -72,7 +72,7 @@ typedef struct {
 
 /* Time stepping.  rebin_every = 1 rebuilds the cell list and the neighbour lists every
  * substep; 0 rebuilds them only when a particle may have moved (relative to the body
- * translation) by 0.45 skin since the last rebuild.  Cells and lists are then 2h + skin wide
+ * translation) by 0.49 skin since the last rebuild.  Cells and lists are then 2h + skin wide
  * (Verlet skin); the float32 predicate |x_i - x_j|^2 < (2h)^2 is re-applied to the current
  * positions every substep, so the neighbour sets are exact in both modes. */
 typedef struct {
@@ -211,6 +211,21 @@ sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr
  * pointers if ptr_on_device, else host (copied in / out; the call synchronises).
  * Errors: SPH_EINVAL bad arguments; SPH_ECUDA solver failure (message in sph_last_error). */
 sph_status sph_eigenvalues(sph_ctx* ctx, int n, double* A, double* w, int ptr_on_device);
+
+/* Analytic estimate of the wall correcting factor gamma1 (Eq. gamma1; SURVEY 8(f)
+ * f4) on rollout `rollout`'s current state:
+ *   gamma1_i = (rho_target / m - sum_f W_cb(r_if)) / sum_g W_cb(r_ig)
+ * (printed denominator subscript i_b read as the ghost sum, reading G1).  Sums as in Eq.
+ * density_update, self term included in the fluid sum, float32 support predicate
+ * (reading A19) over every fluid particle and ghost (O(n_fluid^2) brute force: a calibration
+ * utility, not a per-step call).  Outputs (host pointers, each may be NULL; the call
+ * synchronises): gamma1_i [n_fluid] float32 in canonical id order (NaN where no ghost lies within
+ * 2h); sums [n_fluid][2] float32 = (sum_f W, sum_g W) / (C/h^2); gamma1_wall = the estimate of
+ * the whole wall layer, sum of the numerators over sum of the denominators of the particles with
+ * a ghost within 2h (float64; NaN if there is none).
+ * Errors: SPH_EINVAL bad arguments (rho_target <= 0); SPH_ECUDA launch / allocation failure. */
+sph_status sph_gamma1_estimate(sph_ctx* ctx, int rollout, double rho_target, float* gamma1_i,
+                               float* sums, double* gamma1_wall);
 
 /* Per-rollout counters (host arrays of B, nullable): substeps taken and cell-list / neighbour-
  * list rebuilds performed (with rebin_every = 0 rebuilds happen only when the displacement

@@ -74,6 +74,7 @@ def lib():
             "sph_launches_per_substep": (i32, [vp]),
             "sph_jacobian": (i32, [vp, i32, vp, vp, i32]),
             "sph_eigenvalues": (i32, [vp, i32, vp, vp, i32]),
+            "sph_gamma1_estimate": (i32, [vp, i32, dbl, vp, vp, vp]),
             "sph_get_counters": (i32, [vp, vp, vp]),
             "sph_get_sizes": (None, [vp, vp, vp, vp, vp]),
             "sph_last_error": (C.c_char_p, [vp]),
@@ -93,6 +94,7 @@ def exported_symbols():
             "sph_get_body_state", "sph_settle", "sph_get_status", "sph_debug_cells",
             "sph_debug_neighbours", "sph_profile_substeps", "sph_set_live_timing", "sph_get_live_timing",
             "sph_launches_per_substep", "sph_get_counters", "sph_jacobian", "sph_eigenvalues",
+            "sph_gamma1_estimate",
             "sph_get_sizes", "sph_last_error", "sph_destroy"]
 
 
@@ -347,6 +349,20 @@ class SphContext:
         self._check(self.L.sph_eigenvalues(self.ctx, n, a.ctypes.data, w.ctypes.data, 0),
                     "sph_eigenvalues")
         return w[:, 0] + 1j * w[:, 1]
+
+    def gamma1_estimate(self, rollout: int = 0, rho_target=None):
+        """Analytic gamma1 estimate (Eq. gamma1; sph_gamma1_estimate) on the current
+        state of ``rollout``: (gamma1_wall, gamma1_i [N] canonical order, NaN away from the
+        wall, sums [N, 2] = (sum_f W, sum_g W) in units of C/h^2)."""
+        n = self.N
+        g = np.empty(n, np.float32)
+        sums = np.empty((n, 2), np.float32)
+        wall = C.c_double(0.0)
+        rt = float(self.fp.rho0 if rho_target is None else rho_target)
+        self._check(self.L.sph_gamma1_estimate(self.ctx, int(rollout), rt, g.ctypes.data,
+                                               sums.ctypes.data, C.byref(wall)),
+                    "sph_gamma1_estimate")
+        return wall.value, g, sums
 
     def counters(self):
         steps = np.zeros(self.B, np.int64)

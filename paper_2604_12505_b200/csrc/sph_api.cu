@@ -16,6 +16,7 @@
 #include "../../include/sph.h"
 #include "sph_kernels.cuh"
 #include "sph_jac.cuh"
+#include "sph_calib.cuh"
 
 using namespace sph;
 
@@ -65,6 +66,7 @@ struct sph_ctx {
     void* eig_dbuf = nullptr;
     size_t eig_dbytes = 0;
     std::vector<char> eig_hbuf;
+    double* g1_buf = nullptr;   // sph_gamma1_estimate: (numerator, denominator) sums
 };
 
 // event slots of one sampled substep
@@ -750,6 +752,34 @@ sph_status sph_get_particles(sph_ctx* ctx, int rollout, float* fluid_pv, float* 
     return SPH_OK;
 }
 
+sph_status sph_gamma1_estimate(sph_ctx* ctx, int rollout, double rho_target, float* gamma1_i,
+                               float* sums, double* gamma1_wall) {
+    if (!ctx) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    if (rollout < 0 || rollout >= P.B) return fail(ctx, SPH_EINVAL, "rollout out of range");
+    if (!(rho_target > 0.0)) return fail(ctx, SPH_EINVAL, "rho_target must be > 0");
+    if (gamma1_wall) *gamma1_wall = std::nan("");
+    if (P.N == 0) return SPH_OK;
+    cudaStream_t s = ctx->stream;
+    if (!ctx->g1_buf) CK(cudaMalloc(&ctx->g1_buf, 2 * sizeof(double)));
+    // target density in units of m C / h^2, from the float64 parameters
+    const double wcb = ctx->fp.w_cb_const / (ctx->fp.h * ctx->fp.h);
+    const float rt = (float)(rho_target / (ctx->fp.mass * wcb));
+    float2* parts = reinterpret_cast<float2*>(ctx->D.xfer);   // [N] staging (k_export's)
+    k_gamma1_parts<<<(P.N + G1_T - 1) / G1_T, G1_T, 0, s>>>(P, ctx->D, rollout, rt, parts,
+                                                           ctx->D.xrho);
+    k_gamma1_wall<<<1, 1024, 0, s>>>(P.N, parts, rt, ctx->g1_buf);
+    sph_status st = check_launch(ctx);
+    if (st) return st;
+    double nd[2];
+    if (gamma1_i) CK(cudaMemcpyAsync(gamma1_i, ctx->D.xrho, sizeof(float) * P.N, cudaMemcpyDeviceToHost, s));
+    if (sums) CK(cudaMemcpyAsync(sums, parts, sizeof(float2) * P.N, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(nd, ctx->g1_buf, sizeof(nd), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (gamma1_wall && nd[1] > 0.0) *gamma1_wall = nd[0] / nd[1];
+    return SPH_OK;
+}
+
 sph_status sph_get_ghosts(sph_ctx* ctx, int rollout, float* ghost_pv) {
     if (!ctx || !ghost_pv) return SPH_EINVAL;
     const DevParams& P = ctx->P;
@@ -1109,6 +1139,7 @@ sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr
     if (ctx->jac_bytes < off) {   // grow the cached scratch (kept for the next call)
         CK(cudaStreamSynchronize(s));
         if (ctx->jac_buf) cudaFree(ctx->jac_buf);
+    if (ctx->g1_buf) cudaFree(ctx->g1_buf);
         ctx->jac_buf = nullptr;
         ctx->jac_bytes = 0;
         CK(cudaMalloc(&ctx->jac_buf, off));

@@ -190,6 +190,30 @@ def moving_tank(ell: float = 1.0, seed: int = 1, jitter: float = 0.05, vel: floa
     return t.snapped()
 
 
+def random_spawn(ell: float = 1.0, seed: int = 0, fill: float | None = 0.5,
+                 n_first: int | None = None, **over) -> Tank:
+    """Random-spawn initial state of the paper's settling procedure ("fuel particles
+    are spawned randomly distributed within the tank and allowed to evolve without external
+    actuation until their velocities converge to zero"): as many particles as make_tank(ell,
+    fill, n_first) places (so the fluid mass is the same), uniformly distributed (Philox(seed),
+    rejection sampling) over the region the lattice occupies -- |p| <= R - s/2 and, with a fill
+    level, y <= y_f; with ``n_first`` (the P0 tank) below the level of the last lattice row.
+    At rest, body at the origin; snapped to float32."""
+    t = make_tank(ell, fill=fill, n_first=n_first, **over)
+    p = t.params
+    n = t.n_fluid
+    y_top = _segment_level(fill, p.R) if n_first is None and fill is not None else \
+        float(t.pos[:, 1].max()) + 0.5 * p.spacing
+    rng = np.random.Generator(np.random.Philox(seed))
+    pts = np.zeros((0, 2))
+    while pts.shape[0] < n:
+        c = rng.uniform(-p.R, p.R, size=(4 * n, 2))
+        ok = (np.hypot(c[:, 0], c[:, 1]) <= p.R - 0.5 * p.spacing) & (c[:, 1] <= y_top)
+        pts = np.concatenate([pts, c[ok]])
+    pos = pts[:n]
+    return Tank(p, pos, np.zeros_like(pos), t.ghost_b).snapped()
+
+
 def random_tank(n_fluid: int, n_ghost: int, seed: int, h: float = H_PAPER, R: float = 0.03,
                 vel_scale: float = 0.02, **over) -> Tank:
     """Small random (non-lattice) tank for parity edge cases: uniform points in the disk."""
