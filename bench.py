@@ -49,7 +49,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN", "P0", "C2CL", "SETTLE"],
+    ap.add_argument("--lpv-seqs", type=int, default=1,
+                    help="LPV workload: training sequences (the paper: 1)")
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN", "P0", "C2CL", "SETTLE", "LPV"],
                     help="LIN: linearization (SURVEY 8(f) f1) of the paper's P0 tank; P0: the paper's "
                          "Table 3 benchmark (30 s closed loop); C2CL: the same manoeuvre on the C2 tank (configs[1]); "
                          "none of them is the north-star line")
@@ -728,6 +730,113 @@ def run_settle(a):
     print(json.dumps(line), flush=True)
 
 
+def run_lpv(a):
+    """--workload LPV: the paper's surrogate identification on data
+    the simulator generates.  Dataset: the P0 tank (GPU damped settle), the open-loop excitation
+    train of P:430-432 (2200 samples, multisine [0, 2) Hz + pulses) -> velocities (rd_x, rd_y,
+    thd).  Identification (timed, wall clock with the device synchronised): LTI
+    initialisation (reading LPV2), 8 LPV restarts x (2000 Adam + up to 6000 L-BFGS iterations),
+    best training BFR.  Validation: the closed-loop manoeuvre profiles 1 and 2 on the SPH
+    simulator, their applied inputs replayed through the surrogate (open loop, reading LPV5)."""
+    import torch
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    from paper_2604_12505_b200 import SphContext
+    from paper_2604_12505_b200 import lpv as LP
+    t = si.make_tank(1.0, n_first=666)
+    sp = t.params
+    Ts = sp.dt * sp.n_sub
+    ctx = SphContext(sp, t.pv32(), t.ghost_b, n_rollouts=1, rebin_every=0, skin=0.5 * sp.h,
+                     device=local)
+    ctx.settle(math.exp(-10.0 * sp.dt), int(2.0 / sp.dt))
+    pv0 = ctx.get_particles(0)
+    K = 2200
+    S = int(a.lpv_seqs)
+    us, ys = [], []
+    g0 = time.perf_counter()
+    for sidx in range(S):
+        ctx.set_state(pv0, rollout=0, body=np.zeros(6))
+        u = si.excitation(3000 + sidx, K=K).astype(np.float32)[None]
+        y, _ = ctx.rollout(u)
+        us.append(u[0].astype(np.float64))
+        ys.append(np.asarray(y)[0, :, 3:6].astype(np.float64))
+    gen_s = time.perf_counter() - g0
+    val = {}
+    for pid in (1, 2):
+        Kv = int(round(30.0 / Ts))
+        uv, th = si.profile(pid, Kv)
+        ctx.set_state(pv0, rollout=0, body=np.zeros(6))
+        yv, ua = ctx.rollout(uv.astype(np.float32)[None], theta_ref=th.astype(np.float32)[None],
+                             Kp=sp.Kp, Kd=sp.Kd)
+        val[pid] = (np.asarray(ua)[0].astype(np.float64), np.asarray(yv)[0].astype(np.float64))
+    ctx.close()
+    un, yn, (um, usd, ym, ysd) = LP.normalise(us, ys)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    c0 = time.perf_counter()
+    res = LP.identify(un, yn, restarts=8, adam_iters=2000, lbfgs_iters=6000, lti_iters=2000,
+                      seed=0, lr=1e-3, device=local)
+    torch.cuda.synchronize()
+    train_s = time.perf_counter() - c0
+    ck = clocks.stop()
+    # validation: replay the closed-loop runs' applied inputs through the surrogate
+    vbfr, sim_ms = {}, {}
+    for pid, (ua, yv) in val.items():
+        ua_n = ((ua - um) / usd).astype(np.float32)
+        prob = LP.LpvProblem(1, [ua_n], None, device=local)
+        P = np.concatenate([res["theta"], np.zeros(4)])[None]
+        prob.set_params(P)
+        prob.simulate()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        yh = prob.simulate()
+        e1.record()
+        torch.cuda.synchronize()
+        sim_ms[pid] = e0.elapsed_time(e1)
+        vel = yh[0, 0].cpu().numpy().astype(np.float64) * ysd + ym
+        pos = LP.augment_positions(vel, Ts)
+        b_pos = LP.bfr(yv[:, 0:3], pos)
+        b_vel = LP.bfr(yv[:, 3:6], vel)
+        vbfr[pid] = dict(zip(["r_x", "r_y", "theta", "rd_x", "rd_y", "thd"],
+                             [round(float(v), 2) for v in np.concatenate([b_pos, b_vel])]))
+    cpu = None
+    if not a.no_cpu_baseline:
+        from oracle import lpv as OL
+        th0 = np.concatenate([res["theta"]])
+        x0 = np.zeros((S, 4))
+        c1 = time.perf_counter()
+        OL.objective(th0, x0, [u.astype(np.float64) for u in un], [y.astype(np.float64) for y in yn])
+        one = time.perf_counter() - c1
+        n_obj = res["n_evals"] * (2 * (LP.NT + 4 * S) + 1)
+        cpu = {"value": one * n_obj, "unit": "s", "cores": 1, "kind": "oracle",
+               "sample": f"1 objective evaluation ({S} x {K} samples, float64 numpy oracle, 1 thread, "
+                         f"{one * 1e3:.0f} ms) x {n_obj} (the {res['n_evals']} gradient evaluations "
+                         f"of the run by central differences over {LP.NT + 4 * S} parameters)"}
+    line = {
+        "metric": "LPV surrogate identification time: LTI init + 8 restarts x (2000 Adam + <= 6000 L-BFGS) (P:441-446)",
+        "value": train_s, "unit": "s", "n_gpus": 1, "steps": 1, "warmup": 0,
+        "ms_per_step": train_s * 1e3, "higher_is_better": False, "scaling": "none",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (SPH simulator: P0 tank, open-loop excitation train, {S} x {K} samples)",
+        "config": {"workload": f"LPV: n_x 4, n_u 3, n_y 3, n_p 1, theta 137 + x0; {S} sequence(s) x {K} samples",
+                   "dataset_generation_s": gen_s, "n_evals": res["n_evals"],
+                   "ms_per_eval": train_s * 1e3 / max(res["n_evals"] / 8, 1),
+                   "train_bfr_lti": round(res["bfr_lti"], 2), "train_bfr_lpv": round(res["bfr"], 2),
+                   "train_bfr_restarts": [round(v, 2) for v in res["bfr_all"]],
+                   "validation_bfr_replay": vbfr, "surrogate_sim_ms": sim_ms,
+                   "paper": {"train_s": 48.0, "bfr_lti": 82.16, "bfr_lpv": 98.66,
+                             "surrogate_sim_s": {"1": 0.0242, "2": 0.0056},
+                             "hardware": "RTX 2000 Ada laptop GPU, JAX (P:391, P:446)"}},
+        "gpu_launches": None,
+        "clocks": ck,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     a = parse()
     if a.skin is None:
@@ -740,6 +849,9 @@ def main():
         return
     if a.workload == "SETTLE":
         run_settle(a)
+        return
+    if a.workload == "LPV":
+        run_lpv(a)
         return
     if a.impl == "reference":
         run_reference(a)

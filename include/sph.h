@@ -227,6 +227,37 @@ sph_status sph_eigenvalues(sph_ctx* ctx, int n, double* A, double* w, int ptr_on
 sph_status sph_gamma1_estimate(sph_ctx* ctx, int rollout, double rho_target, float* gamma1_i,
                                float* sums, double* gamma1_wall);
 
+/* ---- LPV surrogate identification (paper Sec. 4, Sec. 5.3
+ * P:423-446).  Context-free calls on DEVICE pointers, enqueued on `stream` (a cudaStream_t, NULL =
+ * the legacy default stream); they do not synchronise.
+ * Model: self-scheduled LPV-SS with affine scheduling (Eqs. surrogate_form, LPVparametrization),
+ * n_x = 4, n_u = 3, n_y = 3, n_p = 1, D = 0, scheduling map [x; u] -> 4 tanh -> 4 tanh -> 1
+ * (P:438-440).  Parameters of restart r: params[r] = [theta (SPH_LPV_NTHETA), x0 (S x 4)], float64,
+ * theta = A0 (4x4) B0 (4x3) C0 (3x4) A1 (4x4) B1 (4x3) C1 (3x4) W1 (4x7) b1 (4) W2 (4x4) b2 (4)
+ * W3 (1x4) b3 (1), row-major (137 values: SPEC's count; the paper prints 130, reading LPV1). */
+#define SPH_LPV_NTHETA 137
+
+/* Device scratch bytes of sph_lpv_eval for R restarts, S sequences of K samples (0 on bad sizes). */
+size_t sph_lpv_scratch_bytes(int R, int S, int K);
+
+/* Objective and gradient of Eq. surrogate_optimization for R parameter sets at once:
+ *   F_r = 1/S sum_s 1/K sum_k ||y_sk - y^_sk||^2 + sigma2/2 ||theta_r||^2
+ *         + sigmax/2 sum_s ||x0_rs||^2                  (Eqs. pem, regularization; reading LPV3)
+ * u: [S][K][3], y: [S][K][3] float32 (the scaled, normalised dataset); obj [R], grad [R][137 + 4S]
+ * (same layout as params; reverse-mode gradient), yhat [R][S][K][3] float32: each may be NULL
+ * (y may be NULL when obj and grad are).  scratch: >= sph_lpv_scratch_bytes(R, S, K) device bytes.
+ * Errors: SPH_EINVAL bad sizes / pointers / weights; SPH_ECUDA launch failure. */
+sph_status sph_lpv_eval(int R, int S, int K, const double* params, const float* u, const float* y,
+                        double sigma2, double sigmax, double* obj, double* grad, float* yhat,
+                        void* scratch, size_t scratch_bytes, void* stream);
+
+/* One Adam step on R x n float64 parameters in place: m, v moment buffers (zero at t = 1),
+ * t >= 1 the step number (bias correction), mask [n] uint8 or NULL: 0 freezes that parameter of
+ * every restart.  Errors: SPH_EINVAL bad arguments; SPH_ECUDA launch failure. */
+sph_status sph_lpv_adam(int R, int n, double* w, const double* g, double* m, double* v, double lr,
+                        double beta1, double beta2, double eps, int t, const uint8_t* mask,
+                        void* stream);
+
 /* Per-rollout counters (host arrays of B, nullable): substeps taken and cell-list / neighbour-
  * list rebuilds performed (with rebin_every = 0 rebuilds happen only when the displacement
  * bound requires them). */

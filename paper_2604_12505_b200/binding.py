@@ -75,6 +75,9 @@ def lib():
             "sph_jacobian": (i32, [vp, i32, vp, vp, i32]),
             "sph_eigenvalues": (i32, [vp, i32, vp, vp, i32]),
             "sph_gamma1_estimate": (i32, [vp, i32, dbl, vp, vp, vp]),
+            "sph_lpv_scratch_bytes": (C.c_size_t, [i32, i32, i32]),
+            "sph_lpv_eval": (i32, [i32, i32, i32, vp, vp, vp, dbl, dbl, vp, vp, vp, vp, C.c_size_t, vp]),
+            "sph_lpv_adam": (i32, [i32, i32, vp, vp, vp, vp, dbl, dbl, dbl, dbl, i32, vp, vp]),
             "sph_get_counters": (i32, [vp, vp, vp]),
             "sph_get_sizes": (None, [vp, vp, vp, vp, vp]),
             "sph_last_error": (C.c_char_p, [vp]),
@@ -94,7 +97,7 @@ def exported_symbols():
             "sph_get_body_state", "sph_settle", "sph_get_status", "sph_debug_cells",
             "sph_debug_neighbours", "sph_profile_substeps", "sph_set_live_timing", "sph_get_live_timing",
             "sph_launches_per_substep", "sph_get_counters", "sph_jacobian", "sph_eigenvalues",
-            "sph_gamma1_estimate",
+            "sph_gamma1_estimate", "sph_lpv_scratch_bytes", "sph_lpv_eval", "sph_lpv_adam",
             "sph_get_sizes", "sph_last_error", "sph_destroy"]
 
 
