@@ -35,6 +35,7 @@ static_assert(NT == SPH_LPV_NTHETA, "parameter layout");
 constexpr int LPV_T = 32;
 constexpr int CH = LPV_T / 4;
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int REC = 4 * NX + 1;   // per step and chain: x, h1, h2, y^ (one per lane), p
 
 __device__ __forceinline__ double q4sum(double v) {
     v += __shfl_xor_sync(FULL, v, 1);
@@ -136,56 +137,24 @@ __global__ void __launch_bounds__(LPV_T) k_lpv(int R, int S, int K, const double
         const float* ys = y ? y + (size_t)s * K * NY : nullptr;
         double xq = x0[(size_t)s * NX + q];
         double J = 0.0;
+        // forward sweep; u_k and y_k are loaded one step ahead (their L2 latency would otherwise
+        // sit on the chain), the step record (x, h1, h2, y^, p) is kept for the backward sweep
+        double un[NU], yn = 0.0;
+#pragma unroll
+        for (int j = 0; j < NU; ++j) un[j] = K > 0 ? (double)us[j] : 0.0;
+        if (ys && q < NY && K > 0) yn = (double)ys[q];
         for (int k = 0; k < K; ++k) {
             double x[NX], uk[NU], h1[NH];
 #pragma unroll
+            for (int j = 0; j < NU; ++j) uk[j] = un[j];
+            const double yk = yn;
+            if (k + 1 < K) {
+#pragma unroll
+                for (int j = 0; j < NU; ++j) un[j] = (double)us[(size_t)(k + 1) * NU + j];
+                if (ys && q < NY) yn = (double)ys[(size_t)(k + 1) * NY + q];
+            }
+#pragma unroll
             for (int j = 0; j < NX; ++j) x[j] = q4get(xq, j);
-            if (want_grad && act) xs[((size_t)k * RS + rs) * NX + q] = xq;
-#pragma unroll
-            for (int j = 0; j < NU; ++j) uk[j] = (double)us[(size_t)k * NU + j];
-            double a = bb1;
-#pragma unroll
-            for (int j = 0; j < NX; ++j) a = fma(w1[j], x[j], a);
-#pragma unroll
-            for (int j = 0; j < NU; ++j) a = fma(w1[NX + j], uk[j], a);
-            const double h1q = tanh_d(a);
-#pragma unroll
-            for (int j = 0; j < NH; ++j) h1[j] = q4get(h1q, j);
-            double a2 = bb2;
-#pragma unroll
-            for (int j = 0; j < NH; ++j) a2 = fma(w2[j], h1[j], a2);
-            const double p = q4sum(w3 * tanh_d(a2)) + bb3;
-            double yq = 0.0, xn = 0.0;
-#pragma unroll
-            for (int j = 0; j < NX; ++j) {
-                yq = fma(fma(p, c1[j], c0[j]), x[j], yq);
-                xn = fma(fma(p, a1[j], a0[j]), x[j], xn);
-            }
-#pragma unroll
-            for (int j = 0; j < NU; ++j) xn = fma(fma(p, b1[j], b0[j]), uk[j], xn);
-            if (q < NY) {
-                if (yhat && act) yhat[(rs * K + k) * NY + q] = (float)yq;
-                if (ys) {
-                    const double e = (double)ys[(size_t)k * NY + q] - yq;
-                    J = fma(e, e, J);
-                }
-            }
-            xq = xn;
-        }
-        J = q4sum(J);
-        if (ys && act && q == 0) jpart[rs] = K > 0 ? J / K : 0.0;
-        if (!want_grad) continue;
-        double ga0[NX] = {}, ga1[NX] = {}, gb0[NU] = {}, gb1[NU] = {}, gc0[NX] = {}, gc1[NX] = {};
-        double gw1[NZ] = {}, gw2[NH] = {};
-        double gbb1 = 0.0, gbb2 = 0.0, gw3 = 0.0, gbb3 = 0.0;
-        double lam[NX] = {0.0, 0.0, 0.0, 0.0};       // dF/dx_{k+1}, every lane holds all of it
-        for (int k = K - 1; k >= 0; --k) {
-            double x[NX], uk[NU], h1[NH];
-            const double* xp = xs + ((size_t)k * RS + rs) * NX;
-#pragma unroll
-            for (int j = 0; j < NX; ++j) x[j] = xp[j];
-#pragma unroll
-            for (int j = 0; j < NU; ++j) uk[j] = (double)us[(size_t)k * NU + j];
             double a = bb1;
 #pragma unroll
             for (int j = 0; j < NX; ++j) a = fma(w1[j], x[j], a);
@@ -199,10 +168,68 @@ __global__ void __launch_bounds__(LPV_T) k_lpv(int R, int S, int K, const double
             for (int j = 0; j < NH; ++j) a2 = fma(w2[j], h1[j], a2);
             const double h2q = tanh_d(a2);
             const double p = q4sum(w3 * h2q) + bb3;
-            double yq = 0.0;
+            double yq = 0.0, xn = 0.0;
 #pragma unroll
-            for (int j = 0; j < NX; ++j) yq = fma(fma(p, c1[j], c0[j]), x[j], yq);
-            const double dyq = q < NY ? cc * (yq - (double)ys[(size_t)k * NY + q]) : 0.0;
+            for (int j = 0; j < NX; ++j) {
+                yq = fma(fma(p, c1[j], c0[j]), x[j], yq);
+                xn = fma(fma(p, a1[j], a0[j]), x[j], xn);
+            }
+#pragma unroll
+            for (int j = 0; j < NU; ++j) xn = fma(fma(p, b1[j], b0[j]), uk[j], xn);
+            if (want_grad && act) {
+                double* rec = xs + ((size_t)k * RS + rs) * REC;
+                rec[q] = xq;
+                rec[NX + q] = h1q;
+                rec[2 * NX + q] = h2q;
+                rec[3 * NX + q] = yq;
+                if (q == 0) rec[4 * NX] = p;
+            }
+            if (q < NY) {
+                if (yhat && act) yhat[(rs * K + k) * NY + q] = (float)yq;
+                if (ys) {
+                    const double e = yk - yq;
+                    J = fma(e, e, J);
+                }
+            }
+            xq = xn;
+        }
+        J = q4sum(J);
+        if (ys && act && q == 0) jpart[rs] = K > 0 ? J / K : 0.0;
+        if (!want_grad) continue;
+        double ga0[NX] = {}, ga1[NX] = {}, gb0[NU] = {}, gb1[NU] = {}, gc0[NX] = {}, gc1[NX] = {};
+        double gw1[NZ] = {}, gw2[NH] = {};
+        double gbb1 = 0.0, gbb2 = 0.0, gw3 = 0.0, gbb3 = 0.0;
+        double lam[NX] = {0.0, 0.0, 0.0, 0.0};       // dF/dx_{k+1}, every lane holds all of it
+        // backward sweep over the stored records; record k-1 is loaded while step k runs, so
+        // the chain per step is the adjoint arithmetic alone
+        double nx[NX], nh1[NH], nh2 = 0.0, nyq = 0.0, npp = 0.0, nu[NU], ny = 0.0;
+        auto load = [&](int k) {
+            const double* rec = xs + ((size_t)k * RS + rs) * REC;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {
+                nx[j] = rec[j];
+                nh1[j] = rec[NX + j];
+            }
+            nh2 = rec[2 * NX + q];
+            nyq = rec[3 * NX + q];
+            npp = rec[4 * NX];
+#pragma unroll
+            for (int j = 0; j < NU; ++j) nu[j] = (double)us[(size_t)k * NU + j];
+            ny = q < NY ? (double)ys[(size_t)k * NY + q] : 0.0;
+        };
+        if (K > 0) load(K - 1);
+        for (int k = K - 1; k >= 0; --k) {
+            double x[NX], uk[NU], h1[NH];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {
+                x[j] = nx[j];
+                h1[j] = nh1[j];
+            }
+#pragma unroll
+            for (int j = 0; j < NU; ++j) uk[j] = nu[j];
+            const double h2q = nh2, p = npp, h1q = pick4(h1, q);
+            const double dyq = q < NY ? cc * (nyq - ny) : 0.0;
+            if (k > 0) load(k - 1);
             const double lq = pick4(lam, q);
             double dpp = 0.0;
 #pragma unroll
@@ -310,7 +337,7 @@ extern "C" {
 size_t sph_lpv_scratch_bytes(int R, int S, int K) {
     if (R <= 0 || S <= 0 || K < 0) return 0;
     const size_t RS = (size_t)R * S;
-    return sizeof(double) * (RS * (size_t)K * NX + RS * NT + RS);
+    return sizeof(double) * (RS * (size_t)K * REC + RS * NT + RS);
 }
 
 sph_status sph_lpv_eval(int R, int S, int K, const double* params, const float* u, const float* y,
@@ -323,7 +350,7 @@ sph_status sph_lpv_eval(int R, int S, int K, const double* params, const float* 
     if (K == 0 && grad) return SPH_EINVAL;
     const size_t RS = (size_t)R * S;
     double* xs = static_cast<double*>(scratch);
-    double* gpart = xs + RS * (size_t)K * NX;
+    double* gpart = xs + RS * (size_t)K * REC;
     double* jpart = gpart + RS * NT;
     k_lpv<<<R, LPV_T, 0, static_cast<cudaStream_t>(stream)>>>(R, S, K, params, u, y, sigma2, sigmax,
                                                              obj, grad, yhat, xs, gpart, jpart);

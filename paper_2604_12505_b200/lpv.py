@@ -163,11 +163,11 @@ class LpvProblem:
 
     def lbfgs(self, max_iter, memory=10, tol_grad=1e-9, ftol=2.2e-9, c1=1e-4, max_backtrack=30):
         """L-BFGS ("warm-start a ... L-BFGS scheme") in lockstep over the restarts:
-        two-loop recursion (memory 10) and Armijo backtracking; a restart stops when its
-        gradient norm falls below tol_grad, its relative decrease (f_k - f_k+1) / max(|f_k|,
-        |f_k+1|, 1) falls to ftol (scipy's L-BFGS-B default; "up to" max_iter, reading LPV6) or
-        its line search fails.  Frozen parameters (mask) stay fixed.  Returns the number of
-        objective evaluations."""
+        two-loop recursion (memory 10, vectorised over the restarts) and Armijo backtracking; a
+        restart stops when its gradient norm falls below tol_grad, its relative decrease
+        (f_k - f_k+1) / max(|f_k|, |f_k+1|, 1) falls to ftol (scipy's L-BFGS-B default; "up to"
+        max_iter, reading LPV6) or its line search fails.  Frozen parameters (mask) stay fixed.
+        Returns the number of objective evaluations (launches x restarts)."""
         torch = self.torch
         mk = None if self.mask is None else self.mask.cpu().numpy().astype(bool)
         f, g = self.eval()
@@ -176,40 +176,45 @@ class LpvProblem:
         g = g.cpu().numpy().copy()
         if mk is not None:
             g[:, ~mk] = 0.0
-        R = self.R
-        S_hist = [[] for _ in range(R)]
-        Y_hist = [[] for _ in range(R)]
+        R, n, m = self.R, self.n, int(memory)
+        ar = np.arange(R)
+        Sh = np.zeros((R, m, n))
+        Yh = np.zeros((R, m, n))
+        rh = np.zeros((R, m))
+        cnt = np.zeros(R, np.int64)
+        head = np.zeros(R, np.int64)          # next slot of each restart's circular history
         active = np.ones(R, bool)
         n_eval = 1
         for _ in range(max_iter):
             active &= np.linalg.norm(g, axis=1) > tol_grad
             if not active.any():
                 break
-            d = np.zeros_like(g)
-            for r in np.flatnonzero(active):
-                q = -g[r].copy()
-                al = []
-                for s_, y_ in zip(reversed(S_hist[r]), reversed(Y_hist[r])):
-                    rho = 1.0 / (y_ @ s_)
-                    a = rho * (s_ @ q)
-                    q -= a * y_
-                    al.append((rho, a))
-                if S_hist[r]:
-                    s_, y_ = S_hist[r][-1], Y_hist[r][-1]
-                    q *= (s_ @ y_) / (y_ @ y_)
-                else:
-                    q *= min(1.0, 1.0 / max(np.abs(g[r]).sum(), 1e-300))
-                for (rho, a), s_, y_ in zip(reversed(al), S_hist[r], Y_hist[r]):
-                    b = rho * (y_ @ q)
-                    q += (a - b) * s_
-                d[r] = q
+            q = -g
+            al = np.zeros((R, m))
+            for j in range(m):                                   # newest -> oldest
+                idx = (head - 1 - j) % m
+                v = j < cnt
+                a = np.where(v, rh[ar, idx] * np.einsum("rn,rn->r", Sh[ar, idx], q), 0.0)
+                q = q - a[:, None] * Yh[ar, idx]
+                al[:, j] = a
+            last = (head - 1) % m
+            sy = np.einsum("rn,rn->r", Sh[ar, last], Yh[ar, last])
+            yy = np.einsum("rn,rn->r", Yh[ar, last], Yh[ar, last])
+            g1 = np.maximum(np.abs(g).sum(1), 1e-300)
+            gam = np.where(cnt > 0, sy / np.where(yy > 0, yy, 1.0), np.minimum(1.0, 1.0 / g1))
+            q = q * gam[:, None]
+            for j in reversed(range(m)):                         # oldest -> newest
+                idx = (head - 1 - j) % m
+                v = j < cnt
+                b = rh[ar, idx] * np.einsum("rn,rn->r", Yh[ar, idx], q)
+                q = q + np.where(v, al[:, j] - b, 0.0)[:, None] * Sh[ar, idx]
+            d = np.where(active[:, None], q, 0.0)
             slope = (g * d).sum(1)
             bad = active & (slope >= 0)          # not a descent direction: restart memory
-            for r in np.flatnonzero(bad):
-                S_hist[r].clear()
-                Y_hist[r].clear()
-                d[r] = -g[r] * min(1.0, 1.0 / max(np.abs(g[r]).sum(), 1e-300))
-            slope = (g * d).sum(1)
+            if bad.any():
+                cnt[bad] = 0
+                d[bad] = -g[bad] * np.minimum(1.0, 1.0 / g1[bad])[:, None]
+                slope = (g * d).sum(1)
             step = np.where(active, 1.0, 0.0)
             done = ~active
             xn, fn, gn = x.copy(), f.copy(), g.copy()
@@ -230,15 +235,16 @@ class LpvProblem:
             active &= ~failed
             if mk is not None:
                 gn[:, ~mk] = 0.0
-            for r in np.flatnonzero(active):
-                s_ = xn[r] - x[r]
-                y_ = gn[r] - g[r]
-                if s_ @ y_ > 1e-12 * np.linalg.norm(s_) * np.linalg.norm(y_):
-                    S_hist[r].append(s_)
-                    Y_hist[r].append(y_)
-                    if len(S_hist[r]) > memory:
-                        S_hist[r].pop(0)
-                        Y_hist[r].pop(0)
+            s_ = xn - x
+            y_ = gn - g
+            sy = np.einsum("rn,rn->r", s_, y_)
+            keep = active & (sy > 1e-12 * np.linalg.norm(s_, axis=1) * np.linalg.norm(y_, axis=1))
+            kk = np.flatnonzero(keep)
+            Sh[kk, head[kk]] = s_[kk]
+            Yh[kk, head[kk]] = y_[kk]
+            rh[kk, head[kk]] = 1.0 / sy[kk]
+            head[kk] = (head[kk] + 1) % m
+            cnt[kk] = np.minimum(cnt[kk] + 1, m)
             stalled = active & ((f - fn) <= ftol * np.maximum(np.maximum(np.abs(f), np.abs(fn)), 1.0))
             active &= ~stalled
             x, f, g = xn, fn, gn
