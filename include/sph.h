@@ -227,6 +227,34 @@ sph_status sph_eigenvalues(sph_ctx* ctx, int n, double* A, double* w, int ptr_on
 sph_status sph_gamma1_estimate(sph_ctx* ctx, int rollout, double rho_target, float* gamma1_i,
                                float* sums, double* gamma1_wall);
 
+/* ---- Spatial domain decomposition of one tank ----------------------------
+ * Replicated-data decomposition over W processes (one GPU each): every process holds the whole
+ * tank, sorts it by cell (identically: the rebuild is deterministic) and computes density,
+ * forces and integration only for its slab of the cell-sorted slots, [slot_lo, slot_hi) -- a
+ * band of cell rows.  Per substep three phases, with the caller all-gathering three
+ * caller-owned device buffers between them (NCCL all-gather over NVLink in
+ * paper_2604_12505_b200/parallel.py):
+ *   phase 0: input u (host float[3], NULL: keep), rebuild if due, densities of the owned slots
+ *            -> aux_io[slot] = (rho, P/rho^2)                          (float2 [n_fluid])
+ *   (all-gather aux_io)
+ *   phase 1: forces + symplectic Euler of the owned slots -> state_io[slot] = new (x, y, vx, vy)
+ *            (float4 [n_fluid]) and part_io[warp] = body partials of the owned warps
+ *            (double4 [8 ceil(n_fluid / 256)]: F_x, F_y, T, max displacement^2)
+ *   (all-gather state_io and part_io)
+ *   phase 2: import the gathered state, body reduction (fixed order over every warp) and body
+ *            step, identical on every process.
+ * Every slot's arithmetic is the single-GPU path's, and the body sum runs in the same order, so
+ * the decomposed trajectory is bitwise identical to the undecomposed one.  Requirements: one
+ * rollout; slot_lo and slot_hi multiples of SPH_DD_ALIGN (slot_hi may be n_fluid).  Setting a
+ * domain switches the context to the per-substep kernel path (no cooperative tick) for good.
+ * Slot order: the cell-sorted order of the last rebuild (sph_get_particles returns canonical
+ * order).  Numerical-failure status stays local to the process whose slot failed.
+ * Errors: SPH_EINVAL bad arguments / range; SPH_ECUDA launch failure. */
+#define SPH_DD_ALIGN 1024
+sph_status sph_set_domain(sph_ctx* ctx, int slot_lo, int slot_hi);
+sph_status sph_dd_phase(sph_ctx* ctx, int phase, const float* u, void* aux_io, void* state_io,
+                        void* part_io);
+
 /* ---- LPV surrogate identification (paper Sec. 4, Sec. 5.3
  * P:423-446).  Context-free calls on DEVICE pointers, enqueued on `stream` (a cudaStream_t, NULL =
  * the legacy default stream); they do not synchronise.

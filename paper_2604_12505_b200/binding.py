@@ -75,6 +75,8 @@ def lib():
             "sph_jacobian": (i32, [vp, i32, vp, vp, i32]),
             "sph_eigenvalues": (i32, [vp, i32, vp, vp, i32]),
             "sph_gamma1_estimate": (i32, [vp, i32, dbl, vp, vp, vp]),
+            "sph_set_domain": (i32, [vp, i32, i32]),
+            "sph_dd_phase": (i32, [vp, i32, vp, vp, vp, vp]),
             "sph_lpv_scratch_bytes": (C.c_size_t, [i32, i32, i32]),
             "sph_lpv_eval": (i32, [i32, i32, i32, vp, vp, vp, dbl, dbl, vp, vp, vp, vp, C.c_size_t, vp]),
             "sph_lpv_adam": (i32, [i32, i32, vp, vp, vp, vp, dbl, dbl, dbl, dbl, i32, vp, vp]),
@@ -98,6 +100,7 @@ def exported_symbols():
             "sph_debug_neighbours", "sph_profile_substeps", "sph_set_live_timing", "sph_get_live_timing",
             "sph_launches_per_substep", "sph_get_counters", "sph_jacobian", "sph_eigenvalues",
             "sph_gamma1_estimate", "sph_lpv_scratch_bytes", "sph_lpv_eval", "sph_lpv_adam",
+            "sph_set_domain", "sph_dd_phase",
             "sph_get_sizes", "sph_last_error", "sph_destroy"]
 
 

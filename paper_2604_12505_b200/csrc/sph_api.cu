@@ -155,6 +155,8 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->ntile = std::max(1, (N + TILE - 1) / TILE);
     P->npart = P->ntile * (TILE / 32);
     P->bsplit = P->npart > 8192 ? (P->npart + 511) / 512 : 1;
+    P->own_lo = 0;
+    P->own_n = N;
     P->nscan = (P->ncell + 1 + SCAN_TILE - 1) / SCAN_TILE;
     if ((P->nscan + SCAN_T - 1) / SCAN_T > SCAN_V) return *why = "cell grid too large for the scan", false;
     P->h = (float)h;
@@ -293,11 +295,11 @@ static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding, bo
         k_density_ring<<<dim3(P.nchunk, P.B), SW_T, kDensityRingSmem, s>>>(P, ctx->D, skip_rebuilding);
     else
         switch (P.td) {
-            case 1024: launch_k(pdl, k_density<1024>, dim3(std::max(1, (P.N + 1023) / 1024), P.B), dim3(1024), 0, s, P, ctx->D, skip_rebuilding); break;
-            case 512: launch_k(pdl, k_density<512>, dim3(std::max(1, (P.N + 511) / 512), P.B), dim3(512), 0, s, P, ctx->D, skip_rebuilding); break;
-            case 128: launch_k(pdl, k_density<128>, dim3(std::max(1, (P.N + 127) / 128), P.B), dim3(128), 0, s, P, ctx->D, skip_rebuilding); break;
-            case 64: launch_k(pdl, k_density<64>, dim3(std::max(1, (P.N + 63) / 64), P.B), dim3(64), 0, s, P, ctx->D, skip_rebuilding); break;
-            default: launch_k(pdl, k_density<256>, dim3(std::max(1, (P.N + 255) / 256), P.B), dim3(256), 0, s, P, ctx->D, skip_rebuilding); break;
+            case 1024: launch_k(pdl, k_density<1024>, dim3(std::max(1, (P.own_n + 1023) / 1024), P.B), dim3(1024), 0, s, P, ctx->D, skip_rebuilding); break;
+            case 512: launch_k(pdl, k_density<512>, dim3(std::max(1, (P.own_n + 511) / 512), P.B), dim3(512), 0, s, P, ctx->D, skip_rebuilding); break;
+            case 128: launch_k(pdl, k_density<128>, dim3(std::max(1, (P.own_n + 127) / 128), P.B), dim3(128), 0, s, P, ctx->D, skip_rebuilding); break;
+            case 64: launch_k(pdl, k_density<64>, dim3(std::max(1, (P.own_n + 63) / 64), P.B), dim3(64), 0, s, P, ctx->D, skip_rebuilding); break;
+            default: launch_k(pdl, k_density<256>, dim3(std::max(1, (P.own_n + 255) / 256), P.B), dim3(256), 0, s, P, ctx->D, skip_rebuilding); break;
         }
 }
 
@@ -310,11 +312,11 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
         k_force_ring<<<dim3(P.nchunk, gy), SW_T, kForceRingSmem, s>>>(P, ctx->D, damping, mode);
     else
         switch (P.tf) {
-            case 1024: launch_k(pdl, k_force<1024>, dim3(std::max(1, (P.N + 1023) / 1024), gy), dim3(1024), 0, s, P, ctx->D, damping, mode); break;
-            case 512: launch_k(pdl, k_force<512>, dim3(std::max(1, (P.N + 511) / 512), gy), dim3(512), 0, s, P, ctx->D, damping, mode); break;
-            case 128: launch_k(pdl, k_force<128>, dim3(std::max(1, (P.N + 127) / 128), gy), dim3(128), 0, s, P, ctx->D, damping, mode); break;
-            case 64: launch_k(pdl, k_force<64>, dim3(std::max(1, (P.N + 63) / 64), gy), dim3(64), 0, s, P, ctx->D, damping, mode); break;
-            default: launch_k(pdl, k_force<256>, dim3(std::max(1, (P.N + 255) / 256), gy), dim3(256), 0, s, P, ctx->D, damping, mode); break;
+            case 1024: launch_k(pdl, k_force<1024>, dim3(std::max(1, (P.own_n + 1023) / 1024), gy), dim3(1024), 0, s, P, ctx->D, damping, mode); break;
+            case 512: launch_k(pdl, k_force<512>, dim3(std::max(1, (P.own_n + 511) / 512), gy), dim3(512), 0, s, P, ctx->D, damping, mode); break;
+            case 128: launch_k(pdl, k_force<128>, dim3(std::max(1, (P.own_n + 127) / 128), gy), dim3(128), 0, s, P, ctx->D, damping, mode); break;
+            case 64: launch_k(pdl, k_force<64>, dim3(std::max(1, (P.own_n + 63) / 64), gy), dim3(64), 0, s, P, ctx->D, damping, mode); break;
+            default: launch_k(pdl, k_force<256>, dim3(std::max(1, (P.own_n + 255) / 256), gy), dim3(256), 0, s, P, ctx->D, damping, mode); break;
         }
 }
 
@@ -350,9 +352,9 @@ static void launch_nlist_density(sph_ctx* ctx, cudaStream_t s, bool pdl = false)
     const int gy = std::min(P.B, 64);
     pdl = pdl && ctx->pdl;
     switch (P.tn) {
-        case 256: launch_k(pdl, k_nlist_density<256>, dim3(std::max(1, (P.N + 255) / 256), gy), dim3(256), 0, s, P, ctx->D); break;
-        case 64: launch_k(pdl, k_nlist_density<64>, dim3(std::max(1, (P.N + 63) / 64), gy), dim3(64), 0, s, P, ctx->D); break;
-        default: launch_k(pdl, k_nlist_density<128>, dim3(std::max(1, (P.N + 127) / 128), gy), dim3(128), 0, s, P, ctx->D); break;
+        case 256: launch_k(pdl, k_nlist_density<256>, dim3(std::max(1, (P.own_n + 255) / 256), gy), dim3(256), 0, s, P, ctx->D); break;
+        case 64: launch_k(pdl, k_nlist_density<64>, dim3(std::max(1, (P.own_n + 63) / 64), gy), dim3(64), 0, s, P, ctx->D); break;
+        default: launch_k(pdl, k_nlist_density<128>, dim3(std::max(1, (P.own_n + 127) / 128), gy), dim3(128), 0, s, P, ctx->D); break;
     }
 }
 
@@ -788,6 +790,63 @@ sph_status sph_get_ghosts(sph_ctx* ctx, int rollout, float* ghost_pv) {
     CK(cudaMemcpyAsync(ghost_pv, ctx->D.gst + (size_t)rollout * P.G, sizeof(float4) * P.G, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return SPH_OK;
+}
+
+sph_status sph_set_domain(sph_ctx* ctx, int slot_lo, int slot_hi) {
+    if (!ctx) return SPH_EINVAL;
+    DevParams& P = ctx->P;
+    if (P.B != 1) return fail(ctx, SPH_EINVAL, "domain decomposition needs a single rollout");
+    if (slot_lo < 0 || slot_hi <= slot_lo || slot_hi > P.N || slot_lo % SPH_DD_ALIGN != 0 ||
+        (slot_hi != P.N && slot_hi % SPH_DD_ALIGN != 0))
+        return fail(ctx, SPH_EINVAL, "slot range must be [lo, hi) within [0, N), lo and hi multiples of SPH_DD_ALIGN (hi may be N)");
+    CK(cudaStreamSynchronize(ctx->stream));
+    P.own_lo = slot_lo;
+    P.own_n = slot_hi - slot_lo;
+    // the per-substep kernel path with grid-wide rebuild kernels (no single-launch tick, no
+    // per-rollout shared-memory sort, no ring kernels); graphs captured before are stale
+    P.ring = 0;
+    P.pf_d = P.pf_f = 0;
+    ctx->coop = false;
+    ctx->small = false;
+    if (ctx->tick_graph) {
+        cudaGraphExecDestroy(ctx->tick_graph);
+        ctx->tick_graph = nullptr;
+    }
+    return SPH_OK;
+}
+
+sph_status sph_dd_phase(sph_ctx* ctx, int phase, const float* u, void* aux_io, void* state_io,
+                        void* part_io) {
+    if (!ctx || !aux_io || !state_io || !part_io || phase < 0 || phase > 2) return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    if (P.B != 1) return fail(ctx, SPH_EINVAL, "domain decomposition needs a single rollout");
+    if (P.N == 0) return SPH_OK;
+    cudaStream_t s = ctx->stream;
+    float2* aux = static_cast<float2*>(aux_io);
+    float4* st = static_cast<float4*>(state_io);
+    double4* part = static_cast<double4*>(part_io);
+    const int lo = P.own_lo, n = P.own_n;
+    const int q0 = lo / 32, q1 = std::min(P.npart, (lo + n + 31) / 32);
+    if (phase == 0) {
+        if (u) {
+            for (int i = 0; i < 3; ++i)
+                if (!std::isfinite(u[i])) return fail(ctx, SPH_EINVAL, "non-finite input u");
+            CK(cudaMemcpyAsync(ctx->D.u_cur, u, sizeof(float) * 3, cudaMemcpyHostToDevice, s));
+        }
+        ctx->damping_cur = 1.0f;
+        launch_rebuild_and_density(ctx, false, nullptr, false);
+        CK(cudaMemcpyAsync(aux + lo, ctx->D.aux + lo, sizeof(float2) * n, cudaMemcpyDeviceToDevice, s));
+    } else if (phase == 1) {
+        CK(cudaMemcpyAsync(ctx->D.aux, aux, sizeof(float2) * P.N, cudaMemcpyDeviceToDevice, s));
+        launch_force(ctx, s, 1.0f, 0, false);
+        k_dd_export<<<(n + 255) / 256, 256, 0, s>>>(P, ctx->D, st);
+        CK(cudaMemcpyAsync(part + q0, ctx->D.part + q0, sizeof(double4) * (q1 - q0), cudaMemcpyDeviceToDevice, s));
+    } else {
+        k_dd_import<<<(P.N + 255) / 256, 256, 0, s>>>(P, ctx->D, st);
+        CK(cudaMemcpyAsync(ctx->D.part, part, sizeof(double4) * P.npart, cudaMemcpyDeviceToDevice, s));
+        launch_body(ctx, s, 0, ctx->ghost_angle0, false);
+    }
+    return check_launch(ctx);
 }
 
 sph_status sph_step(sph_ctx* ctx, const float* u, int n_substeps, int ptr_on_device) {

@@ -385,7 +385,7 @@ __device__ __forceinline__ void prefetch_ahead(const DevParams& P, const DevPtrs
     if (threadIdx.x != 0 || dist <= 0) return;
     const long long c = (long long)blockIdx.y * gridDim.x + blockIdx.x + dist;
     if (c >= (long long)gridDim.x * gridDim.y) return;
-    const int b = (int)(c / gridDim.x), t0 = (int)(c % gridDim.x) * T;
+    const int b = (int)(c / gridDim.x), t0 = P.own_lo + (int)(c % gridDim.x) * T;
     const int cnt = min(T, P.N - t0);
     if (cnt <= 0) return;
     const size_t o = (size_t)b * P.N;
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(TD) k_density(DevParams P, DevPtrs D, int skip
     const int b = blockIdx.y;
     const RolloutState* rs = D.rs + b;
     if (rs->frozen || (skip_rebuilding && rs->need_rebin)) return;   // CTA-uniform
-    const int i = blockIdx.x * TD + threadIdx.x;
+    const int i = P.own_lo + blockIdx.x * TD + threadIdx.x;
     const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
     if (i < P.N) density_at<true>(P, D, b, i, pv);
     prefetch_ahead<false>(P, D, TD, P.pf_d);
@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(TN) k_nlist_density(DevParams P, DevPtrs D) {
     pdl_wait();
     pdl_trigger();
     const int count = *D.rcount;
-    const int i = blockIdx.x * TN + threadIdx.x;
+    const int i = P.own_lo + blockIdx.x * TN + threadIdx.x;
     for (int w = blockIdx.y; w < count; w += gridDim.y) nlist_density_at(P, D, D.rlist[w], i);
 }
 
@@ -1075,12 +1075,12 @@ __global__ void __launch_bounds__(TF, SPH_FORCE_MINB * TILE / TF) k_force(DevPar
     if (mode == 2) {
         const int count = *D.rcount;
         for (int w = blockIdx.y; w < count; w += gridDim.y)
-            force_tile<TF>(P, D, damping, D.rlist[w], blockIdx.x);
+            force_tile<TF>(P, D, damping, D.rlist[w], P.own_lo / TF + blockIdx.x);
         return;
     }
     const int b = blockIdx.y;
     if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
-    force_tile<TF>(P, D, damping, b, blockIdx.x);
+    force_tile<TF>(P, D, damping, b, P.own_lo / TF + blockIdx.x);
     prefetch_ahead<true>(P, D, TF, P.pf_f);
 }
 
@@ -1383,6 +1383,22 @@ __global__ void k_export(DevParams P, DevPtrs D, int b, float4* out, float* rho)
     const uint32_t id = D.id[rs->ip][o + i];
     out[id] = D.pv[rs->sp][o + i];
     if (rho) rho[id] = D.aux[(size_t)b * P.NA + i].x;
+}
+
+// Domain decomposition (f2) exchange: the owned slots' new state (after k_force, before
+// k_body) out to a caller buffer, and the gathered states of every slot back in (rollout 0).
+__global__ void k_dd_export(DevParams P, DevPtrs D, float4* out) {
+    const int i = P.own_lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.own_lo + P.own_n || i >= P.N) return;
+    const RolloutState* rs = D.rs;
+    out[i] = D.pv[rs->sp ^ rs->need_rebin ^ 1][i];
+}
+
+__global__ void k_dd_import(DevParams P, DevPtrs D, const float4* in) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.N) return;
+    const RolloutState* rs = D.rs;
+    D.pv[rs->sp ^ rs->need_rebin ^ 1][i] = in[i];
 }
 
 __global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angle0) {

@@ -65,3 +65,53 @@ def test_gloo_gather_matches_single_rank(n_total):
         assert p.exitcode == 0
     u = si.ensemble_inputs(range(n_total), K)[0]
     assert np.array_equal(got, np.concatenate([u, 2 * u], axis=2))
+
+
+# ---- domain decomposition: slab ranges and the in-place padded all-gather ----
+
+def test_slab_ranges():
+    from paper_2604_12505_b200.parallel import slab_ranges, n_partials, DD_ALIGN
+    for n, w in ((9261, 2), (9261, 3), (1_000_000, 8), (4096, 4)):
+        chunk, rng = slab_ranges(n, w)
+        assert chunk % DD_ALIGN == 0 and rng[0][0] == 0 and rng[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(rng, rng[1:]))
+        assert w * chunk >= n and w * chunk // 32 >= n_partials(n)
+
+
+def _dd_worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_12505_b200.parallel import slab_ranges, all_gather_inplace
+    chunk, rng = slab_ranges(n, world)
+    lo, hi = rng[rank]
+    # each rank fills only its own slab of a padded buffer, as sph_dd_phase does
+    aux = torch.zeros((world * chunk, 2))
+    aux[lo:hi] = torch.arange(lo, hi, dtype=torch.float32)[:, None] * torch.tensor([1.0, -1.0])
+    part = torch.zeros((world * chunk // 32, 4), dtype=torch.float64)
+    part[lo // 32:(hi + 31) // 32] = float(rank + 1)
+    all_gather_inplace(dist, aux, rank)
+    all_gather_inplace(dist, part, rank)
+    q.put((rank, aux[:n].numpy().copy(), part.numpy().copy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [9261, 5000])
+def test_gloo_dd_exchange(n):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dd_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from paper_2604_12505_b200.parallel import slab_ranges
+    chunk, rng = slab_ranges(n, world)
+    ref = np.arange(n, dtype=np.float32)[:, None] * np.array([1.0, -1.0], np.float32)
+    for rank, aux, part in out:
+        assert np.array_equal(aux, ref)                       # every rank holds the whole array
+        for r, (lo, hi) in enumerate(rng):
+            assert np.all(part[lo // 32:(hi + 31) // 32] == r + 1)
