@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lpv-seqs", type=int, default=1,
                     help="LPV workload: training sequences (the paper: 1)")
-    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN", "P0", "C2CL", "SETTLE", "LPV"],
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN", "P0", "C2CL", "SETTLE", "LPV", "C4DD"],
                     help="LIN: linearization (SURVEY 8(f) f1) of the paper's P0 tank; P0: the paper's "
                          "Table 3 benchmark (30 s closed loop); C2CL: the same manoeuvre on the C2 tank (configs[1]); "
                          "none of them is the north-star line")
@@ -837,6 +837,75 @@ def run_lpv(a):
     print(json.dumps(line), flush=True)
 
 
+def run_dd(a):
+    """--workload C4DD: the single 1M-particle C4 tank decomposed over the
+    torchrun ranks (one GPU each) -- slabs of the cell-sorted slots, three NCCL all-gathers per
+    substep (paper_2604_12505_b200.parallel).  One bench step = 50 substeps; value = particle-
+    updates/s of the one tank (strong scaling: the tank is the same at every N)."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    from paper_2604_12505_b200 import SphContext
+    from paper_2604_12505_b200.parallel import DistributedTank, LocalGroup, slab_ranges
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("gloo" if os.environ.get("BENCH_SINGLE_DEVICE_CHECK") == "1" else "nccl",
+                                device_id=torch.device("cuda", local))
+    t = si.make_tank(42.0)
+    sp = t.params
+    ctx = SphContext(sp, t.pv32(), t.ghost_b, n_rollouts=1, rebin_every=0, skin=a.skin * sp.h,
+                     device=local)
+    tank = DistributedTank(ctx) if world > 1 else LocalGroup([ctx])
+    SUB = 50
+    u = np.array([5.0, 2.0, 1.0], np.float32)
+
+    def step():
+        tank.substep(u)                 # input held (ZOH) for the remaining substeps
+        for _ in range(SUB - 1):
+            tank.substep(None)
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ctx.stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(ctx.stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tm = torch.tensor([ms], dtype=torch.float64, device=ctx.device)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ms = float(tm.item())
+    n_sub = a.steps * SUB
+    st = ctx.get_status()[0]
+    n_steps, n_reb = ctx.counters()
+    chunk, rng = slab_ranges(t.n_fluid, world)
+    ctx.close()
+    if rank != 0:
+        return
+    value = t.n_fluid * n_sub / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 (body f64)",
+        "data": "synthetic (C4 lattice tank, constant input)",
+        "config": {"workload": f"C4DD: one C4 tank ({t.n_fluid} fluid + {t.n_ghost} ghosts) decomposed "
+                               f"over {world} GPU(s), {SUB} substeps per step",
+                   "slabs": rng, "exchange_bytes_per_substep": 40 * t.n_fluid,
+                   "us_per_substep": ms * 1e3 / n_sub, "status": int(st[0]),
+                   "substeps_per_rebuild": float(n_steps[0] / max(int(n_reb[0]), 1)),
+                   "path": "per-substep phases (sph_dd_phase), NCCL in-place all-gathers"},
+        "gpu_launches": None, "clocks": ck, "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     a = parse()
     if a.skin is None:
@@ -852,6 +921,9 @@ def main():
         return
     if a.workload == "LPV":
         run_lpv(a)
+        return
+    if a.workload == "C4DD":
+        run_dd(a)
         return
     if a.impl == "reference":
         run_reference(a)

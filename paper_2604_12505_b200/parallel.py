@@ -137,4 +137,5 @@ class LocalGroup:
         for k in range(3):
             for p in self.parts:
                 p.phase(k, u if k == 0 else None)
-            self.torch.cuda.synchronize()
+            if len(self.parts) > 1:     # one part: its phases are ordered on its own stream
+                self.torch.cuda.synchronize()
