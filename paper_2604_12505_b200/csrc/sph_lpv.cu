@@ -155,27 +155,25 @@ __global__ void __launch_bounds__(LPV_T) k_lpv(int R, int S, int K, const double
             }
 #pragma unroll
             for (int j = 0; j < NX; ++j) x[j] = q4get(xq, j);
-            double a = bb1;
-#pragma unroll
-            for (int j = 0; j < NX; ++j) a = fma(w1[j], x[j], a);
-#pragma unroll
-            for (int j = 0; j < NU; ++j) a = fma(w1[NX + j], uk[j], a);
+            // the chain runs x -> eta -> p -> x+; everything affine in p is split as
+            // M0 (x, u) + p M1 (x, u), with both halves formed while eta is evaluated, and the
+            // dot products are pairwise trees (short dependency chains)
+            const double au = fma(w1[NX + 2], uk[2], fma(w1[NX + 1], uk[1], fma(w1[NX], uk[0], bb1)));
+            const double a = au + (fma(w1[1], x[1], w1[0] * x[0]) + fma(w1[3], x[3], w1[2] * x[2]));
+            const double s0 = (fma(a0[1], x[1], a0[0] * x[0]) + fma(a0[3], x[3], a0[2] * x[2])) +
+                              fma(b0[2], uk[2], fma(b0[1], uk[1], b0[0] * uk[0]));
+            const double s1 = (fma(a1[1], x[1], a1[0] * x[0]) + fma(a1[3], x[3], a1[2] * x[2])) +
+                              fma(b1[2], uk[2], fma(b1[1], uk[1], b1[0] * uk[0]));
+            const double t0 = fma(c0[1], x[1], c0[0] * x[0]) + fma(c0[3], x[3], c0[2] * x[2]);
+            const double t1 = fma(c1[1], x[1], c1[0] * x[0]) + fma(c1[3], x[3], c1[2] * x[2]);
             const double h1q = tanh_d(a);
 #pragma unroll
             for (int j = 0; j < NH; ++j) h1[j] = q4get(h1q, j);
-            double a2 = bb2;
-#pragma unroll
-            for (int j = 0; j < NH; ++j) a2 = fma(w2[j], h1[j], a2);
+            const double a2 = bb2 + (fma(w2[1], h1[1], w2[0] * h1[0]) + fma(w2[3], h1[3], w2[2] * h1[2]));
             const double h2q = tanh_d(a2);
             const double p = q4sum(w3 * h2q) + bb3;
-            double yq = 0.0, xn = 0.0;
-#pragma unroll
-            for (int j = 0; j < NX; ++j) {
-                yq = fma(fma(p, c1[j], c0[j]), x[j], yq);
-                xn = fma(fma(p, a1[j], a0[j]), x[j], xn);
-            }
-#pragma unroll
-            for (int j = 0; j < NU; ++j) xn = fma(fma(p, b1[j], b0[j]), uk[j], xn);
+            const double yq = fma(p, t1, t0);
+            const double xn = fma(p, s1, s0);
             if (want_grad && act) {
                 double* rec = xs + ((size_t)k * RS + rs) * REC;
                 rec[q] = xq;
@@ -231,7 +229,15 @@ __global__ void __launch_bounds__(LPV_T) k_lpv(int R, int S, int K, const double
             const double dyq = q < NY ? cc * (nyq - ny) : 0.0;
             if (k > 0) load(k - 1);
             const double lq = pick4(lam, q);
-            double dpp = 0.0;
+            // off the adjoint chain: the record's contractions and the tanh derivatives
+            const double al = (fma(a1[1], x[1], a1[0] * x[0]) + fma(a1[3], x[3], a1[2] * x[2])) +
+                              fma(b1[2], uk[2], fma(b1[1], uk[1], b1[0] * uk[0]));   // A1 x + B1 u
+            const double gm = fma(c1[1], x[1], c1[0] * x[0]) + fma(c1[3], x[3], c1[2] * x[2]);
+            const double K2 = w3 * (1.0 - h2q * h2q), K1 = 1.0 - h1q * h1q;
+            double sl[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j)
+                sl[j] = fma(fma(p, a1[j], a0[j]), lq, fma(p, c1[j], c0[j]) * dyq);
 #pragma unroll
             for (int j = 0; j < NX; ++j) {
                 const double d = lq * x[j], e = dyq * x[j];
@@ -239,26 +245,23 @@ __global__ void __launch_bounds__(LPV_T) k_lpv(int R, int S, int K, const double
                 ga1[j] = fma(p, d, ga1[j]);
                 gc0[j] += e;
                 gc1[j] = fma(p, e, gc1[j]);
-                dpp = fma(a1[j], d, fma(c1[j], e, dpp));
             }
 #pragma unroll
             for (int j = 0; j < NU; ++j) {
                 const double d = lq * uk[j];
                 gb0[j] += d;
                 gb1[j] = fma(p, d, gb1[j]);
-                dpp = fma(b1[j], d, dpp);
             }
-            const double dp = q4sum(dpp);
+            // the adjoint chain: dp = <A1, lam x^T> + <B1, lam u^T> + <C1, dy x^T>
+            const double dp = q4sum(fma(lq, al, dyq * gm));
             gbb3 += dp;
             gw3 = fma(dp, h2q, gw3);
-            const double da2q = dp * w3 * (1.0 - h2q * h2q);
+            const double da2q = dp * K2;
             gbb2 += da2q;
 #pragma unroll
             for (int j = 0; j < NH; ++j) gw2[j] = fma(da2q, h1[j], gw2[j]);
-            double dh1 = 0.0;
-#pragma unroll
-            for (int i = 0; i < NH; ++i) dh1 = fma(w2c[i], q4get(da2q, i), dh1);
-            const double da1q = dh1 * (1.0 - h1q * h1q);
+            const double g0 = q4get(da2q, 0), g1 = q4get(da2q, 1), g2 = q4get(da2q, 2), g3 = q4get(da2q, 3);
+            const double da1q = (fma(w2c[1], g1, w2c[0] * g0) + fma(w2c[3], g3, w2c[2] * g2)) * K1;
             gbb1 += da1q;
 #pragma unroll
             for (int j = 0; j < NX; ++j) gw1[j] = fma(da1q, x[j], gw1[j]);
@@ -266,8 +269,7 @@ __global__ void __launch_bounds__(LPV_T) k_lpv(int R, int S, int K, const double
             for (int j = 0; j < NU; ++j) gw1[NX + j] = fma(da1q, uk[j], gw1[NX + j]);
             // lam_k = A^T lam_{k+1} + C^T dy_k + W1x^T da1: row q's share of every column, summed
 #pragma unroll
-            for (int j = 0; j < NX; ++j)
-                lam[j] = q4sum(fma(fma(p, a1[j], a0[j]), lq, fma(fma(p, c1[j], c0[j]), dyq, w1[j] * da1q)));
+            for (int j = 0; j < NX; ++j) lam[j] = q4sum(fma(w1[j], da1q, sl[j]));
         }
         if (!act) continue;
         grad[(size_t)r * NG + NT + (size_t)NX * s + q] = fma(sigmax, x0[(size_t)s * NX + q], pick4(lam, q));
