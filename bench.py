@@ -399,6 +399,16 @@ def run_ours(a):
             "kernel_share_of_substep": kms / live["substep"] if live["samples"] else kms / prof["substep"],
             "live_ms": {k: live[k] for k in ("density", "force", "substep")},
             "isolated_ms": kern, "substep_ms_isolated": prof["substep"]}
+    # the resource that binds these kernels: instruction issue.  Warp
+    # instructions per launch from the committed ncu capture, over the same live time, against
+    # 4 issue slots per SM per cycle at the SM clock measured during the timed region
+    inst = traffic_from_profiles(top + "_inst", name)
+    if inst:
+        ipk = inst / (kms / 1e3) / 1e9
+        ipeak = 148 * 4 * ck.get("sm_mhz", 1965.0) / 1e3 if isinstance(ck, dict) and ck.get("sm_mhz") else 148 * 4 * 1.965
+        roof["issue"] = {"bound": "issue", "achieved": ipk, "peak": ipeak, "unit": "G warp-instructions/s",
+                         "frac": ipk / ipeak, "instructions_per_launch": inst,
+                         "source": "smsp__inst_executed.sum per launch, profiles/traffic.json (ncu --set full)"}
     lps = ctx.launches_per_substep()
     launches = a.steps * (1 + (sp.n_sub * lps if lps > 0 else 1))   # 0: one cooperative launch per tick
     ctx.close()
