@@ -162,11 +162,14 @@ class LpvProblem:
                 C.c_void_p(self.stream.cuda_stream)), "sph_lpv_adam")
 
     def lbfgs(self, max_iter, memory=10, tol_grad=1e-9, ftol=2.2e-9, c1=1e-4, max_backtrack=30):
-        """L-BFGS ("warm-start a ... L-BFGS scheme") in lockstep over the restarts:
-        two-loop recursion (memory 10, vectorised over the restarts) and Armijo backtracking; a
-        restart stops when its gradient norm falls below tol_grad, its relative decrease
-        (f_k - f_k+1) / max(|f_k|, |f_k+1|, 1) falls to ftol (scipy's L-BFGS-B default; "up to"
-        max_iter, reading LPV6) or its line search fails.  Frozen parameters (mask) stay fixed.
+        """L-BFGS ("warm-start a ... L-BFGS scheme") over the restarts: two-loop recursion
+        (memory 10, vectorised over the restarts) and Armijo backtracking.  The restarts do not
+        wait for each other: every launch evaluates each restart's current trial point, and a
+        restart whose trial is accepted proceeds to its next direction while another backtracks
+        (each launch advances every restart by one trial).  A restart stops after max_iter
+        accepted iterations, when its gradient norm falls below tol_grad, its relative decrease
+        (f_k - f_k+1) / max(|f_k|, |f_k+1|, 1) falls to ftol (scipy's L-BFGS-B default;
+        reading LPV6), or its line search fails.  Frozen parameters (mask) stay fixed.
         Returns the number of objective evaluations (launches x restarts)."""
         torch = self.torch
         mk = None if self.mask is None else self.mask.cpu().numpy().astype(bool)
@@ -183,12 +186,12 @@ class LpvProblem:
         rh = np.zeros((R, m))
         cnt = np.zeros(R, np.int64)
         head = np.zeros(R, np.int64)          # next slot of each restart's circular history
-        active = np.ones(R, bool)
+        active = np.linalg.norm(g, axis=1) > tol_grad
+        iters = np.zeros(R, np.int64)
         n_eval = 1
-        for _ in range(max_iter):
-            active &= np.linalg.norm(g, axis=1) > tol_grad
-            if not active.any():
-                break
+
+        def directions(sel):
+            """Two-loop recursion for the restarts in ``sel`` (bool [R]); others get 0."""
             q = -g
             al = np.zeros((R, m))
             for j in range(m):                                   # newest -> oldest
@@ -208,46 +211,54 @@ class LpvProblem:
                 v = j < cnt
                 b = rh[ar, idx] * np.einsum("rn,rn->r", Yh[ar, idx], q)
                 q = q + np.where(v, al[:, j] - b, 0.0)[:, None] * Sh[ar, idx]
-            d = np.where(active[:, None], q, 0.0)
-            slope = (g * d).sum(1)
-            bad = active & (slope >= 0)          # not a descent direction: restart memory
+            bad = sel & ((g * q).sum(1) >= 0)     # not a descent direction: restart memory
             if bad.any():
                 cnt[bad] = 0
-                d[bad] = -g[bad] * np.minimum(1.0, 1.0 / g1[bad])[:, None]
-                slope = (g * d).sum(1)
-            step = np.where(active, 1.0, 0.0)
-            done = ~active
-            xn, fn, gn = x.copy(), f.copy(), g.copy()
-            for _bt in range(max_backtrack):
-                trial = x + step[:, None] * d
-                trial[done] = xn[done]
-                fo, go = self.eval(torch.from_numpy(trial).to(self.dev))
-                n_eval += 1
-                fo = fo.cpu().numpy()
-                go = go.cpu().numpy()
-                ok = (~done) & np.isfinite(fo) & (fo <= f + c1 * step * slope)
-                xn[ok], fn[ok], gn[ok] = trial[ok], fo[ok], go[ok]
-                done |= ok
-                if done.all():
-                    break
-                step = np.where(done, step, 0.5 * step)
-            failed = active & ~done
-            active &= ~failed
+                q[bad] = -g[bad] * np.minimum(1.0, 1.0 / g1[bad])[:, None]
+            return np.where(sel[:, None], q, 0.0)
+
+        d = directions(active)
+        slope = (g * d).sum(1)
+        step = np.where(active, 1.0, 0.0)
+        nbt = np.zeros(R, np.int64)
+        while active.any():
+            trial = np.where(active[:, None], x + step[:, None] * d, x)
+            fo, go = self.eval(torch.from_numpy(trial).to(self.dev))
+            n_eval += 1
+            fo = fo.cpu().numpy()
+            go = go.cpu().numpy()
             if mk is not None:
-                gn[:, ~mk] = 0.0
-            s_ = xn - x
-            y_ = gn - g
-            sy = np.einsum("rn,rn->r", s_, y_)
-            keep = active & (sy > 1e-12 * np.linalg.norm(s_, axis=1) * np.linalg.norm(y_, axis=1))
-            kk = np.flatnonzero(keep)
-            Sh[kk, head[kk]] = s_[kk]
-            Yh[kk, head[kk]] = y_[kk]
-            rh[kk, head[kk]] = 1.0 / sy[kk]
-            head[kk] = (head[kk] + 1) % m
-            cnt[kk] = np.minimum(cnt[kk] + 1, m)
-            stalled = active & ((f - fn) <= ftol * np.maximum(np.maximum(np.abs(f), np.abs(fn)), 1.0))
-            active &= ~stalled
-            x, f, g = xn, fn, gn
+                go[:, ~mk] = 0.0
+            ok = active & np.isfinite(fo) & (fo <= f + c1 * step * slope)
+            # rejected trials backtrack; exhausted line searches stop their restart
+            rej = active & ~ok
+            nbt[rej] += 1
+            step[rej] *= 0.5
+            active &= ~(rej & (nbt >= max_backtrack))
+            if ok.any():
+                s_ = trial - x
+                y_ = go - g
+                sy = np.einsum("rn,rn->r", s_, y_)
+                keep = ok & (sy > 1e-12 * np.linalg.norm(s_, axis=1) * np.linalg.norm(y_, axis=1))
+                kk = np.flatnonzero(keep)
+                Sh[kk, head[kk]] = s_[kk]
+                Yh[kk, head[kk]] = y_[kk]
+                rh[kk, head[kk]] = 1.0 / sy[kk]
+                head[kk] = (head[kk] + 1) % m
+                cnt[kk] = np.minimum(cnt[kk] + 1, m)
+                stalled = ok & ((f - fo) <= ftol * np.maximum(np.maximum(np.abs(f), np.abs(fo)), 1.0))
+                x[ok], f[ok], g[ok] = trial[ok], fo[ok], go[ok]
+                iters[ok] += 1
+                active &= ~stalled
+                active &= ~(ok & (iters >= max_iter))
+                active &= ~(ok & (np.linalg.norm(g, axis=1) <= tol_grad))
+                nxt = ok & active
+                if nxt.any():
+                    dn = directions(nxt)
+                    d[nxt] = dn[nxt]
+                    slope[nxt] = (g[nxt] * d[nxt]).sum(1)
+                    step[nxt] = 1.0
+                    nbt[nxt] = 0
         self.params.copy_(torch.from_numpy(x))
         return n_eval
 
