@@ -43,7 +43,7 @@ def build(force: bool = False) -> str:
 class Params(C.Structure):
     _fields_ = [(n, C.c_double) for n in (
         "rho0", "k", "alpha", "beta", "gamma1", "eps", "h", "mass", "w_cb_const",
-        "ghost_pressure_sign", "gx", "gy", "m_body", "J_body", "R", "dt")]
+        "ghost_pressure_sign", "gx", "gy", "m_body", "J_body", "R", "dt", "clamp_negative_pressure")]
 
 
 _lib = None
@@ -91,7 +91,7 @@ def params(sp) -> Params:
     """orc params from a sph_inputs.SimParams (plain data)."""
     return Params(sp.rho0, sp.k, sp.alpha, sp.beta, sp.gamma1, sp.eps, sp.h, sp.mass,
                   sp.w_cb_const, sp.ghost_pressure_sign, sp.gx, sp.gy, sp.m_body, sp.J_body,
-                  sp.R, sp.dt)
+                  sp.R, sp.dt, float(getattr(sp, "clamp_negative_pressure", 0.0)))
 
 
 def _c(a, dt=np.float64):

@@ -305,7 +305,8 @@ void orc_density(const orc_params* p, int n, const double* pos, int ng, const do
             sg += orc_W_cb(p, sqrt(dx * dx + dy * dy));
         }
         rho[i] = p->mass * (sf + p->gamma1 * sg);
-        P[i] = p->k * (rho[i] - p->rho0);
+        P[i] = p->k * (rho[i] - p->rho0);                                   /* Eq. EOS */
+        if (p->clamp_negative_pressure != 0.0 && P[i] < 0.0) P[i] = 0.0;
     }
     free(buf);
     grid_free(&gf);

@@ -22,6 +22,7 @@ typedef struct {
     double gx, gy;                /* external acceleration on the fluid */
     double m_body, J_body, R;     /* Table 1 */
     double dt;                    /* fast step */
+    double clamp_negative_pressure; /* 1: P = max(k (rho - rho0), 0) (ablation); 0: Eq. EOS */
 } orc_params;
 
 /* Kernels. r = |x|. dW = dW/dr. */

@@ -56,6 +56,7 @@ class SimParams:
     mass: float = RHO0 * 3.0 * D_PAPER ** 2     # reading R1: m = rho0 s^2
     w_cb_const: float = W_CB_CONST_NORMALISED   # reading A1
     ghost_pressure_sign: float = -1.0           # reading A4 (repulsive)
+    clamp_negative_pressure: float = 0.0        # 0: Eq. EOS as printed; 1: P = max(P, 0) (ablation)
     gx: float = 0.0                             # zero gravity
     gy: float = 0.0
     m_body: float = M_BODY
