@@ -61,6 +61,8 @@ typedef struct {
     double w_cb_const;  /* cubic-spline constant C in C/h^2 (reading A1: 5/(14 pi))        */
     double ghost_pressure_sign; /* -1 repulsive wall (reading A4), +1 literal Alg. 1       */
     double gravity[2];  /* external acceleration on the fluid, world frame (0 = zero-g)    */
+    double clamp_negative_pressure; /* 0: Eq. EOS as printed (default); 1: P = max(k (rho -
+                                       rho0), 0), the ablation of SURVEY 8(b) (E1)  */
 } sph_fluid_params;
 
 /* Rigid spacecraft: Table 1.  Tank = circle of radius tank_radius at the CoM. */

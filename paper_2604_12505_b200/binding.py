@@ -23,7 +23,8 @@ class FluidParams(C.Structure):
     _fields_ = [("rho0", C.c_double), ("k", C.c_double), ("alpha", C.c_double),
                 ("beta", C.c_double), ("gamma1", C.c_double), ("eps", C.c_double),
                 ("h", C.c_double), ("mass", C.c_double), ("w_cb_const", C.c_double),
-                ("ghost_pressure_sign", C.c_double), ("gravity", C.c_double * 2)]
+                ("ghost_pressure_sign", C.c_double), ("gravity", C.c_double * 2),
+                ("clamp_negative_pressure", C.c_double)]
 
 
 class BodyParams(C.Structure):
@@ -109,6 +110,7 @@ def fluid_params(sp) -> FluidParams:
                     sp.w_cb_const, sp.ghost_pressure_sign)
     g.gravity[0] = sp.gx
     g.gravity[1] = sp.gy
+    g.clamp_negative_pressure = float(getattr(sp, "clamp_negative_pressure", 0.0))
     return g
 
 

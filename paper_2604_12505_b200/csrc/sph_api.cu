@@ -168,6 +168,7 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->m2 = (float)(fp->mass * fp->mass);
     P->rho0 = (float)fp->rho0;
     P->k = (float)fp->k;
+    P->clampP = fp->clamp_negative_pressure != 0.0 ? 1 : 0;
     P->gamma1 = (float)fp->gamma1;
     P->alpha2h = (float)(2.0 * fp->alpha * h);
     P->beta = (float)fp->beta;
@@ -1167,6 +1168,7 @@ sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr
     J.m = ctx->fp.mass;
     J.rho0 = ctx->fp.rho0;
     J.k = ctx->fp.k;
+    J.clampP = ctx->fp.clamp_negative_pressure != 0.0 ? 1 : 0;
     J.gamma1 = ctx->fp.gamma1;
     J.alpha2h = 2.0 * ctx->fp.alpha * ctx->fp.h;
     J.beta = ctx->fp.beta;

@@ -63,6 +63,7 @@ struct DevParams {
                             // > 1 = k_body_reduce first sums bsplit fixed chunks (large tanks;
                             // chosen from N only, so bits never depend on B)
     int pf_d, pf_f;         // L2 prefetch distance in CTAs (k_density / k_force; 0 = off)
+    int clampP;             // 1: negative pressures clamped to 0 (ablation E1)
     int own_lo, own_n;      // domain decomposition: the particle kernels compute
                             // slots [own_lo, own_lo + own_n) only (default: all N)
     double dtd, m_body, J_body;

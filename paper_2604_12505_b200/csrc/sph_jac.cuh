@@ -33,6 +33,7 @@ constexpr int JAC_PT = 64;     // threads of the sparse (particle seed) column C
 struct JacParams {
     int N, G, nx;                // particles, ghosts, state dimension 4N + 6
     double h, m, rho0, k, gamma1, alpha2h, beta, eps_h2, sgn2m2, m2, mB, J;
+    int clampP;                  // negative pressures clamped to 0 (dP/drho = 0 there)
     double H2, h2;               // (2h)^2, h^2 (float64 predicates, as the oracle)
     double wc, ws;               // w_cb_const, 10 / pi (kernel constants without h powers)
 };
@@ -199,7 +200,8 @@ __global__ void k_jac_prep(JacParams J, JacPtrs X) {
         X.g2_cnt[i] = min(n2, JAC_GCAP);
         X.g1_cnt[i] = min(n1, JAC_GCAP);
         const double rho = J.m * (wcb(0.0) + ws + J.gamma1 * wg);   // self term
-        const double P = J.k * (rho - J.rho0);
+        double P = J.k * (rho - J.rho0);
+        if (J.clampP && P < 0.0) P = 0.0;
         X.rho[i] = rho;
         X.P[i] = P;
         X.Q[i] = P / (rho * rho);
@@ -256,7 +258,8 @@ __device__ __forceinline__ double2 jac_dacc_i(const JacParams& J, const JacPtrs&
     const double2 xi = X.pos[i], vi = X.vel[i];
     const double2 dxi = seed_pos(d, i), dvi = seed_vel(J, d, i);
     const double rhoi = X.rho[i], Qi = X.Q[i], Pi = X.P[i], drhoi = drho_of(i);
-    const double dQi = drhoi * (J.k / (rhoi * rhoi) - 2.0 * Pi / (rhoi * rhoi * rhoi));
+    const double ki = (J.clampP && rhoi < J.rho0) ? 0.0 : J.k;   // dP/drho (clamped: 0)
+    const double dQi = drhoi * (ki / (rhoi * rhoi) - 2.0 * Pi / (rhoi * rhoi * rhoi));
     double2 da = make_double2(0.0, 0.0);   // d a_i^ff / m
     for (int t = 0; t < X.nf_cnt[i]; ++t) {
         const int j = X.nf[(size_t)i * JAC_NCAP + t];
@@ -274,7 +277,8 @@ __device__ __forceinline__ double2 jac_dacc_i(const JacParams& J, const JacPtrs&
         const double g = W1 / r, dg_dr = (W2 - g) / r;
         const double dr = dot2(x, dx) / r;
         const double rhoj = X.rho[j], Qj = X.Q[j], Pj = X.P[j], drhoj = drho_of(j);
-        const double dQj = drhoj * (J.k / (rhoj * rhoj) - 2.0 * Pj / (rhoj * rhoj * rhoj));
+        const double kj = (J.clampP && rhoj < J.rho0) ? 0.0 : J.k;
+        const double dQj = drhoj * (kj / (rhoj * rhoj) - 2.0 * Pj / (rhoj * rhoj * rhoj));
         const double den = r2 + J.eps_h2, c = dot2(v, x) / den;
         const double rs = rhoi + rhoj;
         const double Pi_ = J.alpha2h * c / rs;

@@ -310,7 +310,8 @@ __device__ __forceinline__ void finish_density(const DevParams& P, const DevPtrs
         }
     });
     const float rho = P.mass * P.wcb * (wf + P.gamma1 * wg);
-    const float pr = P.k * (rho - P.rho0);
+    float pr = P.k * (rho - P.rho0);
+    if (P.clampP) pr = fmaxf(pr, 0.0f);
     D.aux[(size_t)b * P.NA + i] = make_float2(rho, __fdividef(pr, rho * rho));
 }
 

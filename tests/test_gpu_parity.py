@@ -448,8 +448,10 @@ def test_damped_settle_statistics_match_oracle(path, skin):
 
 @pytest.mark.parametrize("over", [dict(w_cb_const=si.W_CB_CONST_PRINTED),
                                   dict(ghost_pressure_sign=1.0),
-                                  dict(gy=-0.05)],
-                         ids=["printed_cubic_constant", "literal_wall_pressure_sign", "gravity"])
+                                  dict(gy=-0.05),
+                                  dict(clamp_negative_pressure=1.0)],
+                         ids=["printed_cubic_constant", "literal_wall_pressure_sign", "gravity",
+                              "clamped_negative_pressure"])
 def test_reading_switches_one_step_parity(over):
     """The readings' switches (A1 printed constant, A4 literal sign, external acceleration) take
     the same path on both sides: one-step parity at 1e-5 on a moving, rotated C1 tank."""
