@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--eos-clamp", action="store_true",
+                    help="LPV / SETTLE workloads: clamp negative pressures (ablation E1, DESIGN.md)")
     ap.add_argument("--lpv-seqs", type=int, default=1,
                     help="LPV workload: training sequences (the paper: 1)")
     ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS) + ["LIN", "P0", "C2CL", "SETTLE", "LPV", "C4DD"],
@@ -755,7 +757,7 @@ def run_lpv(a):
     torch.cuda.set_device(local)
     from paper_2604_12505_b200 import SphContext
     from paper_2604_12505_b200 import lpv as LP
-    t = si.make_tank(1.0, n_first=666)
+    t = si.make_tank(1.0, n_first=666, clamp_negative_pressure=1.0 if a.eos_clamp else 0.0)
     sp = t.params
     Ts = sp.dt * sp.n_sub
     ctx = SphContext(sp, t.pv32(), t.ghost_b, n_rollouts=1, rebin_every=0, skin=0.5 * sp.h,
@@ -830,7 +832,8 @@ def run_lpv(a):
         "value": train_s, "unit": "s", "n_gpus": 1, "steps": 1, "warmup": 0,
         "ms_per_step": train_s * 1e3, "higher_is_better": False, "scaling": "none",
         "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic (SPH simulator: P0 tank, open-loop excitation train, {S} x {K} samples)",
+        "data": f"synthetic (SPH simulator: P0 tank, open-loop excitation train, {S} x {K} samples"
+                f"{', clamped EOS (ablation E1)' if a.eos_clamp else ''})",
         "config": {"workload": f"LPV: n_x 4, n_u 3, n_y 3, n_p 1, theta 137 + x0; {S} sequence(s) x {K} samples",
                    "dataset_generation_s": gen_s, "n_evals": res["n_evals"],
                    "ms_per_eval": train_s * 1e3 / max(res["n_evals"] / 8, 1),
