@@ -100,13 +100,19 @@ class DistributedTank:
         world = dist.get_world_size(group)
         self.part = DomainPart(ctx, rank, world)
         self.torch = ctx.torch
+        self.host_staged = dist.get_backend(group) == "gloo"
 
     def _gather(self, *tensors):
         ctx = self.part.ctx
         cur = self.torch.cuda.current_stream(ctx.device)
         cur.wait_stream(ctx.stream)
         for t in tensors:
-            all_gather_inplace(self.dist, t, self.part.rank, self.group)
+            if self.host_staged:      # gloo: control-flow checks only (host copies)
+                h = t.cpu()
+                all_gather_inplace(self.dist, h, self.part.rank, self.group)
+                t.copy_(h)
+            else:
+                all_gather_inplace(self.dist, t, self.part.rank, self.group)
         ctx.stream.wait_stream(cur)
 
     def substep(self, u=None):

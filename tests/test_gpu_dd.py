@@ -75,3 +75,51 @@ def test_domain_validation():
     c2 = SphContext(t2.params, t2.pv32(), t2.ghost_b, n_rollouts=2)
     assert c2.L.sph_set_domain(c2.ctx, 0, c2.N) != 0         # more than one rollout
     c2.close()
+
+
+def _dd_rank(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_12505_b200.parallel import DistributedTank
+    t = si.moving_tank(4.0, seed=7, vel=0.02, body=BODY)
+    ctx = _ctx(t, rebin_every=0, skin=0.3 * t.params.h)
+    tank = DistributedTank(ctx)
+    r = np.random.Generator(np.random.Philox(5))
+    for k in range(12):
+        tank.substep((r.normal(size=3) * 20.0).astype(np.float32))
+    torch.cuda.synchronize()
+    q.put((rank, ctx.get_particles(0), ctx.get_body_state()[0]))
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_distributed_tank_two_processes():
+    """DistributedTank across two processes (gloo, host-staged all-gathers; both processes on
+    this one device, nothing on the device waits for the other process): both end with the
+    single-context trajectory, bitwise."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    procs = [ctxm.Process(target=_dd_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    t = si.moving_tank(4.0, seed=7, vel=0.02, body=BODY)
+    ref = _ctx(t, rebin_every=0, skin=0.3 * t.params.h)
+    r = np.random.Generator(np.random.Philox(5))
+    for k in range(12):
+        ref.step((r.normal(size=3) * 20.0).astype(np.float32)[None], 1)
+    pv, body = ref.get_particles(0), ref.get_body_state()[0]
+    for rank, pvr, br in out:
+        assert np.array_equal(pvr, pv) and np.array_equal(br, body)

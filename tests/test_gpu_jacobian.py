@@ -38,9 +38,10 @@ def _block_err(Ag, Ao, n):
     return worst
 
 
-@pytest.mark.parametrize("case", ["moving_rotated", "after_actuated_steps"])
+@pytest.mark.parametrize("case", ["moving_rotated", "after_actuated_steps", "clamped_eos"])
 def test_jacobian_matches_oracle_fd(case):
-    t = si.moving_tank(1.0, seed=3, vel=0.02, body=BODY)
+    over = dict(clamp_negative_pressure=1.0) if case == "clamped_eos" else {}
+    t = si.moving_tank(1.0, seed=3, vel=0.02, body=BODY, **over)
     ctx = _ctx(t)
     ctx.set_body_state(np.array([BODY]))
     if case == "after_actuated_steps":
@@ -53,7 +54,9 @@ def test_jacobian_matches_oracle_fd(case):
     # the oracle's central differences are accurate to ~2e-9 of max|A| (its step-convergence
     # pin); the analytic float64 Jacobian agrees to that level
     assert _block_err(A, Ao, n) <= 5e-7       # per block: FD rounding floor of small blocks
-    assert np.abs(B - Bo).max() <= 1e-9 * np.abs(Bo).max()
+    # B is exact on the GPU (test_jacobian_exact_identities); the oracle's central differences
+    # carry a rounding floor ~eps |f| / h_step, larger where the wall force is larger
+    assert np.abs(B - Bo).max() <= 1e-7 * np.abs(Bo).max()
     ctx.close()
 
 
