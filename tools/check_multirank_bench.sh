@@ -9,3 +9,6 @@ echo "multi-rank bench exit $?"
 BENCH_SINGLE_DEVICE_CHECK=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
     --master-addr 127.0.0.1 --master-port 29556 bench.py --impl reference --gpus 2 --steps 1 --warmup 0
 echo "multi-rank reference exit $?"
+BENCH_SINGLE_DEVICE_CHECK=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 29557 bench.py --workload C4DD --gpus 2 --steps 1 --warmup 1
+echo "multi-rank C4DD exit $?"
