@@ -142,6 +142,15 @@ sph_status sph_get_body_state(sph_ctx* ctx, double* out);
  * fluid velocities multiplied by `damping` after each substep. */
 sph_status sph_settle(sph_ctx* ctx, double damping, int n_steps);
 
+/* P:323-324, "allowed to evolve without external actuation until their velocities converge to
+ * zero": sph_settle in chunks of check_every substeps, each followed by the test, until every
+ * rollout's largest fluid speed is below v_tol (m/s) or max_steps substeps were taken (at least
+ * one chunk runs: a spawn starts at rest).  steps_done (nullable): substeps taken;
+ * max_speed (nullable, host float[B]): the final largest speed per rollout.  Synchronises.
+ * Errors: SPH_EINVAL bad arguments; SPH_ECUDA launch failure. */
+sph_status sph_settle_until(sph_ctx* ctx, double damping, double v_tol, int max_steps,
+                            int check_every, int* steps_done, float* max_speed);
+
 /* Per-rollout numerical status (host int32[B]); bad_step (host int64[B], nullable) = substep
  * index of the failure; bad_particle (host int32[B], nullable) = canonical particle id. */
 sph_status sph_get_status(sph_ctx* ctx, int32_t* rollout_status, int64_t* bad_step,

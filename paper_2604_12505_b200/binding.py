@@ -77,6 +77,7 @@ def lib():
             "sph_eigenvalues": (i32, [vp, i32, vp, vp, i32]),
             "sph_gamma1_estimate": (i32, [vp, i32, dbl, vp, vp, vp]),
             "sph_set_domain": (i32, [vp, i32, i32]),
+            "sph_settle_until": (i32, [vp, dbl, dbl, i32, i32, vp, vp]),
             "sph_dd_phase": (i32, [vp, i32, vp, vp, vp, vp]),
             "sph_lpv_scratch_bytes": (C.c_size_t, [i32, i32, i32]),
             "sph_lpv_eval": (i32, [i32, i32, i32, vp, vp, vp, dbl, dbl, vp, vp, vp, vp, C.c_size_t, vp]),
@@ -101,7 +102,7 @@ def exported_symbols():
             "sph_debug_neighbours", "sph_profile_substeps", "sph_set_live_timing", "sph_get_live_timing",
             "sph_launches_per_substep", "sph_get_counters", "sph_jacobian", "sph_eigenvalues",
             "sph_gamma1_estimate", "sph_lpv_scratch_bytes", "sph_lpv_eval", "sph_lpv_adam",
-            "sph_set_domain", "sph_dd_phase",
+            "sph_set_domain", "sph_dd_phase", "sph_settle_until",
             "sph_get_sizes", "sph_last_error", "sph_destroy"]
 
 
@@ -244,6 +245,16 @@ class SphContext:
 
     def settle(self, damping: float, n_steps: int):
         self._check(self.L.sph_settle(self.ctx, float(damping), int(n_steps)), "sph_settle")
+
+    def settle_until(self, damping: float, v_tol: float, max_steps: int, check_every: int = 500):
+        """Damped settle until every rollout's largest fluid speed < v_tol; returns
+        (substeps taken, final largest speed per rollout)."""
+        n = C.c_int(0)
+        sp = np.zeros(self.B, np.float32)
+        self._check(self.L.sph_settle_until(self.ctx, float(damping), float(v_tol), int(max_steps),
+                                            int(check_every), C.byref(n), sp.ctypes.data),
+                    "sph_settle_until")
+        return n.value, sp
 
     def rollout(self, u_seq, theta_ref=None, Kp: float = 0.0, Kd: float = 0.0, y_out=None,
                 u_applied=None):

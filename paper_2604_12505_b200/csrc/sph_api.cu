@@ -1027,6 +1027,40 @@ sph_status sph_settle(sph_ctx* ctx, double damping, int n_steps) {
     return SPH_OK;
 }
 
+sph_status sph_settle_until(sph_ctx* ctx, double damping, double v_tol, int max_steps,
+                            int check_every, int* steps_done, float* max_speed) {
+    if (!ctx || max_steps < 0 || check_every <= 0 || !(damping > 0 && damping <= 1) || !(v_tol >= 0))
+        return SPH_EINVAL;
+    const DevParams& P = ctx->P;
+    sph_status st = ensure_stage(ctx, sizeof(float) * P.B);   // device [B] speeds
+    if (st) return st;
+    float* d_speed = static_cast<float*>(ctx->stage);
+    std::vector<float> sp(P.B, 0.0f);
+    int done = 0;
+    // a spawn starts at rest, so the test runs after each chunk, never before the first one
+    for (;;) {
+        const int n = std::min(check_every, max_steps - done);
+        if (n > 0) {
+            st = sph_settle(ctx, damping, n);
+            if (st) return st;
+            done += n;
+        }
+        if (P.N > 0) {
+            k_max_speed<<<P.B, 256, 0, ctx->stream>>>(P, ctx->D, d_speed);
+            st = check_launch(ctx);
+            if (st) return st;
+            CK(cudaMemcpyAsync(sp.data(), d_speed, sizeof(float) * P.B, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        bool conv = true;
+        for (float v : sp) conv = conv && v < v_tol;
+        if (conv || done >= max_steps) break;
+    }
+    if (steps_done) *steps_done = done;
+    if (max_speed) std::copy(sp.begin(), sp.end(), max_speed);
+    return SPH_OK;
+}
+
 sph_status sph_get_status(sph_ctx* ctx, int32_t* rollout_status, int64_t* bad_step,
                           int32_t* bad_particle) {
     if (!ctx || !rollout_status) return SPH_EINVAL;

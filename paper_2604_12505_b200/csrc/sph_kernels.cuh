@@ -1407,6 +1407,27 @@ __global__ void k_dd_import(DevParams P, DevPtrs D, const float4* in) {
     D.pv[rs->sp ^ rs->need_rebin ^ 1][i] = in[i];
 }
 
+// Largest fluid speed of each rollout (sph_settle_until's convergence test).
+__global__ void k_max_speed(DevParams P, DevPtrs D, float* out) {
+    const int b = blockIdx.x;
+    const RolloutState* rs = D.rs + b;
+    const float4* pv = D.pv[rs->sp] + (size_t)b * P.N;
+    float m = 0.0f;
+    for (int i = threadIdx.x; i < P.N; i += blockDim.x) {
+        const float4 v = pv[i];
+        m = fmaxf(m, v.z * v.z + v.w * v.w);
+    }
+    m = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));   // m >= 0
+    __shared__ float sm[32];
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float r = 0.0f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmaxf(r, sm[w]);
+        out[b] = sqrtf(r);
+    }
+}
+
 __global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angle0) {
     const int b = b0 + blockIdx.x;
     RolloutState* rs = D.rs + b;

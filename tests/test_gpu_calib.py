@@ -115,3 +115,20 @@ def test_reading_ablations_classified_alike(reading):
         assert out_o > 0
         if reading in ("literal_sign", "R0"):
             assert out_o > 0.2 * t.n_fluid
+
+
+def test_settle_until_converges():
+    """sph_settle_until ("until their velocities converge to zero"): a random spawn of the
+    C1 tank settles below 2e-3 m/s in chunks of 250 substeps; an already converged state takes
+    one chunk; the reported speed is the largest fluid speed of the returned state."""
+    t = si.random_spawn(1.0, seed=12)
+    sp = t.params
+    damp = math.exp(-10.0 * sp.dt)
+    ctx = _ctx(t)
+    n, v = ctx.settle_until(damp, 2e-3, int(4.0 / sp.dt), 250)
+    pv = ctx.get_particles(0).astype(np.float64)
+    assert 0 < n < int(4.0 / sp.dt) and n % 250 == 0
+    assert v[0] < 2e-3 and abs(np.hypot(pv[:, 2], pv[:, 3]).max() - v[0]) <= 1e-6
+    n2, v2 = ctx.settle_until(damp, 1.0, 1000, 250)     # converged: one chunk, then the test
+    assert n2 == 250 and v2[0] < v[0]
+    ctx.close()
