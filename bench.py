@@ -62,11 +62,13 @@ def parse():
                     help="1: rebuild cell list + neighbour lists every substep; 0: adaptive (skin)")
     ap.add_argument("--skin", type=float, default=None,
                     help="Verlet skin in units of h (adaptive); default 0.15 for the open-loop ensembles, "
-                         "0.5 for the closed-loop manoeuvre runs (P0, C2CL: energetic flow, see DESIGN.md)")
+                         "0.5 for the closed-loop manoeuvre runs (P0, C2CL: energetic flow, see DESIGN.md), "
+                         "0.8 for C4 (wall-layer particles at 0.3-0.5 m/s trip a small skin every 2 substeps)")
     ap.add_argument("--live-every", type=int, default=16,
                     help="live kernel timing: event nodes every N-th substep of the timed ticks (0 = off)")
-    ap.add_argument("--settle-seconds", type=float, default=4.0,
-                    help="damped settle of the initial tank (reading A17; ell=4 needs >= 4 s)")
+    ap.add_argument("--settle-seconds", type=float, default=None,
+                    help="damped settle of the initial tank (reading A17; ell=4 needs >= 4 s); default 4 s, "
+                         "C4: 1,000 damped substeps (SURVEY 8(d)) when no settled snapshot exists")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-substeps", type=int, default=20)
     return ap.parse_args()
@@ -923,7 +925,10 @@ def run_dd(a):
 def main():
     a = parse()
     if a.skin is None:
-        a.skin = 0.5 if a.workload in ("P0", "C2CL", "SETTLE") else 0.15
+        a.skin = {"P0": 0.5, "C2CL": 0.5, "SETTLE": 0.5, "C4": 0.8}.get(a.workload, 0.15)
+    if a.settle_seconds is None:
+        # C4: lattice start + 1,000 untimed damped warm-up substeps; dt = 1 ms / 42
+        a.settle_seconds = 1000 * 1e-3 / 42.0 if a.workload == "C4" else 4.0
     if a.workload == "LIN":
         run_linearize(a)
         return

@@ -1152,19 +1152,38 @@ __global__ void __launch_bounds__(SW_T, 3) k_force_ring(DevParams P, DevPtrs D, 
 // Ghost kinematics, Eq. kinematicghost, in fp64 from the fp64 body state.
 // ---------------------------------------------------------------------------------------
 // body[6], body[7] = cos(theta), sin(theta) (computed once per rollout)
+// The body-frame loads of GU ghosts per thread are issued together before any store (restrict
+// pointers, body state in registers): the loop is one L2 round trip per GU ghosts instead of one
+// per ghost (k_body is a latency chain; same arithmetic, same bits).
+constexpr int GU = 4;
 __device__ __forceinline__ void ghost_update(const DevParams& P, const DevPtrs& D, int b,
                                              const double* body, int tid, int nthr) {
     const double c = body[6], s = body[7];
-    for (int g = tid; g < P.G; g += nthr) {
-        const double2 q = D.ghost_b[g];
-        const double ax = c * q.x - s * q.y, ay = s * q.x + c * q.y;
-        const double wx = ax + body[0], wy = ay + body[1];
-        const double vx = body[3] - body[5] * (wy - body[1]);
-        const double vy = body[4] + body[5] * (wx - body[0]);
-        const float hx = (float)wx, hy = (float)wy;
-        D.gst[(size_t)b * P.G + g] = make_float4(hx, hy, (float)vx, (float)vy);
-        D.glo[(size_t)b * P.G + g] = make_float2((float)(wx - (double)hx), (float)(wy - (double)hy));
-        D.garm[(size_t)b * P.G + g] = make_float2((float)(wx - body[0]), (float)(wy - body[1]));
+    const double r0 = body[0], r1 = body[1], v0 = body[3], v1 = body[4], w = body[5];
+    const double2* __restrict__ gb = D.ghost_b;
+    float4* __restrict__ gst = D.gst + (size_t)b * P.G;
+    float2* __restrict__ glo = D.glo + (size_t)b * P.G;
+    float2* __restrict__ garm = D.garm + (size_t)b * P.G;
+    for (int g0 = tid; g0 < P.G; g0 += GU * nthr) {
+        double2 q[GU];
+#pragma unroll
+        for (int k = 0; k < GU; ++k) {
+            const int g = g0 + k * nthr;
+            if (g < P.G) q[k] = __ldg(gb + g);
+        }
+#pragma unroll
+        for (int k = 0; k < GU; ++k) {
+            const int g = g0 + k * nthr;
+            if (g >= P.G) break;
+            const double ax = c * q[k].x - s * q[k].y, ay = s * q[k].x + c * q[k].y;
+            const double wx = ax + r0, wy = ay + r1;
+            const double vx = v0 - w * (wy - r1);
+            const double vy = v1 + w * (wx - r0);
+            const float hx = (float)wx, hy = (float)wy;
+            gst[g] = make_float4(hx, hy, (float)vx, (float)vy);
+            glo[g] = make_float2((float)(wx - (double)hx), (float)(wy - (double)hy));
+            garm[g] = make_float2((float)(wx - r0), (float)(wy - r1));
+        }
     }
 }
 
@@ -1212,6 +1231,24 @@ __device__ __forceinline__ void body_step(const DevParams& P, const DevPtrs& D, 
                                           float ghost_angle0, double4* red, int nt) {
     RolloutState* rs = D.rs + b;
     __shared__ double sbody[8];
+    // thread 0's state loads, all issued before the reduction (independent; they complete while
+    // the partials are summed) -- the serial part below then touches only registers
+    double bd[6];
+    float uu[3];
+    int r_sp = 0, r_ip = 0, r_nr = 0, r_reb = 0, r_status = 0;
+    if (threadIdx.x == 0) {
+        const double* body = D.body + (size_t)b * 6;
+        const float* u = D.u_cur + (size_t)b * 3;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) bd[c] = body[c];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) uu[c] = u[c];
+        r_sp = rs->sp;
+        r_ip = rs->ip;
+        r_nr = rs->need_rebin;
+        r_reb = rs->rebuilds;
+        r_status = rs->status;
+    }
     double4 s = make_double4(0, 0, 0, 0);
     const int np = P.bsplit > 1 ? P.bsplit : P.npart;
     const double4* part = P.bsplit > 1 ? D.part2 + (size_t)b * P.bsplit : D.part + (size_t)b * P.npart;
@@ -1225,7 +1262,11 @@ __device__ __forceinline__ void body_step(const DevParams& P, const DevPtrs& D, 
         }
     if (threadIdx.x < nt) red[threadIdx.x] = s;
     __syncthreads();
-    for (int w = nt / 2; w > 0; w >>= 1) {
+    // Tree over nt slots; slots >= np hold +0 (s starts at +0, so no slot is ever -0): the
+    // levels whose upper halves are all such slots add exact zeros and are skipped (same bits).
+    int w0 = nt / 2;
+    while (w0 >= np && w0 > 1) w0 >>= 1;
+    for (int w = w0; w > 0; w >>= 1) {
         if (threadIdx.x < w) {
             double4 a = red[threadIdx.x], c = red[threadIdx.x + w];
             red[threadIdx.x] = make_double4(a.x + c.x, a.y + c.y, a.z + c.z, fmax(a.w, c.w));
@@ -1234,42 +1275,47 @@ __device__ __forceinline__ void body_step(const DevParams& P, const DevPtrs& D, 
     }
     if (threadIdx.x == 0) {
         double* body = D.body + (size_t)b * 6;
-        const float* u = D.u_cur + (size_t)b * 3;
         const double4 f = red[0];
         double ax = 0.0, ay = 0.0;
         if (!pin) {
-            ax = (f.x + (double)u[0]) / P.m_body;
-            ay = (f.y + (double)u[1]) / P.m_body;
-            const double ath = (f.z + (double)u[2]) / P.J_body;
-            body[3] += P.dtd * ax;
-            body[4] += P.dtd * ay;
-            body[5] += P.dtd * ath;
-            body[0] += P.dtd * body[3];
-            body[1] += P.dtd * body[4];
-            body[2] += P.dtd * body[5];
+            ax = (f.x + (double)uu[0]) / P.m_body;
+            ay = (f.y + (double)uu[1]) / P.m_body;
+            const double ath = (f.z + (double)uu[2]) / P.J_body;
+            bd[3] += P.dtd * ax;
+            bd[4] += P.dtd * ay;
+            bd[5] += P.dtd * ath;
+            bd[0] += P.dtd * bd[3];
+            bd[1] += P.dtd * bd[4];
+            bd[2] += P.dtd * bd[5];
         }
         bool fin = true, big = false;
+#pragma unroll
         for (int c = 0; c < 6; ++c) {
-            sbody[c] = body[c];
-            fin = fin && isfinite(body[c]);
-            big = big || fabs(body[c]) > 1e9;
+            body[c] = bd[c];
+            sbody[c] = bd[c];
+            fin = fin && isfinite(bd[c]);
+            big = big || fabs(bd[c]) > 1e9;
         }
-        if (!fin || big) set_status(rs, fin ? 2 : 1, -1);
-        sincos(body[2], &sbody[7], &sbody[6]);
-        D.geom[b] = Geom{(float)body[0], (float)body[1], (float)((double)body[2] + ghost_angle0),
-                         (float)body[3], (float)body[4], {0.f, 0.f, 0.f}};
-        const int nr = rs->need_rebin;
-        rs->sp = rs->sp ^ nr ^ 1;
-        rs->ip ^= nr;
-        rs->rebuilds += nr;
+        if (!fin || big) {
+            set_status(rs, fin ? 2 : 1, -1);   // (reads rs->step: this substep, before the increment)
+            r_status = 1;
+        }
+        sincos(bd[2], &sbody[7], &sbody[6]);
+        D.geom[b] = Geom{(float)bd[0], (float)bd[1], (float)(bd[2] + ghost_angle0),
+                         (float)bd[3], (float)bd[4], {0.f, 0.f, 0.f}};
+        const int nr = r_nr;
+        rs->sp = r_sp ^ nr ^ 1;
+        rs->ip = r_ip ^ nr;
+        rs->rebuilds = r_reb + nr;
         // max over particles of |(x_i - x_i^build) - (r_n - r^build)| (from k_force) plus the
         // body's drift in this substep: a strict bound on every particle's displacement
         // relative to the body translation since the last rebuild (Verlet criterion)
-        const double d = sqrt(f.w) + P.dtd * sqrt(body[3] * body[3] + body[4] * body[4]);
-        rs->disp = (float)d;
-        rs->need_rebin = P.rebin_every ? 1 : (rs->disp >= P.rebuild_disp ? 1 : 0);
+        const double d = sqrt(f.w) + P.dtd * sqrt(bd[3] * bd[3] + bd[4] * bd[4]);
+        const float disp = (float)d;
+        rs->disp = disp;
+        rs->need_rebin = P.rebin_every ? 1 : (disp >= P.rebuild_disp ? 1 : 0);
         rs->step += 1;
-        if (rs->status) rs->frozen = 1;
+        if (r_status) rs->frozen = 1;
     }
     __syncthreads();
     ghost_update(P, D, b, sbody, threadIdx.x, blockDim.x);
