@@ -231,7 +231,11 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
         const double arg = support / (2.0 * std::sqrt(d_min * R));
         if (!(arg < 1.0)) return false;
         const double dphi = 2.0 * std::asin(arg);
-        *K = (int)std::ceil(dphi * G / (2.0 * M_PI)) + 2;
+        // ghost j lies at index distance |j - c| < dphi G / 2pi from the particle's continuous
+        // index c = (atan2 - th) G / 2pi; the walk centres on j0 = round(c) (|c - j0| <= 1/2);
+        // 0.05 index units (3e-4 rad at C2) cover the float error of atan2f / th / the body
+        // position (~1e-6 rad).  (The ghost-set tests compare against brute force.)
+        *K = (int)std::ceil(dphi * G / (2.0 * M_PI) + 0.5 + 0.05);
         *wall = std::nextafter((float)(d_min * d_min), 0.0f);
         return 2 * *K + 1 < G;
     };
