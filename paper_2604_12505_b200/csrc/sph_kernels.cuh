@@ -319,17 +319,17 @@ __device__ __forceinline__ void finish_density(const DevParams& P, const DevPtrs
 // rollout (global state buffer, shared-memory ring, or the shared-memory copy inside
 // k_rebuild_small); posg(j) that of a cell-scan candidate (list overflow; may lie outside a
 // ring window, so the ring kernel passes a global-memory reader here).
+// wn0 / n: the list's first offset quad and length, loaded by the caller.  (Loading them before
+// k_density's rollout-state check measured 4 us slower on C3; in k_force it pays, see force_tile.)
 template <bool NC, class PosF, class PosG>
 __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& D, int b, int i,
-                                             PosF&& pos, PosG&& posg) {
+                                             PosF&& pos, PosG&& posg, uint2 wn0, int n) {
     const size_t o = (size_t)b * P.N;
     const float2 p = pos((uint32_t)i);
     const float4 xi = make_float4(p.x, p.y, 0.f, 0.f);
     float wf = 4.0f;   // self term W_cb(0) ("all particles"): (2-0)^3 - 4 (1-0)^3 = 4
     const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
-    uint2 wn = ld<NC>(nq);   // first offsets, independent of the count load; then the next
-                             // quad's offsets stay in flight while this one is evaluated
-    const int n = ld<NC>(D.ncnt + o + i);
+    uint2 wn = wn0;   // the next quad's offsets stay in flight while this one is evaluated
     auto as4 = [](float2 v) { return make_float4(v.x, v.y, 0.f, 0.f); };
     if (n != NL_OVERFLOW) {
         for (int k = 0; k < n; k += 4) {
@@ -359,6 +359,15 @@ __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& 
                             [&](uint32_t j) { wf += w_masked(P, xi, as4(posg(j)), j != (uint32_t)i); });
     }
     finish_density(P, D, b, i, p, wf);
+}
+
+template <bool NC, class PosF, class PosG>
+__device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& D, int b, int i,
+                                             PosF&& pos, PosG&& posg) {
+    // first offsets, independent of the count load
+    const uint2 wn = ld<NC>(D.nbr + (size_t)b * KQ * P.N + i);
+    const int n = ld<NC>(D.ncnt + (size_t)b * P.N + i);
+    density_core<NC>(P, D, b, i, pos, posg, wn, n);
 }
 
 template <bool NC, class PosF>
@@ -950,12 +959,11 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
                                                float4 xi, float2 ai,
                                                const float4* __restrict__ pv,
                                                const float2* __restrict__ aux, PV&& pvj, AX&& axj,
-                                               BodyAcc& acc) {
+                                               BodyAcc& acc, uint2 q0, int n) {
+    // q0 / n: the list's first offset quad and length (loaded by the caller, see force_tile)
     const size_t o = (size_t)b * P.N;
     float sx = 0.0f, sy = 0.0f;   // sum of (-pressure + viscous) * grad W / m^2
     const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
-    const uint2 q0 = __ldg(nq);            // first offsets, independent of the count load
-    const int n = D.ncnt[o + i];
 
     if (n != NL_OVERFLOW) {
         force_list(P, nq, n, q0, xi, ai, pvj, axj, sx, sy);
@@ -1045,12 +1053,27 @@ __device__ __forceinline__ void write_partial(const DevParams& P, const DevPtrs&
         D.part[(size_t)b * P.npart + q] = make_double4(a.fbx, a.fby, a.tq, a.vmax);
 }
 
+// List head (first offset quad, length) of slot i of rollout b: independent of the rollout
+// state, so the callers issue it before reading that state.
+__device__ __forceinline__ void list_head(const DevParams& P, const DevPtrs& D, int b, int i,
+                                          uint2& q0, int& n) {
+    q0 = make_uint2(0u, 0u);
+    n = 0;
+    if (i < P.N) {
+        q0 = __ldg(D.nbr + (size_t)b * KQ * P.N + i);
+        n = D.ncnt[(size_t)b * P.N + i];
+    }
+}
+
 template <int TF>
 __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D, float damping,
                                            int b, int tile) {
+    const int i = tile * TF + threadIdx.x;
+    uint2 q0;
+    int n;
+    list_head(P, D, b, i, q0, n);   // (discarded if the rollout is frozen)
     const RolloutState* rs = D.rs + b;
     if (rs->frozen) return;   // CTA-uniform (before any warp-level collective)
-    const int i = tile * TF + threadIdx.x;
     const int cur = rs->sp ^ rs->need_rebin;
     const float4* __restrict__ pv = D.pv[cur] + (size_t)b * P.N;
     const float2* __restrict__ aux = D.aux + (size_t)b * P.NA;
@@ -1060,7 +1083,7 @@ __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D,
         const float2* __restrict__ axi = opaque(aux + i);
         force_particle(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
                        [&](int d) { return __ldg(pvi + d); },
-                       [&](int d) { return __ldg(axi + d); }, acc);
+                       [&](int d) { return __ldg(axi + d); }, acc, q0, n);
     }
     write_partial(P, D, b, i >> 5, acc);
 }
@@ -1106,12 +1129,15 @@ __device__ __forceinline__ void force_ring_chunk(const DevParams& P, const DevPt
         for (int t = ta; t < tb; ++t) {
             const int i = t * SW_T + threadIdx.x;
             BodyAcc acc;
+            uint2 q0;
+            int n;
+            list_head(P, D, b, i, q0, n);
             if (i < P.N) {
                 const float4* __restrict__ pvi = pv + i;
                 const float2* __restrict__ axi = aux + i;
                 force_particle(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
                                [&](int d) { return __ldg(pvi + d); },
-                               [&](int d) { return __ldg(axi + d); }, acc);
+                               [&](int d) { return __ldg(axi + d); }, acc, q0, n);
             }
             write_partial(P, D, b, i >> 5, acc);
         }
@@ -1121,11 +1147,14 @@ __device__ __forceinline__ void force_ring_chunk(const DevParams& P, const DevPt
     ring_walk(P, io, ta, tb, [&](int t) {
         const int i = t * SW_T + threadIdx.x;
         BodyAcc acc;
+        uint2 q0;
+        int n;
+        list_head(P, D, b, i, q0, n);
         if (i < P.N) {
             const uint32_t s = (uint32_t)i & (RING - 1);
             force_particle(P, D, damping, b, i, cur, rs, ring_pv[s], ring_aux[s], pv, aux,
                            [&](int d) { return ring_pv[(uint32_t)(i + d) & (RING - 1)]; },
-                           [&](int d) { return ring_aux[(uint32_t)(i + d) & (RING - 1)]; }, acc);
+                           [&](int d) { return ring_aux[(uint32_t)(i + d) & (RING - 1)]; }, acc, q0, n);
         }
         write_partial(P, D, b, i >> 5, acc);
     });
