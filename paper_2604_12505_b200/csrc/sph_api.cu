@@ -45,6 +45,7 @@ struct sph_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool fork = true;   // small path: rebuild branch concurrent with density/forces (SPH_FORK=0: serial)
     bool pdl = true;    // programmatic dependent launch on the substep chain (SPH_PDL=0: off)
+    int wp = 0;         // warp-persistent density (bit 0) / force (bit 1) kernels, bit 2: no L2 prefetch (SPH_WP)
     bool m2side = true; // small path: forces of the rebuilt rollouts at the end of the rebuild
                         // branch (overlapping the others' forces); SPH_M2SIDE=0: after the join
     float damping_cur = 1.0f;
@@ -211,6 +212,10 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
         P->td = pick("SPH_DTILE", 128);
         P->tf = pick("SPH_FTILE", 64);
         P->tn = pick("SPH_NTILE", 128);
+        // k_force in reverse rollout order (SPH_SNAKE=0: off); C3 A/B, 3 pairs on one box:
+        // force 327.3 -> 326.5 us live, 18.34 -> 18.40 G/s, same bits
+        const char* sn = std::getenv("SPH_SNAKE");
+        P->snake = (sn && sn[0] == '0') ? 0 : 1;
         // L2 prefetch distance: SPH_PF waves ahead (a wave = 148 SMs x resident CTAs per SM at
         // 48 (force) / 64 (density) warps per SM); 0 disables
         const char* e = std::getenv("SPH_PF");
@@ -292,10 +297,26 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
 // ---------------------------------------------------------------------------------------
 // Launch sequencing
 // ---------------------------------------------------------------------------------------
+// CTAs of one full wave of a WP_T-thread kernel (at most one per 32-slot unit of the batch)
+template <class K>
+static int wave_ctas(K kern, const DevParams& P) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, WP_T, 0);
+    const int units = ((P.N + 31) / 32) * P.B;
+    return std::max(1, std::min(std::max(per, 1) * sms, (units + 7) / 8));
+}
+
 static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding, bool pdl = false) {
     pdl = pdl && ctx->pdl;
     const DevParams& P = ctx->P;
     dim3 gp(P.ntile, P.B);
+    if ((ctx->wp & 1) && !P.ring && P.own_lo == 0 && P.own_n == P.N) {
+        launch_k(pdl, k_density_wp, dim3(wave_ctas(k_density_wp, P)), dim3(WP_T), 0, s, P, ctx->D,
+                 skip_rebuilding, (ctx->wp & 4) ? 0 : 1);
+        return;
+    }
     if (P.ring)
         k_density_ring<<<dim3(P.nchunk, P.B), SW_T, kDensityRingSmem, s>>>(P, ctx->D, skip_rebuilding);
     else
@@ -313,6 +334,11 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
     pdl = pdl && ctx->pdl;
     const DevParams& P = ctx->P;
     const int gy = mode == 2 ? std::min(P.B, 64) : P.B;
+    if ((ctx->wp & 2) && mode != 2 && !P.ring && P.own_lo == 0 && P.own_n == P.N) {
+        launch_k(pdl, k_force_wp, dim3(wave_ctas(k_force_wp, P)), dim3(WP_T), 0, s, P, ctx->D,
+                 damping, mode, (ctx->wp & 4) ? 0 : 1);
+        return;
+    }
     if (P.ring)
         k_force_ring<<<dim3(P.nchunk, gy), SW_T, kForceRingSmem, s>>>(P, ctx->D, damping, mode);
     else
@@ -603,6 +629,10 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
         // SPH_PDL=0/1 forces it.
         const char* e = std::getenv("SPH_PDL");
         ctx->pdl = e ? (e[0] == '1') : (P.B < kSmallMinBatch);
+    }
+    {   // warp-persistent k_density_wp / k_force_wp (whole-tank launches only)
+        const char* e = std::getenv("SPH_WP");
+        ctx->wp = (e && P.own_lo == 0 && P.own_n == P.N) ? (std::atoi(e) & 7) : 0;
     }
     ctx->n_sub = tp->substeps_per_sample;
     ctx->ghost_angle0 = (float)a0;

@@ -59,6 +59,7 @@ struct DevParams {
     int nblk, chunk, nchunk;// ring kernels: super-tiles of SW_T slots per rollout, super-tiles
                             // per CTA, CTAs per rollout
     int td, tf, tn;         // slots (threads) per CTA of k_density / k_force / k_nlist_density
+    int snake;              // k_force walks the rollouts last to first (L2 reuse after k_density)
     int bsplit;             // body reduction: 1 = k_body sums the npart partials itself;
                             // > 1 = k_body_reduce first sums bsplit fixed chunks (large tanks;
                             // chosen from N only, so bits never depend on B)

@@ -391,11 +391,13 @@ __device__ __forceinline__ void density_at(const DevParams& P, const DevPtrs& D,
 // starting about one wave later will process -- so its list rows, counts and state come from L2
 // instead of DRAM.  Issued after the thread's own work; 1x traffic (each tile once).
 template <bool FORCE>
-__device__ __forceinline__ void prefetch_ahead(const DevParams& P, const DevPtrs& D, int T, int dist) {
+__device__ __forceinline__ void prefetch_ahead(const DevParams& P, const DevPtrs& D, int T, int dist,
+                                               bool rev = false) {
     if (threadIdx.x != 0 || dist <= 0) return;
     const long long c = (long long)blockIdx.y * gridDim.x + blockIdx.x + dist;
     if (c >= (long long)gridDim.x * gridDim.y) return;
-    const int b = (int)(c / gridDim.x), t0 = P.own_lo + (int)(c % gridDim.x) * T;
+    const int by = (int)(c / gridDim.x);
+    const int b = rev ? (int)gridDim.y - 1 - by : by, t0 = P.own_lo + (int)(c % gridDim.x) * T;
     const int cnt = min(T, P.N - t0);
     if (cnt <= 0) return;
     const size_t o = (size_t)b * P.N;
@@ -1107,10 +1109,127 @@ __global__ void __launch_bounds__(TF, SPH_FORCE_MINB * TILE / TF) k_force(DevPar
             force_tile<TF>(P, D, damping, D.rlist[w], tile);
         return;
     }
-    const int b = blockIdx.y;
+    // snake order: k_density walks the rollouts first to last, k_force last to first, so the
+    // first force CTAs find the rollouts k_density touched last still in L2
+    const int b = P.snake ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
     if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
     force_tile<TF>(P, D, damping, b, tile);
-    prefetch_ahead<true>(P, D, TF, P.pf_f);
+    prefetch_ahead<true>(P, D, TF, P.pf_f, P.snake != 0);
+}
+
+// ---------------------------------------------------------------------------------------
+// Warp-persistent variants (SPH_WP, opt-in for measurement): a grid of one wave; each warp
+// strides over 32-slot units u = (rollout, slot block) of the whole batch (u += all warps).  The
+// next unit's list head is loaded before the current unit's walk and the unit two strides ahead
+// is bulk-prefetched into L2, so a warp's first loads overlap its previous unit's work, and no
+// slot waits for a slower warp of its CTA.  Whole-tank launches only (own_lo = 0, own_n = N).
+// ---------------------------------------------------------------------------------------
+constexpr int WP_T = 256;
+
+template <bool FORCE>
+__device__ __forceinline__ void prefetch_unit(const DevParams& P, const DevPtrs& D, int u, int nu,
+                                              int total) {
+    if ((threadIdx.x & 31) != 0 || u >= total) return;
+    const int b = u / nu, t0 = (u - b * nu) * 32;
+    const int cnt = min(32, P.N - t0);
+    const size_t o = (size_t)b * P.N;
+    auto pf = [](const void* p, size_t bytes) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+        const uintptr_t lo = a & ~(uintptr_t)15, hi = (a + bytes + 15) & ~(uintptr_t)15;
+        bulk_prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
+    };
+    for (int q = 0; q < 3; ++q)
+        pf(D.nbr + (size_t)b * KQ * P.N + (size_t)q * P.N + t0, (size_t)cnt * 8);
+    pf(D.ncnt + o + t0, (size_t)cnt);
+    const RolloutState* rs = D.rs + b;
+    pf(D.pv[rs->sp ^ rs->need_rebin] + o + t0, (size_t)cnt * 16);
+    if (FORCE) {
+        pf(D.aux + (size_t)b * P.NA + t0, (size_t)cnt * 8);
+        pf(D.xb + o + t0, (size_t)cnt * 8);
+    }
+}
+
+// list head of this lane's slot of unit u (zero / 0 past the end)
+__device__ __forceinline__ void unit_head(const DevParams& P, const DevPtrs& D, int u, int nu,
+                                          int total, uint2& q0, int& n) {
+    q0 = make_uint2(0u, 0u);
+    n = 0;
+    if (u < total) {
+        const int b = u / nu, i = (u - b * nu) * 32 + (threadIdx.x & 31);
+        if (i < P.N) {
+            q0 = __ldg(D.nbr + (size_t)b * KQ * P.N + i);
+            n = __ldg(D.ncnt + (size_t)b * P.N + i);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(WP_T, 8) k_density_wp(DevParams P, DevPtrs D, int skip_rebuilding,
+                                                     int pf) {
+    pdl_wait();
+    pdl_trigger();
+    const int nu = (P.N + 31) >> 5;
+    const int total = nu * P.B;
+    const int stride = gridDim.x * (WP_T >> 5);
+    int u = blockIdx.x * (WP_T >> 5) + (threadIdx.x >> 5);
+    int n;
+    uint2 wn;
+    unit_head(P, D, u, nu, total, wn, n);
+    for (; u < total; u += stride) {   // warp-uniform
+        const int b = u / nu, i = (u - b * nu) * 32 + (threadIdx.x & 31);
+        int nn;
+        uint2 wnn;
+        unit_head(P, D, u + stride, nu, total, wnn, nn);
+        if (pf) prefetch_unit<false>(P, D, u + 2 * stride, nu, total);
+        const RolloutState* rs = D.rs + b;
+        if (!(rs->frozen || (skip_rebuilding && rs->need_rebin)) && i < P.N) {
+            const float4* __restrict__ pv = opaque(D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N);
+            auto pos = [&](uint32_t j) {
+                const float4 v = __ldg(pv + j);
+                return make_float2(v.x, v.y);
+            };
+            density_core<true>(P, D, b, i, pos, pos, wn, n);
+        }
+        wn = wnn;
+        n = nn;
+    }
+}
+
+// modes 0 / 1 of k_force (mode 2 keeps the grid kernel)
+__global__ void __launch_bounds__(WP_T, SPH_FORCE_MINB) k_force_wp(DevParams P, DevPtrs D,
+                                                                   float damping, int mode, int pf) {
+    pdl_wait();
+    pdl_trigger();
+    const int nu = (P.N + 31) >> 5;
+    const int total = nu * P.B;
+    const int stride = gridDim.x * (WP_T >> 5);
+    int u = blockIdx.x * (WP_T >> 5) + (threadIdx.x >> 5);
+    int n;
+    uint2 q0;
+    unit_head(P, D, u, nu, total, q0, n);
+    for (; u < total; u += stride) {   // warp-uniform
+        const int b = u / nu, i = (u - b * nu) * 32 + (threadIdx.x & 31);
+        int nn;
+        uint2 qn;
+        unit_head(P, D, u + stride, nu, total, qn, nn);
+        if (pf) prefetch_unit<true>(P, D, u + 2 * stride, nu, total);
+        const RolloutState* rs = D.rs + b;
+        if (!(rs->frozen || (mode == 1 && rs->need_rebin))) {
+            const int cur = rs->sp ^ rs->need_rebin;
+            const float4* __restrict__ pv = D.pv[cur] + (size_t)b * P.N;
+            const float2* __restrict__ aux = D.aux + (size_t)b * P.NA;
+            BodyAcc acc;
+            if (i < P.N) {
+                const float4* __restrict__ pvi = opaque(pv + i);
+                const float2* __restrict__ axi = opaque(aux + i);
+                force_particle(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
+                               [&](int d) { return __ldg(pvi + d); },
+                               [&](int d) { return __ldg(axi + d); }, acc, q0, n);
+            }
+            write_partial(P, D, b, i >> 5, acc);
+        }
+        q0 = qn;
+        n = nn;
+    }
 }
 
 // Ring variant: CTA (x, y) walks super-tiles [x chunk, (x + 1) chunk) of rollout y (modes 0/1)
