@@ -691,7 +691,11 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             ctx->small_smem = smem;
             ctx->small_grid = std::max(1, std::min(P.B, nsm));
         }
-        if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess ||
+        int prio_lo = 0, prio_hi = 0;   // SPH_SIDE_PRIO=1: rebuild branch at the highest priority
+        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+        const char* sp = std::getenv("SPH_SIDE_PRIO");
+        const int side_prio = (sp && sp[0] == '1') ? prio_hi : prio_lo;
+        if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, side_prio)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess)
             return bail("side stream", e);
