@@ -75,8 +75,9 @@ typedef struct {
 /* Time stepping.  rebin_every = 1 rebuilds the cell list and the neighbour lists every
  * substep; 0 rebuilds them only when a particle may have moved (relative to the body
  * translation) by 0.49 skin since the last rebuild.  Cells and lists are then 2h + skin wide
- * (Verlet skin); the float32 predicate |x_i - x_j|^2 < (2h)^2 is re-applied to the current
- * positions every substep, so the neighbour sets are exact in both modes. */
+ * (Verlet skin).  The lists hold every particle within 2h + skin (float32 predicate, reading
+ * A19) and the density / force sums are cut at 2h by the kernels' shape (W and grad W vanish
+ * continuously there, B3), so both modes evaluate the same neighbour sums. */
 typedef struct {
     double dt;                /* fast step > 0                                 */
     int substeps_per_sample;  /* n_sub = T_s / dt >= 1 (multi-rate)    */
@@ -85,6 +86,15 @@ typedef struct {
     int rebuild_path;         /* 0 auto; 1 one CTA per rebuilding rollout in shared memory
                                  (needs (n_cells+1)*4 + 10*n_fluid bytes <= 200 KB, else
                                  SPH_EINVAL); 2 grid-wide multi-kernel counting sort        */
+    int exec_path;            /* how a slow tick runs; every path computes
+                                 the same substep (Algorithm 1):
+                                 0 auto: 3 when the rollout fits a cluster's shared memory and
+                                   B >= 64, else 2 for B*N <= 65536, else 1;
+                                 1 per-substep kernels, one CUDA graph per tick;
+                                 2 one cooperative launch per tick (k_coop);
+                                 3 rollout-resident clusters: one thread-block cluster per
+                                   rollout keeps its particles in distributed shared memory for
+                                   the whole tick (k_resident); SPH_EINVAL if it does not fit  */
 } sph_time_params;
 
 /* PD attitude law tau_k = Kp (theta_ref_k - theta_k) - Kd thetadot_k, ZOH. */
@@ -113,7 +123,8 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
  * in canonical order; body (host double[6]) may be NULL to keep it.  Clears its status. */
 sph_status sph_set_state(sph_ctx* ctx, int rollout, const float* fluid_pv, const double* body);
 
-/* Set all body states from host double[B][6]. */
+/* Set all body states from host double[B][6].  Ghosts and the cell grid follow the new pose; the
+ * rollouts' numerical status (sph_get_status) is kept: a failed rollout stays frozen. */
 sph_status sph_set_body_state(sph_ctx* ctx, const double* body);
 
 /* Copy one rollout's particles to host float[n_fluid][4] (canonical order).  rho (nullable):

@@ -33,7 +33,7 @@ class BodyParams(C.Structure):
 
 class TimeParams(C.Structure):
     _fields_ = [("dt", C.c_double), ("substeps_per_sample", C.c_int), ("rebin_every", C.c_int),
-                ("skin", C.c_double), ("rebuild_path", C.c_int)]
+                ("skin", C.c_double), ("rebuild_path", C.c_int), ("exec_path", C.c_int)]
 
 
 class PdAttitude(C.Structure):
@@ -119,8 +119,10 @@ def body_params(sp) -> BodyParams:
     return BodyParams(sp.m_body, sp.J_body, sp.R)
 
 
-def time_params(sp, rebin_every: int = 1, skin: float = 0.0, rebuild_path: int = 0) -> TimeParams:
-    return TimeParams(sp.dt, int(sp.n_sub), int(rebin_every), float(skin), int(rebuild_path))
+def time_params(sp, rebin_every: int = 1, skin: float = 0.0, rebuild_path: int = 0,
+                exec_path: int = 0) -> TimeParams:
+    return TimeParams(sp.dt, int(sp.n_sub), int(rebin_every), float(skin), int(rebuild_path),
+                      int(exec_path))
 
 
 def _ptr(a):
@@ -139,13 +141,13 @@ class SphContext:
     """One batched ensemble of B identical tanks on one GPU (sph_init_tank)."""
 
     def __init__(self, sp, fluid_pv, ghost_b, n_rollouts: int = 1, rebin_every: int = 1,
-                 skin: float = 0.0, device: int = 0, rebuild_path: int = 0):
+                 skin: float = 0.0, device: int = 0, rebuild_path: int = 0, exec_path: int = 0):
         import torch
         self.torch = torch
         self.L = lib()
         self.device = torch.device("cuda", device)
         self.fp, self.bp = fluid_params(sp), body_params(sp)
-        self.tp = time_params(sp, rebin_every, skin, rebuild_path)
+        self.tp = time_params(sp, rebin_every, skin, rebuild_path, exec_path)
         pv = _host(fluid_pv, np.float32).reshape(-1, 4)
         gb = _host(ghost_b, np.float64).reshape(-1, 2)
         self.N, self.G, self.B = pv.shape[0], gb.shape[0], int(n_rollouts)
@@ -264,12 +266,19 @@ class SphContext:
         on_dev = hasattr(u_seq, "is_cuda") and u_seq.is_cuda
         if on_dev:
             K = int(u_seq.shape[1])
-            u_seq = self._dev_in(u_seq.contiguous())
+            u_seq = self._dev_in(u_seq.contiguous().float())
+            if tuple(u_seq.shape) != (self.B, K, 3):
+                raise SphError(f"u_seq must be [B, K, 3] = [{self.B}, K, 3], got {tuple(u_seq.shape)}")
             if y_out is None:
                 y_out = torch.empty((self.B, K, 6), dtype=torch.float32, device=self.device)
             if u_applied is None:
                 u_applied = torch.empty((self.B, K, 3), dtype=torch.float32, device=self.device)
-            th = None if theta_ref is None else theta_ref.contiguous()
+            for nm, t_, shp in (("y_out", y_out, (self.B, K, 6)), ("u_applied", u_applied, (self.B, K, 3))):
+                if not (t_.is_cuda and t_.dtype == torch.float32 and t_.is_contiguous() and tuple(t_.shape) == shp):
+                    raise SphError(f"{nm} must be a contiguous float32 cuda tensor of shape {shp}")
+            th = None if theta_ref is None else theta_ref.contiguous().float()
+            if th is not None and tuple(th.shape) != (self.B, K):
+                raise SphError(f"theta_ref must be [B, K] = [{self.B}, {K}]")
             pd = None if th is None else PdAttitude(Kp, Kd, th.data_ptr())
             self._check(self.L.sph_rollout_batch(self.ctx, u_seq.data_ptr(), K,
                                                  None if pd is None else C.byref(pd),
@@ -279,9 +288,17 @@ class SphContext:
             return y_out, u_applied
         u_seq = _host(u_seq, np.float32)
         K = u_seq.shape[1]
+        if u_seq.shape != (self.B, K, 3):
+            raise SphError(f"u_seq must be [B, K, 3] = [{self.B}, K, 3], got {u_seq.shape}")
         y = y_out if y_out is not None else np.zeros((self.B, K, 6), np.float32)
         ua = u_applied if u_applied is not None else np.zeros((self.B, K, 3), np.float32)
+        for nm, a_, shp in (("y_out", y, (self.B, K, 6)), ("u_applied", ua, (self.B, K, 3))):
+            if not (isinstance(a_, np.ndarray) and a_.dtype == np.float32 and a_.flags.c_contiguous
+                    and a_.shape == shp):
+                raise SphError(f"{nm} must be a C-contiguous float32 array of shape {shp}")
         th = None if theta_ref is None else _host(theta_ref, np.float32)
+        if th is not None and th.shape != (self.B, K):
+            raise SphError(f"theta_ref must be [B, K] = [{self.B}, {K}]")
         pd = None if th is None else PdAttitude(Kp, Kd, _ptr(th))
         self._check(self.L.sph_rollout_batch(self.ctx, _ptr(u_seq), K,
                                              None if pd is None else C.byref(pd), _ptr(y),

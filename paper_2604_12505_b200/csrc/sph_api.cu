@@ -43,11 +43,10 @@ struct sph_ctx {
     int small_grid = 0;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    bool fork = true;   // small path: rebuild branch concurrent with density/forces (SPH_FORK=0: serial)
-    bool pdl = true;    // programmatic dependent launch on the substep chain (SPH_PDL=0: off)
-    int wp = 0;         // warp-persistent density (bit 0) / force (bit 1) kernels, bit 2: no L2 prefetch (SPH_WP)
+    bool fork = true;   // small path: rebuild branch concurrent with density/forces
+    bool pdl = true;    // programmatic dependent launch on the substep chain
     bool m2side = true; // small path: forces of the rebuilt rollouts at the end of the rebuild
-                        // branch (overlapping the others' forces); SPH_M2SIDE=0: after the join
+                        // branch (overlapping the others' forces)
     float damping_cur = 1.0f;
     // small batches: the substep loop of a tick as one cooperative launch (k_coop)
     bool coop = false;
@@ -74,9 +73,6 @@ struct sph_ctx {
 enum { LV_SUB0 = 0, LV_DEN0, LV_DEN1, LV_F1_0, LV_F1_1, LV_F2_0, LV_F2_1, LV_SUB1, LIVE_SLOTS };
 
 static std::string g_init_err;
-// dynamic shared memory of the ring kernels (state ring; + aux ring for the forces)
-static constexpr size_t kDensityRingSmem = (size_t)RING * 16;
-static constexpr size_t kForceRingSmem = (size_t)RING * 24;
 static const int kSmallMinBatch = 512;   // auto policy: per-rollout-CTA rebuild from this B on
 
 #define CK(expr)                                                                       \
@@ -137,6 +133,8 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
         return *why = "invalid time parameters (dt > 0, substeps_per_sample >= 1, rebin_every in {0,1}, skin >= 0)", false;
     if (tp->rebuild_path < 0 || tp->rebuild_path > 2)
         return *why = "rebuild_path must be 0 (auto), 1 (per-rollout CTA) or 2 (multi-kernel)", false;
+    if (tp->exec_path < 0 || tp->exec_path > 3)
+        return *why = "exec_path must be 0 (auto), 1 (per-substep kernels), 2 (cooperative tick) or 3 (resident clusters)", false;
     if (tp->rebin_every == 0 && !(tp->skin > 0))
         return *why = "adaptive rebinning (rebin_every = 0) needs skin > 0", false;
     const double h = fp->h, R = bp->tank_radius;
@@ -191,37 +189,19 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->RL2 = tp->rebin_every ? P->H2 : RL * RL;      // list radius (2h + skin)^2
     P->rebuild_disp = (float)(0.49 * tp->skin);      // < skin / 2; float rounding of the bound ~1e-4 skin
     P->NA = (N + 1) & ~1;
-    {   // TMA-fed shared-memory ring kernels: opt-in (SPH_RING=1), measured no faster than the
-        // plain gather kernels on C3
-        const char* e = std::getenv("SPH_RING");
-        P->ring = (e && e[0] == '1') ? 1 : 0;
-        const char* c = std::getenv("SPH_RING_CHUNK");
-        P->chunk = (c && std::atoi(c) > 0) ? std::atoi(c) : 4;
-        P->nblk = std::max(1, (N + SW_T - 1) / SW_T);
-        P->chunk = std::min(P->chunk, P->nblk);
-        P->nchunk = (P->nblk + P->chunk - 1) / P->chunk;
-    }
-    {   // CTA sizes of the plain density / force kernels (env SPH_DTILE / SPH_FTILE for sweeps).
-        // Small CTAs win (C3 sweep): a CTA's slot frees only when its
-        // slowest warp ends, and list lengths / wall work differ from warp to warp.
-        auto pick = [](const char* name, int def) {
-            const char* e = std::getenv(name);
-            const int v = e ? std::atoi(e) : def;
-            return (v == 64 || v == 128 || v == 256 || v == 512 || v == 1024) ? v : def;
-        };
-        P->td = pick("SPH_DTILE", 128);
-        P->tf = pick("SPH_FTILE", 64);
-        P->tn = pick("SPH_NTILE", 128);
-        // k_force in reverse rollout order (SPH_SNAKE=0: off); C3 A/B, 3 pairs on one box:
-        // force 327.3 -> 326.5 us live, 18.34 -> 18.40 G/s, same bits
-        const char* sn = std::getenv("SPH_SNAKE");
-        P->snake = (sn && sn[0] == '0') ? 0 : 1;
-        // L2 prefetch distance: SPH_PF waves ahead (a wave = 148 SMs x resident CTAs per SM at
-        // 48 (force) / 64 (density) warps per SM); 0 disables
-        const char* e = std::getenv("SPH_PF");
-        const double waves = e ? std::atof(e) : 1.5;   // sweep: 0.5 16.7, 1 17.1, 2 17.2, 4 16.8 G/s
-        P->pf_f = (int)(waves * 148 * (48 / (P->tf / 32)));
-        P->pf_d = (int)(waves * 148 * (64 / (P->td / 32)));
+    {   // CTA sizes of the plain density / force / list kernels.  Small CTAs win (C3 sweeps,
+        // DESIGN.md section 7): a CTA's slot frees only when its slowest warp ends, and list
+        // lengths / wall work differ from warp to warp.
+        P->td = 128;
+        P->tf = 64;
+        P->tn = 128;
+        // k_force walks the rollouts last to first (L2 reuse after k_density; C3 A/B: force
+        // 327.3 -> 326.5 us live, same bits)
+        P->snake = 1;
+        // L2 prefetch 1.5 waves ahead (a wave = 148 SMs x resident CTAs per SM at 48 (force) /
+        // 64 (density) warps per SM; sweep: 0.5 16.7, 1 17.1, 1.5 17.2, 2 17.2, 4 16.8 G/s)
+        P->pf_f = (int)(1.5 * 148 * (48 / (P->tf / 32)));
+        P->pf_d = (int)(1.5 * 148 * (64 / (P->td / 32)));
     }
     // ghost-ring window (see for_ghost_candidates): only particles farther than d_min from the
     // centre can have a ghost within 2h; their ghosts lie within +-dphi of their polar angle.
@@ -297,30 +277,10 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
 // ---------------------------------------------------------------------------------------
 // Launch sequencing
 // ---------------------------------------------------------------------------------------
-// CTAs of one full wave of a WP_T-thread kernel (at most one per 32-slot unit of the batch)
-template <class K>
-static int wave_ctas(K kern, const DevParams& P) {
-    int dev = 0, sms = 148, per = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, WP_T, 0);
-    const int units = ((P.N + 31) / 32) * P.B;
-    return std::max(1, std::min(std::max(per, 1) * sms, (units + 7) / 8));
-}
-
 static void launch_density(sph_ctx* ctx, cudaStream_t s, int skip_rebuilding, bool pdl = false) {
     pdl = pdl && ctx->pdl;
     const DevParams& P = ctx->P;
-    dim3 gp(P.ntile, P.B);
-    if ((ctx->wp & 1) && !P.ring && P.own_lo == 0 && P.own_n == P.N) {
-        launch_k(pdl, k_density_wp, dim3(wave_ctas(k_density_wp, P)), dim3(WP_T), 0, s, P, ctx->D,
-                 skip_rebuilding, (ctx->wp & 4) ? 0 : 1);
-        return;
-    }
-    if (P.ring)
-        k_density_ring<<<dim3(P.nchunk, P.B), SW_T, kDensityRingSmem, s>>>(P, ctx->D, skip_rebuilding);
-    else
-        switch (P.td) {
+    switch (P.td) {
             case 1024: launch_k(pdl, k_density<1024>, dim3(std::max(1, (P.own_n + 1023) / 1024), P.B), dim3(1024), 0, s, P, ctx->D, skip_rebuilding); break;
             case 512: launch_k(pdl, k_density<512>, dim3(std::max(1, (P.own_n + 511) / 512), P.B), dim3(512), 0, s, P, ctx->D, skip_rebuilding); break;
             case 128: launch_k(pdl, k_density<128>, dim3(std::max(1, (P.own_n + 127) / 128), P.B), dim3(128), 0, s, P, ctx->D, skip_rebuilding); break;
@@ -334,15 +294,7 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
     pdl = pdl && ctx->pdl;
     const DevParams& P = ctx->P;
     const int gy = mode == 2 ? std::min(P.B, 64) : P.B;
-    if ((ctx->wp & 2) && mode != 2 && !P.ring && P.own_lo == 0 && P.own_n == P.N) {
-        launch_k(pdl, k_force_wp, dim3(wave_ctas(k_force_wp, P)), dim3(WP_T), 0, s, P, ctx->D,
-                 damping, mode, (ctx->wp & 4) ? 0 : 1);
-        return;
-    }
-    if (P.ring)
-        k_force_ring<<<dim3(P.nchunk, gy), SW_T, kForceRingSmem, s>>>(P, ctx->D, damping, mode);
-    else
-        switch (P.tf) {
+    switch (P.tf) {
             case 1024: launch_k(pdl, k_force<1024>, dim3(std::max(1, (P.own_n + 1023) / 1024), gy), dim3(1024), 0, s, P, ctx->D, damping, mode); break;
             case 512: launch_k(pdl, k_force<512>, dim3(std::max(1, (P.own_n + 511) / 512), gy), dim3(512), 0, s, P, ctx->D, damping, mode); break;
             case 128: launch_k(pdl, k_force<128>, dim3(std::max(1, (P.own_n + 127) / 128), gy), dim3(128), 0, s, P, ctx->D, damping, mode); break;
@@ -620,20 +572,9 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
     ctx->P = P;
     ctx->fp = *fp;
     ctx->bp = *bp;
-    {
-        const char* e = std::getenv("SPH_M2SIDE");
-        ctx->m2side = !(e && e[0] == '0');
-    }
-    {   // PDL pays for latency-bound small batches (C1 / C2 single tank +4 %); at C3 it is
-        // neutral to -1 %, so it is on below the per-rollout rebuild threshold only.
-        // SPH_PDL=0/1 forces it.
-        const char* e = std::getenv("SPH_PDL");
-        ctx->pdl = e ? (e[0] == '1') : (P.B < kSmallMinBatch);
-    }
-    {   // warp-persistent k_density_wp / k_force_wp (whole-tank launches only)
-        const char* e = std::getenv("SPH_WP");
-        ctx->wp = (e && P.own_lo == 0 && P.own_n == P.N) ? (std::atoi(e) & 7) : 0;
-    }
+    // PDL pays for latency-bound small batches (C1 / C2 single tank +4 %); at C3 it is
+    // neutral to -1 %, so it is on below the per-rollout rebuild threshold only.
+    ctx->pdl = P.B < kSmallMinBatch;
     ctx->n_sub = tp->substeps_per_sample;
     ctx->ghost_angle0 = (float)a0;
     carve(P, (char*)d_workspace, &ctx->D);
@@ -653,16 +594,6 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
         return SPH_ECUDA;
     };
     cudaError_t e;
-    if (P.ring) {   // ring kernels: 48 KB (force) / 32 KB (density) dynamic shared memory
-        cudaError_t e1 = cudaFuncSetAttribute(k_force_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)kForceRingSmem);
-        cudaError_t e2 = cudaFuncSetAttribute(k_density_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)kDensityRingSmem);
-        if (e1 != cudaSuccess || e2 != cudaSuccess) {
-            sph_destroy(ctx);
-            return fail(nullptr, SPH_ECUDA, "cannot raise the ring kernels' shared-memory limit");
-        }
-    }
     // rebuild path: one CTA per rebuilding rollout when its cell table and sort scratch fit in
     // shared memory (rebuild_path 0 = auto, 1 = force per-rollout CTA, 2 = force multi-kernel)
     {
@@ -685,30 +616,19 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             want = false;
         }
         if (want) {
-            const char* f = std::getenv("SPH_FORK");
-            ctx->fork = !(f && f[0] == '0');
             ctx->small = true;
             ctx->small_smem = smem;
             ctx->small_grid = std::max(1, std::min(P.B, nsm));
         }
-        int prio_lo = 0, prio_hi = 0;   // SPH_SIDE_PRIO=1: rebuild branch at the highest priority
-        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-        const char* sp = std::getenv("SPH_SIDE_PRIO");
-        const int side_prio = (sp && sp[0] == '1') ? prio_hi : prio_lo;
-        if ((e = cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, side_prio)) != cudaSuccess ||
+        if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess)
             return bail("side stream", e);
         // k_body: enough threads to reduce the per-warp partials of big tanks (N only)
         while (ctx->body_threads < 1024 && ctx->body_threads * 4 < P.npart) ctx->body_threads *= 2;
-        if (const char* bt = std::getenv("SPH_BODY_T")) {   // sweep override (power of two)
-            const int v = std::atoi(bt);
-            if (v >= 32 && v <= 1024 && (v & (v - 1)) == 0) ctx->body_threads = v;
-        }
-        {   // cooperative tick for latency-bound small batches (SPH_COOP=0/1 forces it)
-            const char* ce = std::getenv("SPH_COOP");
-            bool want = ce ? ce[0] == '1' : ((size_t)P.B * P.N <= 65536 && !ctx->small);
-            want = want && !P.ring && ctx->body_threads <= COOP_T && P.bsplit == 1;
+        {   // cooperative tick for latency-bound small batches (exec_path 2 forces it)
+            bool want = tp->exec_path == 2 || (tp->exec_path == 0 && (size_t)P.B * P.N <= 65536 && !ctx->small);
+            want = want && ctx->body_threads <= COOP_T && P.bsplit == 1;
             int coop_ok = 0, per_sm = 0;
             cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, dev);
             if (want && coop_ok &&
@@ -732,7 +652,7 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             return bail("state copy", e);
         k_import<<<dim3((n_fluid + 255) / 256, P.B), 256, 0, s>>>(P, ctx->D, 0, ctx->D.xfer);
     }
-    k_reset_rollout<<<P.B, BODY_T, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0);
+    k_reset_rollout<<<P.B, BODY_T, 0, s>>>(P, ctx->D, 0, ctx->ghost_angle0, 1);
     if ((e = cudaGetLastError()) != cudaSuccess) return bail("init kernels", e);
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return bail("init sync", e);
     *out = ctx;
@@ -757,7 +677,7 @@ sph_status sph_set_state(sph_ctx* ctx, int rollout, const float* fluid_pv, const
             CK(cudaMemcpyAsync(ctx->D.body + (size_t)b * 6, body, 48, cudaMemcpyHostToDevice, s));
     }
     CK(cudaMemsetAsync(ctx->D.counts + (size_t)b0 * P.ncell, 0, sizeof(uint32_t) * P.ncell * nb, s));
-    k_reset_rollout<<<nb, BODY_T, 0, s>>>(P, ctx->D, b0, ctx->ghost_angle0);
+    k_reset_rollout<<<nb, BODY_T, 0, s>>>(P, ctx->D, b0, ctx->ghost_angle0, 1);
     sph_status st = check_launch(ctx);
     if (st) return st;
     CK(cudaStreamSynchronize(s));
@@ -770,8 +690,8 @@ sph_status sph_set_body_state(sph_ctx* ctx, const double* body) {
     for (int i = 0; i < 6 * P.B; ++i)
         if (!std::isfinite(body[i])) return fail(ctx, SPH_EINVAL, "non-finite body state");
     CK(cudaMemcpyAsync(ctx->D.body, body, 48 * (size_t)P.B, cudaMemcpyHostToDevice, ctx->stream));
-    // keep status / parity, refresh ghosts and the float pose
-    k_reset_rollout<<<P.B, BODY_T, 0, ctx->stream>>>(P, ctx->D, 0, ctx->ghost_angle0);
+    // keep status / freeze / failure record, refresh ghosts and the float pose
+    k_reset_rollout<<<P.B, BODY_T, 0, ctx->stream>>>(P, ctx->D, 0, ctx->ghost_angle0, 0);
     sph_status st = check_launch(ctx);
     if (st) return st;
     CK(cudaStreamSynchronize(ctx->stream));
@@ -843,7 +763,6 @@ sph_status sph_set_domain(sph_ctx* ctx, int slot_lo, int slot_hi) {
     P.own_n = slot_hi - slot_lo;
     // the per-substep kernel path with grid-wide rebuild kernels (no single-launch tick, no
     // per-rollout shared-memory sort, no ring kernels); graphs captured before are stale
-    P.ring = 0;
     P.pf_d = P.pf_f = 0;
     ctx->coop = false;
     ctx->small = false;
@@ -926,7 +845,7 @@ static sph_status accumulate_live(sph_ctx* ctx) {
             CK(el(ev, LV_SUB0, LV_F1_1, &b));
             CK(el(ev, LV_SUB0, LV_F2_0, &c));
             CK(el(ev, LV_SUB0, LV_F2_1, &d));
-            ctx->live_ms[SPH_LIVE_FORCE] += std::max(b, d) - std::min(a, c);
+            ctx->live_ms[SPH_LIVE_FORCE] += (b - a) + (d - c) - std::max(0.0, std::min(b, d) - std::max(a, c));
         } else {
             CK(el(ev, LV_F1_0, LV_F1_1, &ctx->live_ms[SPH_LIVE_FORCE]));
             if (ctx->small && ctx->fork) CK(el(ev, LV_F2_0, LV_F2_1, &ctx->live_ms[SPH_LIVE_FORCE]));
@@ -1272,7 +1191,6 @@ sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr
     if (ctx->jac_bytes < off) {   // grow the cached scratch (kept for the next call)
         CK(cudaStreamSynchronize(s));
         if (ctx->jac_buf) cudaFree(ctx->jac_buf);
-    if (ctx->g1_buf) cudaFree(ctx->g1_buf);
         ctx->jac_buf = nullptr;
         ctx->jac_bytes = 0;
         CK(cudaMalloc(&ctx->jac_buf, off));
@@ -1421,6 +1339,7 @@ void sph_destroy(sph_ctx* ctx) {
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     for (auto e : ctx->live_ev) cudaEventDestroy(e);
     if (ctx->jac_buf) cudaFree(ctx->jac_buf);
+    if (ctx->g1_buf) cudaFree(ctx->g1_buf);
     if (ctx->eig_dbuf) cudaFree(ctx->eig_dbuf);
     if (ctx->solver_params) cusolverDnDestroyParams(ctx->solver_params);
     if (ctx->solver) cusolverDnDestroy(ctx->solver);

@@ -11,9 +11,10 @@
 //              Alg. 1 l.8, kick-then-drift of the fluid, per-CTA body partials
 //   k_body     Eq. tankdynamics fixed-order fp64 reduction, body kick-drift,
 //              Eq. kinematicghost for the next substep, status, rebuild policy
-// The exact float32 neighbour predicate |x_i - x_j|^2 < (2h)^2 (reading A19) is applied to the
-// CURRENT positions inside k_density / k_force; the list is only a superset (Verlet skin), so
-// the neighbour sets are identical to a fresh all-pairs search every substep.
+// The neighbour SETS are fixed by the exact float32 predicate |x_i - x_j|^2 < (2h + skin)^2
+// (reading A19) when the lists are built; inside k_density / k_force the sums are cut at 2h by
+// the kernels' shape (W and dW vanish there, B3), so with the Verlet skin the sums
+// equal those of a fresh all-pairs search every substep.
 // Every rollout owns whole CTAs (blockIdx.y = rollout): results never depend on the batch.
 #pragma once
 #include <cuda_runtime.h>
@@ -53,11 +54,6 @@ struct DevParams {
     float rebuild_disp;     // rebuild when the displacement bound reaches this (< skin / 2)
     int rebin_every;
     int NA;                 // aux row stride per rollout = N rounded up to even (16-B rows)
-    int ring;               // 1: density / force kernels stream the state through a TMA-fed
-                            //    shared-memory ring (rollouts with span <= SW_T); opt-in via
-                            //    env SPH_RING=1 (default 0: plain global-gather kernels)
-    int nblk, chunk, nchunk;// ring kernels: super-tiles of SW_T slots per rollout, super-tiles
-                            // per CTA, CTAs per rollout
     int td, tf, tn;         // slots (threads) per CTA of k_density / k_force / k_nlist_density
     int snake;              // k_force walks the rollouts last to first (L2 reuse after k_density)
     int bsplit;             // body reduction: 1 = k_body sums the npart partials itself;
@@ -130,14 +126,6 @@ struct DevPtrs {
 // ---------------------------------------------------------------------------------------
 // TMA bulk copies (cp.async.bulk global -> shared, completion on an mbarrier)
 // ---------------------------------------------------------------------------------------
-// Ring kernels: a CTA of SW_T threads walks `chunk` consecutive super-tiles of SW_T slots of one
-// rollout; the state of the slots [512 (t - 1), 512 (t + 2)) sits in a 4-block shared-memory ring
-// (slot j at j & (RING - 1)) fed by TMA bulk copies one super-tile ahead.  Every list neighbour
-// of a slot in super-tile t lies in blocks t - 1 .. t + 1 when the rollout's span <= SW_T.
-constexpr int SW_T = 512;
-constexpr int RING_NB = 4;
-constexpr int RING = SW_T * RING_NB;
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }

@@ -293,6 +293,9 @@ __device__ __forceinline__ T ld(const T* p) {
 
 // Wall term gamma1 sum_g W_cb(r_ig) (Eq. density_update), EOS, and the (rho, P/rho^2) store,
 // given the fluid sum wf (self term included, in units of C/h^2).
+// NC = false: coherent loads (k_coop reads ghost rows that an earlier phase of the same launch
+// wrote; the read-only path is only defined for data constant over the whole kernel)
+template <bool NC = true>
 __device__ __forceinline__ void finish_density(const DevParams& P, const DevPtrs& D, int b, int i,
                                                float2 xi, float wf) {
     float wg = 0.0f;
@@ -300,10 +303,10 @@ __device__ __forceinline__ void finish_density(const DevParams& P, const DevPtrs
     const float4* gst = D.gst + (size_t)b * P.G;
     const float2* glo = D.glo + (size_t)b * P.G;
     for_ghost_candidates(P, gm, xi, P.ghost_K, P.wall_r2, [&](int g) {
-        const float4 xg = __ldg(gst + g);
+        const float4 xg = ld<NC>(gst + g);
         const float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
         if (dist2(dx, dy) < P.H2) {
-            const float2 lo = __ldg(glo + g);
+            const float2 lo = ld<NC>(glo + g);
             const float ex = dx - lo.x, ey = dy - lo.y;
             const float r2 = ex * ex + ey * ey;
             wg += wcb_poly(r2 > 0.0f ? r2 * rsqrtf(r2) * P.inv_h : 0.0f);
@@ -316,9 +319,7 @@ __device__ __forceinline__ void finish_density(const DevParams& P, const DevPtrs
 }
 
 // Density + EOS of slot i of rollout b.  pos(j) returns the (x, y) of list neighbour j of the
-// rollout (global state buffer, shared-memory ring, or the shared-memory copy inside
-// k_rebuild_small); posg(j) that of a cell-scan candidate (list overflow; may lie outside a
-// ring window, so the ring kernel passes a global-memory reader here).
+// rollout; posg(j) that of a cell-scan candidate (list overflow).
 // wn0 / n: the list's first offset quad and length, loaded by the caller.  (Loading them before
 // k_density's rollout-state check measured 4 us slower on C3; in k_force it pays, see force_tile.)
 template <bool NC, class PosF, class PosG>
@@ -358,7 +359,7 @@ __device__ __forceinline__ void density_core(const DevParams& P, const DevPtrs& 
         for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), ld<NC>(D.skey + o + i),
                             [&](uint32_t j) { wf += w_masked(P, xi, as4(posg(j)), j != (uint32_t)i); });
     }
-    finish_density(P, D, b, i, p, wf);
+    finish_density<NC>(P, D, b, i, p, wf);
 }
 
 template <bool NC, class PosF, class PosG>
@@ -433,118 +434,6 @@ __global__ void __launch_bounds__(TD) k_density(DevParams P, DevPtrs D, int skip
     const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
     if (i < P.N) density_at<true>(P, D, b, i, pv);
     prefetch_ahead<false>(P, D, TD, P.pf_d);
-}
-
-// ---------------------------------------------------------------------------------------
-// Shared-memory ring (see SW_T): TMA bulk copies of whole super-tile blocks, one mbarrier per
-// ring block, phase parity per block kept in a CTA-uniform bit mask.
-// ---------------------------------------------------------------------------------------
-struct RingIO {
-    float4* s_pv;          // [RING]
-    float2* s_aux;         // [RING] (force) or nullptr (density)
-    uint64_t* bar;         // [RING_NB] "full" barriers (TMA transaction count)
-    uint32_t* rel;         // [RING_NB] warps done with the block in a ring slot
-    const float4* pv;      // rollout's state rows (global)
-    const float2* aux;     // rollout's aux row (global, 16-B aligned: stride NA)
-    const uint2* nbr;      // rollout's neighbour-list rows [KQ][N] (L2 prefetch)
-    uint32_t ph = 0;       // expected parity per ring block (per thread, uniform)
-
-    // one thread: start the copy of super-tile block k into ring block k % RING_NB and prefetch
-    // the list rows of super-tile k - 1 (first used one tile later) into L2
-    __device__ __forceinline__ void issue(const DevParams& P, int k) const {
-        const int cnt = min(SW_T, P.N - k * SW_T);
-        const int r = k & (RING_NB - 1);
-        const uint32_t bp = (uint32_t)cnt * 16u;
-        const uint32_t ba = s_aux ? (uint32_t)((cnt + 1) & ~1) * 8u : 0u;   // even: 16-B multiple
-        mbar_expect_tx(&bar[r], cnt > 0 ? bp + ba : 0u);   // (N = 0: plain arrive)
-        if (cnt <= 0) return;
-        bulk_g2s(s_pv + r * SW_T, pv + (size_t)k * SW_T, bp, &bar[r]);
-        if (s_aux) bulk_g2s(s_aux + r * SW_T, aux + (size_t)k * SW_T, ba, &bar[r]);
-        if (k >= 1) prefetch_lists(P, k - 1);
-    }
-    __device__ __forceinline__ void prefetch_lists(const DevParams& P, int t) const {
-        const int cnt = min(SW_T, P.N - t * SW_T);
-        for (int q = 0; q < KQ; ++q) {
-            const uintptr_t a0 = reinterpret_cast<uintptr_t>(nbr + (size_t)q * P.N + (size_t)t * SW_T);
-            const uintptr_t lo = a0 & ~(uintptr_t)15, hi = (a0 + (uintptr_t)cnt * 8 + 15) & ~(uintptr_t)15;
-            bulk_prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
-        }
-    }
-    // every thread: wait until block k has landed
-    __device__ __forceinline__ void wait(int k) {
-        const int r = k & (RING_NB - 1);
-        mbar_wait(&bar[r], (ph >> r) & 1u);
-        ph ^= 1u << r;
-    }
-};
-
-// Drives one CTA over super-tiles [ta, tb) of a rollout (P.nblk blocks), warps independently.
-// Super-tile t reads blocks t-1 .. t+1, so the chunk needs blocks lo = max(ta-1, 0) .. hi =
-// min(tb, nblk-1).  The prologue fills the ring with blocks lo .. lo+3; block k > lo+3 goes into
-// the slot of block k-4, which the last super-tile reading it (k-3) releases: when a warp
-// finishes super-tile t it releases block t-1, and the last warp to do so starts the copy of
-// block t+3.  A warp waits only for the blocks its next super-tile reads; warps may drift
-// apart by about one super-tile; no CTA barrier inside the walk.
-template <class Body>
-__device__ __forceinline__ void ring_walk(const DevParams& P, RingIO& io, int ta, int tb, Body&& body) {
-    const int nw = blockDim.x >> 5;
-    const int lo = max(ta - 1, 0), hi = min(tb, P.nblk - 1);
-    if (threadIdx.x == 0) {
-        for (int r = 0; r < RING_NB; ++r) {
-            mbar_init(&io.bar[r], 1);
-            io.rel[r] = 0u;
-        }
-        if (ta < P.nblk) io.prefetch_lists(P, ta);
-        for (int k = lo; k <= min(lo + RING_NB - 1, hi); ++k) io.issue(P, k);
-    }
-    __syncthreads();
-    for (int k = lo; k <= min(ta + 1, hi); ++k) io.wait(k);
-    for (int t = ta; t < tb; ++t) {
-        if (t > ta && t + 1 <= hi) io.wait(t + 1);
-        body(t);
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0 && t - 1 >= lo) {
-            const int r = (t - 1) & (RING_NB - 1);
-            __threadfence_block();   // this warp's reads of block t-1 precede the release
-            if (atomicAdd(&io.rel[r], 1u) == (uint32_t)(nw - 1)) {
-                io.rel[r] = 0u;
-                if (t + 3 <= hi && t + 3 > lo + RING_NB - 1) io.issue(P, t + 3);
-            }
-        }
-    }
-    __syncthreads();   // ring reusable (mode 2 walks several rollouts with one CTA)
-}
-
-// Ring variant of k_density: grid (nchunk, B); dynamic smem RING float4.
-__global__ void __launch_bounds__(SW_T, 4) k_density_ring(DevParams P, DevPtrs D, int skip_rebuilding) {
-    extern __shared__ float4 ring_pv[];
-    __shared__ __align__(8) uint64_t bar[RING_NB];
-    __shared__ uint32_t rel[RING_NB];
-    const int b = blockIdx.y;
-    const RolloutState* rs = D.rs + b;
-    if (rs->frozen || (skip_rebuilding && rs->need_rebin)) return;   // CTA-uniform
-    const int ta = blockIdx.x * P.chunk, tb = min(ta + P.chunk, P.nblk);
-    const float4* pv = D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N;
-    auto posg = [&](uint32_t j) {
-        const float4 v = __ldg(pv + j);
-        return make_float2(v.x, v.y);
-    };
-    if (rs->span > SW_T) {   // wide rows (large tanks): plain gathers
-        for (int t = ta; t < tb; ++t) {
-            const int i = t * SW_T + threadIdx.x;
-            if (i < P.N) density_at<true>(P, D, b, i, pv);
-        }
-        return;
-    }
-    RingIO io{ring_pv, nullptr, bar, rel, pv, nullptr, D.nbr + (size_t)b * KQ * P.N};
-    ring_walk(P, io, ta, tb, [&](int t) {
-        const int i = t * SW_T + threadIdx.x;
-        if (i < P.N)
-            density_core<true>(P, D, b, i, [&](uint32_t j) {
-                const float4 v = ring_pv[j & (RING - 1)];
-                return make_float2(v.x, v.y);
-            }, posg);
-    });
 }
 
 // ---------------------------------------------------------------------------------------
@@ -796,12 +685,13 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
 // slot cells and sorted state come from the sort (k_rebuild_small or the grid-wide
 // rebuild kernels); the list just written by a thread is read back by the same thread.
 // lists + density of slot i of the rebuilt rollout b (every lane of the warp calls it)
+template <bool NC = true>
 __device__ __forceinline__ void nlist_density_at(const DevParams& P, const DevPtrs& D, int b, int i) {
     RolloutState* rs = D.rs + b;
     const size_t o = (size_t)b * P.N;
     const float4* __restrict__ pv = opaque(D.pv[rs->sp ^ 1] + o);   // sorted (rebuilt) buffer
     auto pos = [&](uint32_t j) {
-        const float4 v = __ldg(pv + j);
+        const float4 v = ld<NC>(pv + j);
         return make_float2(v.x, v.y);
     };
     int span = 0;
@@ -809,7 +699,7 @@ __device__ __forceinline__ void nlist_density_at(const DevParams& P, const DevPt
         float wf;
         span = build_list_core<true>(P, D, b, i, D.cstart + (size_t)b * (P.ncell + 1),
                                      D.skey[o + i], pos, &wf);
-        if (span >= 0) finish_density(P, D, b, i, pos((uint32_t)i), wf);
+        if (span >= 0) finish_density<NC>(P, D, b, i, pos((uint32_t)i), wf);
         else density_core<false>(P, D, b, i, pos);   // list overflow: cell-scan density
     }
     span = __reduce_max_sync(0xffffffffu, span);
@@ -901,7 +791,7 @@ __device__ __forceinline__ void pair_force(const DevParams& P, float4 xi, float2
 // List walk of the force kernel: four candidates per 8-byte offset load.  PV / AX return the
 // state / aux of a neighbour given its signed slot offset from i (pointer arithmetic relative
 // to slot i's own address: one PRMT/SHF + one LEA pair per neighbour, no 64-bit index math).
-template <class PV, class AX>
+template <bool NC = true, class PV, class AX>
 __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __restrict__ nq, int n,
                                            uint2 q0, float4 xi, float2 ai, PV&& pvj, AX&& axj,
                                            float& sx, float& sy) {
@@ -912,7 +802,7 @@ __device__ __forceinline__ void force_list(const DevParams& P, const uint2* __re
     for (int k = 0; k < n; k += 4) {
         const uint2 w = wn;
         nq += P.N;
-        if (k + 4 < n) wn = __ldg(nq);
+        if (k + 4 < n) wn = ld<NC>(nq);
         // pairs granularity: the second half of a quad only when some lane of the warp needs it
         // (padding entries are the particle itself: exact zero contribution)
         const int d0 = quad_offset(w, 0), d1 = quad_offset(w, 1);
@@ -952,10 +842,10 @@ struct BodyAcc {
 };
 
 // Forces, wall, integration and Verlet displacement of slot i (i < N) of rollout b.
-// pvj(d) / axj(d) read list neighbour i + d (global or ring); pv / aux are the rollout's global
+// pvj(d) / axj(d) read list neighbour i + d; pv / aux are the rollout's global
 // rows (cell-scan fallback of overflowing lists).  The body geometry is loaded after the list
 // walk so it does not occupy registers during it.
-template <class PV, class AX>
+template <bool NC = true, class PV, class AX>
 __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs& D, float damping,
                                                int b, int i, int cur, const RolloutState* rs,
                                                float4 xi, float2 ai,
@@ -968,10 +858,10 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
     const uint2* __restrict__ nq = D.nbr + (size_t)b * KQ * P.N + i;
 
     if (n != NL_OVERFLOW) {
-        force_list(P, nq, n, q0, xi, ai, pvj, axj, sx, sy);
+        force_list<NC>(P, nq, n, q0, xi, ai, pvj, axj, sx, sy);
     } else {
         for_cell_candidates(P, D.cstart + (size_t)b * (P.ncell + 1), D.skey[o + i], [&](uint32_t j) {
-            pair_force(P, xi, ai, __ldg(pv + j), __ldg(aux + j), j != (uint32_t)i, sx, sy);
+            pair_force(P, xi, ai, ld<NC>(pv + j), ld<NC>(aux + j), j != (uint32_t)i, sx, sy);
         });
     }
     const Geom gm = D.geom[b];
@@ -983,10 +873,10 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
     const float cvb = __fdividef(P.m2 * P.beta, ai.x);      // m^2 beta / rho_i
     float tq = 0.0f;
     for_ghost_candidates(P, gm, make_float2(xi.x, xi.y), P.ghost_K1, P.wall1_r2, [&](int g) {
-        const float4 xg = __ldg(gst + g);
+        const float4 xg = ld<NC>(gst + g);
         float dx = __fsub_rn(xi.x, xg.x), dy = __fsub_rn(xi.y, xg.y);
         if (dist2(dx, dy) < P.h2) {
-            const float2 lo = __ldg(glo + g);
+            const float2 lo = ld<NC>(glo + g);
             dx -= lo.x;
             dy -= lo.y;
             const float r2 = dx * dx + dy * dy;
@@ -1000,7 +890,7 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
             const float Gx = c * dx, Gy = c * dy;
             gxs += Gx;
             gys += Gy;
-            const float2 a = __ldg(garm + g);
+            const float2 a = ld<NC>(garm + g);
             tq -= a.x * Gy - a.y * Gx;     // (r_g - r) x (-G_ig)
         }
     });
@@ -1020,7 +910,7 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
     // Verlet criterion on actual displacements: displacement since the last rebuild
     // relative to the body translation since then (k_body adds this step's body drift).
     // vmax carries the squared displacement through the reductions.
-    const float2 xb = __ldg(D.xb + o + i);
+    const float2 xb = ld<NC>(D.xb + o + i);
     const float ddx = (xn.x - xb.x) - (gm.rx - rs->rbx), ddy = (xn.y - xb.y) - (gm.ry - rs->rby);
     acc.vmax = ddx * ddx + ddy * ddy;
     // one test for the common case: the abs-sum is NaN / inf for any non-finite element and
@@ -1057,23 +947,24 @@ __device__ __forceinline__ void write_partial(const DevParams& P, const DevPtrs&
 
 // List head (first offset quad, length) of slot i of rollout b: independent of the rollout
 // state, so the callers issue it before reading that state.
+template <bool NC = true>
 __device__ __forceinline__ void list_head(const DevParams& P, const DevPtrs& D, int b, int i,
                                           uint2& q0, int& n) {
     q0 = make_uint2(0u, 0u);
     n = 0;
     if (i < P.N) {
-        q0 = __ldg(D.nbr + (size_t)b * KQ * P.N + i);
+        q0 = ld<NC>(D.nbr + (size_t)b * KQ * P.N + i);
         n = D.ncnt[(size_t)b * P.N + i];
     }
 }
 
-template <int TF>
+template <int TF, bool NC = true>
 __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D, float damping,
                                            int b, int tile) {
     const int i = tile * TF + threadIdx.x;
     uint2 q0;
     int n;
-    list_head(P, D, b, i, q0, n);   // (discarded if the rollout is frozen)
+    list_head<NC>(P, D, b, i, q0, n);   // (discarded if the rollout is frozen)
     const RolloutState* rs = D.rs + b;
     if (rs->frozen) return;   // CTA-uniform (before any warp-level collective)
     const int cur = rs->sp ^ rs->need_rebin;
@@ -1083,9 +974,9 @@ __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D,
     if (i < P.N) {
         const float4* __restrict__ pvi = opaque(pv + i);
         const float2* __restrict__ axi = opaque(aux + i);
-        force_particle(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
-                       [&](int d) { return __ldg(pvi + d); },
-                       [&](int d) { return __ldg(axi + d); }, acc, q0, n);
+        force_particle<NC>(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
+                           [&](int d) { return ld<NC>(pvi + d); },
+                           [&](int d) { return ld<NC>(axi + d); }, acc, q0, n);
     }
     write_partial(P, D, b, i >> 5, acc);
 }
@@ -1115,185 +1006,6 @@ __global__ void __launch_bounds__(TF, SPH_FORCE_MINB * TILE / TF) k_force(DevPar
     if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
     force_tile<TF>(P, D, damping, b, tile);
     prefetch_ahead<true>(P, D, TF, P.pf_f, P.snake != 0);
-}
-
-// ---------------------------------------------------------------------------------------
-// Warp-persistent variants (SPH_WP, opt-in for measurement): a grid of one wave; each warp
-// strides over 32-slot units u = (rollout, slot block) of the whole batch (u += all warps).  The
-// next unit's list head is loaded before the current unit's walk and the unit two strides ahead
-// is bulk-prefetched into L2, so a warp's first loads overlap its previous unit's work, and no
-// slot waits for a slower warp of its CTA.  Whole-tank launches only (own_lo = 0, own_n = N).
-// ---------------------------------------------------------------------------------------
-constexpr int WP_T = 256;
-
-template <bool FORCE>
-__device__ __forceinline__ void prefetch_unit(const DevParams& P, const DevPtrs& D, int u, int nu,
-                                              int total) {
-    if ((threadIdx.x & 31) != 0 || u >= total) return;
-    const int b = u / nu, t0 = (u - b * nu) * 32;
-    const int cnt = min(32, P.N - t0);
-    const size_t o = (size_t)b * P.N;
-    auto pf = [](const void* p, size_t bytes) {
-        const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-        const uintptr_t lo = a & ~(uintptr_t)15, hi = (a + bytes + 15) & ~(uintptr_t)15;
-        bulk_prefetch_l2(reinterpret_cast<const void*>(lo), (uint32_t)(hi - lo));
-    };
-    for (int q = 0; q < 3; ++q)
-        pf(D.nbr + (size_t)b * KQ * P.N + (size_t)q * P.N + t0, (size_t)cnt * 8);
-    pf(D.ncnt + o + t0, (size_t)cnt);
-    const RolloutState* rs = D.rs + b;
-    pf(D.pv[rs->sp ^ rs->need_rebin] + o + t0, (size_t)cnt * 16);
-    if (FORCE) {
-        pf(D.aux + (size_t)b * P.NA + t0, (size_t)cnt * 8);
-        pf(D.xb + o + t0, (size_t)cnt * 8);
-    }
-}
-
-// list head of this lane's slot of unit u (zero / 0 past the end)
-__device__ __forceinline__ void unit_head(const DevParams& P, const DevPtrs& D, int u, int nu,
-                                          int total, uint2& q0, int& n) {
-    q0 = make_uint2(0u, 0u);
-    n = 0;
-    if (u < total) {
-        const int b = u / nu, i = (u - b * nu) * 32 + (threadIdx.x & 31);
-        if (i < P.N) {
-            q0 = __ldg(D.nbr + (size_t)b * KQ * P.N + i);
-            n = __ldg(D.ncnt + (size_t)b * P.N + i);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(WP_T, 8) k_density_wp(DevParams P, DevPtrs D, int skip_rebuilding,
-                                                     int pf) {
-    pdl_wait();
-    pdl_trigger();
-    const int nu = (P.N + 31) >> 5;
-    const int total = nu * P.B;
-    const int stride = gridDim.x * (WP_T >> 5);
-    int u = blockIdx.x * (WP_T >> 5) + (threadIdx.x >> 5);
-    int n;
-    uint2 wn;
-    unit_head(P, D, u, nu, total, wn, n);
-    for (; u < total; u += stride) {   // warp-uniform
-        const int b = u / nu, i = (u - b * nu) * 32 + (threadIdx.x & 31);
-        int nn;
-        uint2 wnn;
-        unit_head(P, D, u + stride, nu, total, wnn, nn);
-        if (pf) prefetch_unit<false>(P, D, u + 2 * stride, nu, total);
-        const RolloutState* rs = D.rs + b;
-        if (!(rs->frozen || (skip_rebuilding && rs->need_rebin)) && i < P.N) {
-            const float4* __restrict__ pv = opaque(D.pv[rs->sp ^ rs->need_rebin] + (size_t)b * P.N);
-            auto pos = [&](uint32_t j) {
-                const float4 v = __ldg(pv + j);
-                return make_float2(v.x, v.y);
-            };
-            density_core<true>(P, D, b, i, pos, pos, wn, n);
-        }
-        wn = wnn;
-        n = nn;
-    }
-}
-
-// modes 0 / 1 of k_force (mode 2 keeps the grid kernel)
-__global__ void __launch_bounds__(WP_T, SPH_FORCE_MINB) k_force_wp(DevParams P, DevPtrs D,
-                                                                   float damping, int mode, int pf) {
-    pdl_wait();
-    pdl_trigger();
-    const int nu = (P.N + 31) >> 5;
-    const int total = nu * P.B;
-    const int stride = gridDim.x * (WP_T >> 5);
-    int u = blockIdx.x * (WP_T >> 5) + (threadIdx.x >> 5);
-    int n;
-    uint2 q0;
-    unit_head(P, D, u, nu, total, q0, n);
-    for (; u < total; u += stride) {   // warp-uniform
-        const int b = u / nu, i = (u - b * nu) * 32 + (threadIdx.x & 31);
-        int nn;
-        uint2 qn;
-        unit_head(P, D, u + stride, nu, total, qn, nn);
-        if (pf) prefetch_unit<true>(P, D, u + 2 * stride, nu, total);
-        const RolloutState* rs = D.rs + b;
-        if (!(rs->frozen || (mode == 1 && rs->need_rebin))) {
-            const int cur = rs->sp ^ rs->need_rebin;
-            const float4* __restrict__ pv = D.pv[cur] + (size_t)b * P.N;
-            const float2* __restrict__ aux = D.aux + (size_t)b * P.NA;
-            BodyAcc acc;
-            if (i < P.N) {
-                const float4* __restrict__ pvi = opaque(pv + i);
-                const float2* __restrict__ axi = opaque(aux + i);
-                force_particle(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
-                               [&](int d) { return __ldg(pvi + d); },
-                               [&](int d) { return __ldg(axi + d); }, acc, q0, n);
-            }
-            write_partial(P, D, b, i >> 5, acc);
-        }
-        q0 = qn;
-        n = nn;
-    }
-}
-
-// Ring variant: CTA (x, y) walks super-tiles [x chunk, (x + 1) chunk) of rollout y (modes 0/1)
-// or of the work-list entries y, y + gridDim.y, ... (mode 2).  Dynamic smem: RING float4 |
-// RING float2.
-__device__ __forceinline__ void force_ring_chunk(const DevParams& P, const DevPtrs& D,
-                                                 float damping, int b, float4* ring_pv,
-                                                 float2* ring_aux, uint64_t* bar, uint32_t* rel) {
-    const RolloutState* rs = D.rs + b;
-    if (rs->frozen) return;   // CTA-uniform
-    const int ta = blockIdx.x * P.chunk, tb = min(ta + P.chunk, P.nblk);
-    const int cur = rs->sp ^ rs->need_rebin;
-    const float4* __restrict__ pv = D.pv[cur] + (size_t)b * P.N;
-    const float2* __restrict__ aux = D.aux + (size_t)b * P.NA;
-    if (rs->span > SW_T) {   // wide rows: plain gathers
-        for (int t = ta; t < tb; ++t) {
-            const int i = t * SW_T + threadIdx.x;
-            BodyAcc acc;
-            uint2 q0;
-            int n;
-            list_head(P, D, b, i, q0, n);
-            if (i < P.N) {
-                const float4* __restrict__ pvi = pv + i;
-                const float2* __restrict__ axi = aux + i;
-                force_particle(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
-                               [&](int d) { return __ldg(pvi + d); },
-                               [&](int d) { return __ldg(axi + d); }, acc, q0, n);
-            }
-            write_partial(P, D, b, i >> 5, acc);
-        }
-        return;
-    }
-    RingIO io{ring_pv, ring_aux, bar, rel, pv, aux, D.nbr + (size_t)b * KQ * P.N};
-    ring_walk(P, io, ta, tb, [&](int t) {
-        const int i = t * SW_T + threadIdx.x;
-        BodyAcc acc;
-        uint2 q0;
-        int n;
-        list_head(P, D, b, i, q0, n);
-        if (i < P.N) {
-            const uint32_t s = (uint32_t)i & (RING - 1);
-            force_particle(P, D, damping, b, i, cur, rs, ring_pv[s], ring_aux[s], pv, aux,
-                           [&](int d) { return ring_pv[(uint32_t)(i + d) & (RING - 1)]; },
-                           [&](int d) { return ring_aux[(uint32_t)(i + d) & (RING - 1)]; }, acc, q0, n);
-        }
-        write_partial(P, D, b, i >> 5, acc);
-    });
-}
-
-__global__ void __launch_bounds__(SW_T, 3) k_force_ring(DevParams P, DevPtrs D, float damping,
-                                                        int mode) {
-    extern __shared__ float4 ring_pv[];
-    float2* ring_aux = reinterpret_cast<float2*>(ring_pv + RING);
-    __shared__ __align__(8) uint64_t bar[RING_NB];
-    __shared__ uint32_t rel[RING_NB];
-    if (mode == 2) {
-        const int count = *D.rcount;
-        for (int w = blockIdx.y; w < count; w += gridDim.y)
-            force_ring_chunk(P, D, damping, D.rlist[w], ring_pv, ring_aux, bar, rel);
-        return;
-    }
-    const int b = blockIdx.y;
-    if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
-    force_ring_chunk(P, D, damping, b, ring_pv, ring_aux, bar, rel);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1522,14 +1234,15 @@ __global__ void __launch_bounds__(COOP_T, 2) k_coop(DevParams P, DevPtrs D, int 
             const int b = v / P.ntile, i = (v % P.ntile) * TILE + threadIdx.x;
             const RolloutState* rs = D.rs + b;
             if (rs->frozen) continue;                      // CTA-uniform
+            // coherent loads (NC = false): these rows were written earlier in this launch
             if (rs->need_rebin) {
-                nlist_density_at(P, D, b, i);
+                nlist_density_at<false>(P, D, b, i);
             } else if (i < P.N) {
-                density_at<true>(P, D, b, i, D.pv[rs->sp] + (size_t)b * P.N);
+                density_at<false>(P, D, b, i, D.pv[rs->sp] + (size_t)b * P.N);
             }
         }
         grid.sync();
-        for (int v = blockIdx.x; v < nt; v += G) force_tile<TILE>(P, D, damping, v / P.ntile, v % P.ntile);
+        for (int v = blockIdx.x; v < nt; v += G) force_tile<TILE, false>(P, D, damping, v / P.ntile, v % P.ntile);
         grid.sync();
         for (int b = blockIdx.x; b < P.B; b += G)
             if (!D.rs[b].frozen) body_step(P, D, b, pin, ghost_angle0, red, body_nt);
@@ -1622,16 +1335,20 @@ __global__ void k_max_speed(DevParams P, DevPtrs D, float* out) {
     }
 }
 
-__global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angle0) {
+// clear_status = 0 (sph_set_body_state): only the pose-derived data (ghosts, float pose, rebuild
+// flag) is refreshed; a failed rollout keeps its status, freeze and failure record.
+__global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angle0, int clear_status) {
     const int b = b0 + blockIdx.x;
     RolloutState* rs = D.rs + b;
     __shared__ double sbody[8];
     if (threadIdx.x == 0) {
         rs->need_rebin = 1;
-        rs->status = 0;
-        rs->frozen = 0;
-        rs->bad_step = -1;
-        rs->bad_particle = -1;
+        if (clear_status) {
+            rs->status = 0;
+            rs->frozen = 0;
+            rs->bad_step = -1;
+            rs->bad_particle = -1;
+        }
         rs->disp = 0.f;
         const double* body = D.body + (size_t)b * 6;
         for (int c = 0; c < 6; ++c) sbody[c] = body[c];

@@ -126,14 +126,13 @@ def settled_c1():
     return t2.snapped()
 
 
-@pytest.mark.parametrize("rebin_every,path,ring", [(1, 0, 1), (0, 0, 1), (0, 2, 1), (0, 0, 0)])
-def test_200_step_body_trajectory(settled_c1, rebin_every, path, ring, monkeypatch):
-    """ring = 1 (default): TMA-fed shared-memory ring kernels; 0: plain gather kernels."""
-    monkeypatch.setenv("SPH_RING", str(ring))
+@pytest.mark.parametrize("rebin_every,path,ex", [(1, 0, 0), (0, 0, 0), (0, 2, 0), (0, 0, 1), (0, 1, 1)])
+def test_200_step_body_trajectory(settled_c1, rebin_every, path, ex):
+    """ex = exec_path: 0 auto (cooperative tick at this size), 1 per-substep kernels."""
     t = settled_c1
     u = (5.0, 2.0, 1.0)
-    kw = dict(rebuild_path=path) if rebin_every else dict(rebin_every=0, skin=0.2 * t.params.h,
-                                                         rebuild_path=path)
+    kw = dict(rebuild_path=path, exec_path=ex) if rebin_every else dict(
+        rebin_every=0, skin=0.2 * t.params.h, rebuild_path=path, exec_path=ex)
     ctx = _ctx(t, **kw)
     ref = O.State.from_tank(t)
     yg, yo = [], []
@@ -209,17 +208,16 @@ def test_graph_rollout_equals_direct_steps(settled_c1):
 
 
 @pytest.mark.parametrize("path", [1, 2])
-def test_live_timing_nodes_do_not_change_results(settled_c1, path, monkeypatch):
+def test_live_timing_nodes_do_not_change_results(settled_c1, path):
     """Event-record nodes in the tick graph (bench's live kernel timing) leave the trajectory
     bitwise unchanged, and the sampled times are consistent (parts <= whole substep).
-    (Graph path: the cooperative small-batch tick has no per-kernel nodes.)"""
-    monkeypatch.setenv("SPH_COOP", "0")
+    (Graph path, exec_path 1: the cooperative small-batch tick has no per-kernel nodes.)"""
     t = settled_c1
     K = 2
     u = si.ensemble_inputs([3, 4], K)[0]
-    a = _ctx(t, B=2, rebin_every=0, skin=0.15 * t.params.h, rebuild_path=path)
+    a = _ctx(t, B=2, rebin_every=0, skin=0.15 * t.params.h, rebuild_path=path, exec_path=1)
     ya, _ = a.rollout(u)
-    b = _ctx(t, B=2, rebin_every=0, skin=0.15 * t.params.h, rebuild_path=path)
+    b = _ctx(t, B=2, rebin_every=0, skin=0.15 * t.params.h, rebuild_path=path, exec_path=1)
     b.set_live_timing(3)
     yb, _ = b.rollout(u)
     live = b.live_timing()
@@ -230,40 +228,6 @@ def test_live_timing_nodes_do_not_change_results(settled_c1, path, monkeypatch):
     assert b.live_timing()["samples"] == 0   # reset
     a.close()
     b.close()
-
-
-@pytest.mark.parametrize("chunk", [1, 4, 7])
-def test_ring_kernels_match_plain_kernels(chunk, monkeypatch):
-    """The ring kernels (neighbour state from the TMA-fed shared-memory ring) evaluate the same
-    lists in the same order as the plain gather kernels; they differ only in where the compiler
-    contracts multiply-adds (FMA).  C2 tank (19 super-tiles, ragged last one), batch of 3, a
-    strongly forced unsettled start (adaptive rebuilds every few substeps): particle states
-    agree to 1e-4 over 30 substeps (float32 rounding differences, amplified by the violent
-    start), the body trajectory over 2 ticks to 1e-3."""
-    t = si.make_tank(4.0)
-    sp = t.params
-    u = si.ensemble_inputs([11, 12, 13], 2)[0] * 50.0
-    out = []
-    for ring in ("0", "1"):
-        monkeypatch.setenv("SPH_RING", ring)
-        monkeypatch.setenv("SPH_RING_CHUNK", str(chunk))
-        ctx = _ctx(t, B=3, rebin_every=0, skin=0.15 * sp.h)
-        ctx.step(u[:, 0], 30)
-        pv30 = [ctx.get_particles(b) for b in range(3)]
-        reb30 = ctx.counters()[1]
-        ctx.close()
-        ctx = _ctx(t, B=3, rebin_every=0, skin=0.15 * sp.h)
-        y, _ = ctx.rollout(u)
-        assert (ctx.get_status()[0] == 0).all()
-        out.append((pv30, reb30, y))
-        ctx.close()
-    assert t.n_fluid % 512 != 0
-    assert out[1][1].min() >= 2                             # rebuilds within the 30 substeps
-    for b in range(3):
-        assert _rel(out[1][0][b][:, :2], out[0][0][b][:, :2]) <= 1e-4
-        assert _rel(out[1][0][b][:, 2:], out[0][0][b][:, 2:], sp.dt * sp.k / sp.h) <= 1e-4
-    for c in range(6):
-        assert _rel(out[1][2][..., c], out[0][2][..., c], 1e-9) <= 1e-3
 
 
 def test_device_pointer_rollout_equals_host_pointer(settled_c1):
@@ -474,7 +438,7 @@ def test_reading_switches_one_step_parity(over):
 
 
 @pytest.mark.parametrize("ell,B", [(1.0, 1), (1.0, 3), (4.0, 1)])
-def test_cooperative_tick_bitwise_equals_kernel_path(ell, B, monkeypatch):
+def test_cooperative_tick_bitwise_equals_kernel_path(ell, B):
     """Small batches run a whole tick as one cooperative launch (k_coop); its phases use the
     multi-kernel path's per-particle / per-warp / per-rollout arithmetic, so trajectories,
     particle states and rebuild counts are bitwise equal to the per-substep kernels."""
@@ -482,10 +446,9 @@ def test_cooperative_tick_bitwise_equals_kernel_path(ell, B, monkeypatch):
     sp = t.params
     u = si.ensemble_inputs(list(range(B)), 3)[0] * 20.0
     out = []
-    for coop in ("0", "1"):
-        monkeypatch.setenv("SPH_COOP", coop)
-        ctx = _ctx(t, B=B, rebin_every=0, skin=0.15 * sp.h)
-        assert (ctx.launches_per_substep() == 0) == (coop == "1")
+    for ex in (1, 2):
+        ctx = _ctx(t, B=B, rebin_every=0, skin=0.15 * sp.h, exec_path=ex)
+        assert (ctx.launches_per_substep() == 0) == (ex == 2)
         y, ua = ctx.rollout(u)
         ctx.step(u[:, 0], 7)                                   # sph_step path too
         out.append((y, ctx.get_particles(B - 1), ctx.get_body_state(), ctx.counters()[1]))
