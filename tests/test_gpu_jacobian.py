@@ -160,3 +160,20 @@ def test_eigenvalues_library_solver():
     evd = ctx.eigenvalues(torch.from_numpy(M).cuda())
     assert evd.is_cuda and np.allclose(np.sort_complex(evd.cpu().numpy()), np.sort_complex(ev), atol=1e-12)
     ctx.close()
+
+
+def test_jacobian_scratch_growth_keeps_gamma1_buffer_valid():
+    """Scratch ownership on one context: gamma1 estimate -> Jacobian (device pointers) ->
+    Jacobian (host pointers: larger scratch, re-allocated) -> gamma1 estimate.  The gamma1
+    reduction buffer must survive the Jacobian's scratch growth (no use after free): both
+    estimates are identical, and so are both Jacobians."""
+    t = si.moving_tank(1.0, seed=5, vel=0.01)
+    ctx = _ctx(t)
+    w0, g0, s0 = ctx.gamma1_estimate(0)
+    Ad, Bd = ctx.jacobian(0, device=True)
+    Ah, Bh = ctx.jacobian(0, device=False)
+    w1, g1, s1 = ctx.gamma1_estimate(0)
+    assert np.isfinite(w0) and w0 == w1
+    assert np.array_equal(s0, s1) and np.array_equal(np.isnan(g0), np.isnan(g1))
+    assert np.array_equal(Ad.cpu().numpy(), Ah) and np.array_equal(Bd.cpu().numpy(), Bh)
+    ctx.close()
