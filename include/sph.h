@@ -16,8 +16,11 @@
  *  - Errors: every call returns sph_status; nothing throws or aborts across the ABI.
  *    Argument / configuration errors return SPH_EINVAL before any device work.
  *    Numerical failure is per rollout (status 1 non-finite, 2 |x| > 1e9, 3 particle left the
- *    grid = tunnelled): that rollout freezes, the others continue, calls return SPH_OK and
- *    sph_get_status reports it; SPH_EBLOWUP only if every rollout failed.
+ *    grid = tunnelled, 4 resident path only: a CTA's halo outgrew its shared-memory window,
+ *    i.e. more than ~8 particles per cell along a cell row -- a compression the weakly
+ *    compressible fluid does not reach before blowing up): that rollout freezes, the others
+ *    continue, calls return SPH_OK and sph_get_status reports it; SPH_EBLOWUP only if every
+ *    rollout failed.
  *  - Ownership: the caller owns the device workspace and every host buffer; the library never
  *    frees them.  The context owns only CUDA handles (graphs, events) and small staging
  *    buffers for host-pointer calls.
@@ -203,7 +206,10 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms);
  * the force launches overlap the rebuild branch, so these are in-situ durations; the forces of
  * the rebuilt rollouts run on that branch concurrently with the others', and the force time is
  * the union of the two launches' active intervals. */
-enum { SPH_LIVE_DENSITY = 0, SPH_LIVE_FORCE = 1, SPH_LIVE_SUBSTEP = 2, SPH_NUM_LIVE = 3 };
+/* Resident path (exec_path 3): each tick is ONE kernel launch (k_resident: every substep of the
+ * tick for every rollout); every > 0 records CUDA events around every such launch, and
+ * ms_sum[SPH_LIVE_TICK] sums their durations (n_samples counts ticks; the other slots stay 0). */
+enum { SPH_LIVE_DENSITY = 0, SPH_LIVE_FORCE = 1, SPH_LIVE_SUBSTEP = 2, SPH_LIVE_TICK = 3, SPH_NUM_LIVE = 4 };
 sph_status sph_set_live_timing(sph_ctx* ctx, int every);
 sph_status sph_get_live_timing(sph_ctx* ctx, double* ms_sum, int64_t* n_samples, int reset);
 
@@ -317,6 +323,17 @@ sph_status sph_get_counters(sph_ctx* ctx, int64_t* steps, int32_t* rebuilds);
  * 0 when the context runs small batches as one cooperative launch per tick (or per sph_step /
  * sph_settle call) instead of per-substep kernels. */
 int sph_launches_per_substep(const sph_ctx* ctx);
+
+/* Exact number of our kernel launches one slow tick of sph_rollout_batch issues: 1 + n_sub x
+ * (launches per substep) on the per-substep path (sampling kernel + graph), 2 for the
+ * cooperative tick, 1 for the resident path (sampling fused into k_resident); 0 on a NULL ctx. */
+int sph_launches_per_tick(const sph_ctx* ctx);
+
+/* Execution path the context runs (1, 2 or 3, see sph_time_params.exec_path; 0 on NULL) and, for
+ * the resident path, its shape: CTAs per rollout (cluster size), threads per CTA, slots per CTA
+ * and dynamic shared memory per CTA in bytes (any pointer may be NULL). */
+int sph_exec_path(const sph_ctx* ctx, int* cluster_ctas, int* threads, int* slots_per_cta,
+                  int* smem_bytes);
 
 /* Sizes of the context (any pointer may be NULL). */
 void sph_get_sizes(const sph_ctx* ctx, int* n_fluid, int* n_ghost, int* n_rollouts,

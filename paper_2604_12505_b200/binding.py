@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("SPH_LIB_PATH") or os.path.join(_HERE, "libsphb200.so"
 
 SPH_OK, SPH_EINVAL, SPH_ENOMEM, SPH_ECUDA, SPH_EBLOWUP, SPH_ESTATE = 0, 1, 2, 3, 4, 6
 TIMER_NAMES = ["rebuild", "density", "force", "body", "substep"]
-LIVE_NAMES = ["density", "force", "substep"]   # SPH_LIVE_* order
+LIVE_NAMES = ["density", "force", "substep", "tick"]   # SPH_LIVE_* order
 
 
 class FluidParams(C.Structure):
@@ -73,6 +73,8 @@ def lib():
             "sph_set_live_timing": (i32, [vp, i32]),
             "sph_get_live_timing": (i32, [vp, vp, vp, i32]),
             "sph_launches_per_substep": (i32, [vp]),
+            "sph_launches_per_tick": (i32, [vp]),
+            "sph_exec_path": (i32, [vp, vp, vp, vp, vp]),
             "sph_jacobian": (i32, [vp, i32, vp, vp, i32]),
             "sph_eigenvalues": (i32, [vp, i32, vp, vp, i32]),
             "sph_gamma1_estimate": (i32, [vp, i32, dbl, vp, vp, vp]),
@@ -100,7 +102,7 @@ def exported_symbols():
             "sph_get_particles", "sph_get_ghosts", "sph_step", "sph_rollout_batch",
             "sph_get_body_state", "sph_settle", "sph_get_status", "sph_debug_cells",
             "sph_debug_neighbours", "sph_profile_substeps", "sph_set_live_timing", "sph_get_live_timing",
-            "sph_launches_per_substep", "sph_get_counters", "sph_jacobian", "sph_eigenvalues",
+            "sph_launches_per_substep", "sph_launches_per_tick", "sph_exec_path", "sph_get_counters", "sph_jacobian", "sph_eigenvalues",
             "sph_gamma1_estimate", "sph_lpv_scratch_bytes", "sph_lpv_eval", "sph_lpv_adam",
             "sph_set_domain", "sph_dd_phase", "sph_settle_until",
             "sph_get_sizes", "sph_last_error", "sph_destroy"]
@@ -337,7 +339,9 @@ class SphContext:
         self._check(self.L.sph_set_live_timing(self.ctx, int(every)), "sph_set_live_timing")
 
     def live_timing(self, reset: bool = True):
-        """Mean in-situ ms per sampled substep: {"density", "force", "substep", "samples"}."""
+        """Mean in-situ ms per sample: {"density", "force", "substep", "tick", "samples"}
+        (per-substep path: per sampled substep; resident path: "tick" = ms per k_resident
+        launch = one slow tick, samples = ticks)."""
         ms = np.zeros(len(LIVE_NAMES), np.float64)
         n = np.zeros(1, np.int64)
         self._check(self.L.sph_get_live_timing(self.ctx, ms.ctypes.data, n.ctypes.data,
@@ -409,3 +413,13 @@ class SphContext:
 
     def launches_per_substep(self):
         return int(self.L.sph_launches_per_substep(self.ctx))
+
+    def launches_per_tick(self):
+        return int(self.L.sph_launches_per_tick(self.ctx))
+
+    def exec_path(self):
+        """(path, {cluster_ctas, threads, slots_per_cta, smem_bytes}) -- path 1 per-substep
+        kernels, 2 cooperative tick, 3 resident clusters."""
+        v = [C.c_int(0) for _ in range(4)]
+        p = int(self.L.sph_exec_path(self.ctx, *[C.byref(x) for x in v]))
+        return p, dict(zip(["cluster_ctas", "threads", "slots_per_cta", "smem_bytes"], [x.value for x in v]))

@@ -6,7 +6,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", f) for f in ("sph_api.cu", "sph_lpv.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("sph_device.cuh", "sph_kernels.cuh", "sph_jac.cuh",
-                                                       "sph_calib.cuh")] + \
+                                                       "sph_calib.cuh", "sph_resident.cuh")] + \
     [os.path.join(ROOT, "include", "sph.h")]
 OUT = os.path.join(HERE, "libsphb200.so")
 # -ftz=true: denormals never arise in the canonical predicates (coordinates ~1e-3..1 m;

@@ -15,6 +15,7 @@
 
 #include "../../include/sph.h"
 #include "sph_kernels.cuh"
+#include "sph_resident.cuh"
 #include "sph_jac.cuh"
 #include "sph_calib.cuh"
 
@@ -48,6 +49,12 @@ struct sph_ctx {
     bool m2side = true; // small path: forces of the rebuilt rollouts at the end of the rebuild
                         // branch (overlapping the others' forces)
     float damping_cur = 1.0f;
+    // execution path of a tick (sph_time_params.exec_path): 1 per-substep kernels, 2 cooperative
+    // tick, 3 rollout-resident clusters
+    int exec = 1;
+    ResParams res{};     // resident path: cluster shape and shared-memory carve-up
+    int res_nt = 0;      // resident path: threads per CTA
+    cudaEvent_t res_ev[2] = {nullptr, nullptr};
     // small batches: the substep loop of a tick as one cooperative launch (k_coop)
     bool coop = false;
     int coop_grid = 0;
@@ -55,7 +62,7 @@ struct sph_ctx {
     // the density / force launches of every live_every-th substep, read after each tick
     int live_every = 0;
     std::vector<cudaEvent_t> live_ev;   // [sampled substep][LIVE_SLOTS]
-    double live_ms[SPH_NUM_LIVE] = {0, 0, 0};
+    double live_ms[SPH_NUM_LIVE] = {0, 0, 0, 0};
     int64_t live_n = 0;
     // linearization scratch (sph_jacobian), kept between calls
     void* jac_buf = nullptr;
@@ -524,6 +531,137 @@ static sph_status all_failed(sph_ctx* ctx) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Resident path (k_resident, sph_resident.cuh)
+// ---------------------------------------------------------------------------------------
+// Cluster shape and shared-memory carve-up for CS CTAs per rollout; false if it does not fit.
+static bool res_layout(const DevParams& P, int CS, int smem_max, ResParams* out, int* nt_out) {
+    if (P.N <= 0 || P.N >= 65536) return false;
+    ResParams R{};
+    R.CS = CS;
+    R.S = ((P.N + CS - 1) / CS + 31) / 32 * 32;
+    if ((long long)(CS - 1) * R.S >= P.N) return false;          // every CTA owns slots
+    const int units = R.S / 32;
+    const int rounds = (units + RES_MAXT / 32 - 1) / (RES_MAXT / 32);
+    if (rounds > RES_RU) return false;
+    const int nt = 32 * ((units + rounds - 1) / rounds);
+    if (R.S > RES_RU * nt) return false;
+    int idb = 1;
+    while ((1 << idb) < P.N) ++idb;
+    R.IDB = idb;
+    R.idmask = (1u << idb) - 1u;
+    if (((unsigned long long)(P.ncell + 1) << idb) > 0xffffffffull) return false;
+    // halo per side: one cell row + 3 cells at up to 8 particles per cell (rest lattice: 3.8 per
+    // 2h + skin cell; the weakly compressible fluid stays below ~1.35 rho0)
+    R.HCAP = std::min(((P.nx + 3) * 8 + 31) / 32 * 32, (CS - 1) * R.S);
+    R.W = R.S + 2 * R.HCAP;
+    if (R.W > 65535) return false;
+    R.KR = 12;
+    R.KQ = R.KR / 4;
+    R.MCAP = 1024;
+    R.NCT = P.ncell + 2;
+    R.npart = (P.N + 31) / 32;
+    int o = 0;
+    auto put = [&](int* off, long long bytes) {
+        *off = o;
+        o += (int)((bytes + 15) & ~15ll);
+    };
+    put(&R.o_pv, 16ll * R.W);
+    put(&R.o_rpv, 16ll * R.S);
+    put(&R.o_gst, 16ll * std::max(P.G, 1));
+    put(&R.o_glo, 16ll * std::max(P.G, 1));
+    put(&R.o_part, 32ll * R.npart);
+    put(&R.o_aux, 8ll * R.W);
+    put(&R.o_xb, 8ll * R.S);
+    put(&R.o_nbr, 8ll * R.KQ * R.S);
+    put(&R.o_key, 4ll * R.W);
+    put(&R.o_rkey, 4ll * R.S);
+    put(&R.o_nmk, 4ll * R.S);
+    put(&R.o_obk, 4ll * R.S);
+    put(&R.o_mkg, 4ll * R.MCAP);
+    put(&R.o_mks, 4ll * R.MCAP);
+    put(&R.o_wcs, 2ll * R.NCT);
+    put(&R.o_obj, 2ll * R.S);
+    put(&R.o_ncnt, R.S);
+    put(&R.o_misc, sizeof(ResMisc));
+    R.smem = o;
+    if (R.smem > smem_max) return false;
+    *out = R;
+    *nt_out = nt;
+    return true;
+}
+
+static cudaError_t launch_resident(sph_ctx* ctx, const TickArgs& T) {
+    const DevParams& P = ctx->P;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.B * ctx->res.CS);
+    cfg.blockDim = dim3(ctx->res_nt);
+    cfg.dynamicSmemBytes = ctx->res.smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ctx->res.CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const bool timed = ctx->live_every > 0 && T.u_seq != nullptr;
+    if (timed) cudaEventRecord(ctx->res_ev[0], ctx->stream);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_resident, P, ctx->D, ctx->res, T);
+    if (timed) cudaEventRecord(ctx->res_ev[1], ctx->stream);
+    return e;
+}
+
+static TickArgs hold_args(const sph_ctx* ctx, int n, float damping, int pin) {
+    TickArgs T{};
+    T.n_sub = n;
+    T.damping = damping;
+    T.pin = pin;
+    T.ghost_angle0 = ctx->ghost_angle0;
+    return T;
+}
+
+// Resident-path eligibility at init: the smallest cluster (1, 2, 4, 8, 16 CTAs per rollout)
+// whose carve-up fits one CTA's shared memory and that the device can co-schedule.
+static bool res_setup(sph_ctx* ctx) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    for (int CS = 1; CS <= RES_MAXCS; CS *= 2) {
+        ResParams R;
+        int nt = 0;
+        if (!res_layout(ctx->P, CS, optin, &R, &nt)) continue;
+        if (cudaFuncSetAttribute(k_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, R.smem) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (CS > 8 && cudaFuncSetAttribute(k_resident, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(CS * std::max(ctx->P.B, 1));
+        cfg.blockDim = dim3(nt);
+        cfg.dynamicSmemBytes = R.smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CS;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_resident, &cfg) != cudaSuccess || ncl < 1) {
+            cudaGetLastError();
+            continue;
+        }
+        ctx->res = R;
+        ctx->res_nt = nt;
+        return true;
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------------------
 extern "C" {
@@ -640,6 +778,22 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
                 ctx->coop = true;
             }
             cudaGetLastError();
+        }
+    }
+    // resident clusters (exec_path 3, or auto for batches that fill the GPU with clusters)
+    ctx->exec = ctx->coop ? 2 : 1;
+    if (tp->exec_path == 3 || (tp->exec_path == 0 && P.B >= 64)) {
+        const bool ok = res_setup(ctx);
+        if (!ok && tp->exec_path == 3) {
+            sph_destroy(ctx);
+            return fail(nullptr, SPH_EINVAL, "exec_path = 3 but the rollout does not fit a cluster's shared memory (n_fluid < 65536, one cell row of halo per CTA)");
+        }
+        if (ok) {
+            ctx->exec = 3;
+            ctx->coop = false;
+            if ((e = cudaEventCreate(&ctx->res_ev[0])) != cudaSuccess ||
+                (e = cudaEventCreate(&ctx->res_ev[1])) != cudaSuccess)
+                return bail("resident events", e);
         }
     }
     if ((e = cudaMemsetAsync(d_workspace, 0, total, s)) != cudaSuccess) return bail("memset", e);
@@ -766,6 +920,7 @@ sph_status sph_set_domain(sph_ctx* ctx, int slot_lo, int slot_hi) {
     P.pf_d = P.pf_f = 0;
     ctx->coop = false;
     ctx->small = false;
+    ctx->exec = 1;
     if (ctx->tick_graph) {
         cudaGraphExecDestroy(ctx->tick_graph);
         ctx->tick_graph = nullptr;
@@ -816,7 +971,9 @@ sph_status sph_step(sph_ctx* ctx, const float* u, int n_substeps, int ptr_on_dev
         for (int i = 0; i < 3 * P.B; ++i)
             if (!std::isfinite(u[i])) return fail(ctx, SPH_EINVAL, "non-finite input u");
     CK(cudaMemcpyAsync(ctx->D.u_cur, u, ub, ptr_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    if (ctx->coop) {
+    if (ctx->exec == 3) {
+        if (n_substeps > 0) CK(launch_resident(ctx, hold_args(ctx, n_substeps, 1.0f, 0)));
+    } else if (ctx->coop) {
         if (n_substeps > 0) CK(launch_coop(ctx, n_substeps, 1.0f, 0));
     } else {
         for (int k = 0; k < n_substeps; ++k) launch_substep(ctx, 1.0f, 0);
@@ -936,10 +1093,31 @@ sph_status sph_rollout_batch(sph_ctx* ctx, const float* u_seq, int K, const sph_
         du = su;
         dth = pd ? sth : nullptr;
     }
-    sph_status st = ctx->coop ? SPH_OK : capture_tick_graph(ctx);
+    sph_status st = (ctx->coop || ctx->exec == 3) ? SPH_OK : capture_tick_graph(ctx);
     if (st) return st;
     const int tb = 128, tg = (P.B + tb - 1) / tb;
     for (int k = 0; k < K; ++k) {
+        if (ctx->exec == 3) {   // sampling, ZOH / PD input and the n_sub substeps in one launch
+            TickArgs T = hold_args(ctx, ctx->n_sub, 1.0f, 0);
+            T.u_seq = du;
+            T.theta_ref = dth;
+            T.y = dy;
+            T.u_applied = dua;
+            T.K = K;
+            T.k = k;
+            T.pd = pd ? 1 : 0;
+            T.Kp = pd ? pd->Kp : 0.0;
+            T.Kd = pd ? pd->Kd : 0.0;
+            CK(launch_resident(ctx, T));
+            if (ctx->live_every > 0) {
+                CK(cudaEventSynchronize(ctx->res_ev[1]));
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, ctx->res_ev[0], ctx->res_ev[1]));
+                ctx->live_ms[SPH_LIVE_TICK] += ms;
+                ++ctx->live_n;
+            }
+            continue;
+        }
         k_tick<<<tg, tb, 0, s>>>(P, ctx->D, du, dth, dy, dua, K, k, pd ? 1 : 0, pd ? pd->Kp : 0.0, pd ? pd->Kd : 0.0);
         if (ctx->coop) {
             CK(launch_coop(ctx, ctx->n_sub, 1.0f, 0));
@@ -973,7 +1151,9 @@ sph_status sph_get_body_state(sph_ctx* ctx, double* out) {
 sph_status sph_settle(sph_ctx* ctx, double damping, int n_steps) {
     if (!ctx || n_steps < 0 || !(damping > 0 && damping <= 1)) return SPH_EINVAL;
     CK(cudaMemsetAsync(ctx->D.u_cur, 0, sizeof(float) * 3 * ctx->P.B, ctx->stream));
-    if (ctx->coop) {
+    if (ctx->exec == 3) {
+        if (n_steps > 0) CK(launch_resident(ctx, hold_args(ctx, n_steps, (float)damping, 1)));
+    } else if (ctx->coop) {
         if (n_steps > 0) CK(launch_coop(ctx, n_steps, (float)damping, 1));
     } else {
         for (int k = 0; k < n_steps; ++k) launch_substep(ctx, (float)damping, 1);
@@ -1104,6 +1284,22 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
     if (!ctx || !ms || n_substeps < 1) return SPH_EINVAL;
     const DevParams& P = ctx->P;
     cudaStream_t s = ctx->stream;
+    if (ctx->exec == 3) {   // one resident launch of n_substeps (u held): ms per substep
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        cudaEventRecord(e0, s);
+        CK(launch_resident(ctx, hold_args(ctx, n_substeps, 1.0f, 0)));
+        cudaEventRecord(e1, s);
+        CK(cudaEventSynchronize(e1));
+        float m = 0.f;
+        CK(cudaEventElapsedTime(&m, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        for (int t = 0; t < SPH_NUM_TIMERS; ++t) ms[t] = 0.f;
+        ms[SPH_TIMER_SUBSTEP] = m / n_substeps;
+        return SPH_OK;
+    }
     cudaEvent_t ev[5];
     for (auto& e : ev) CK(cudaEventCreate(&e));
     double acc[SPH_NUM_TIMERS] = {0};
@@ -1142,7 +1338,25 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
 }
 
 int sph_launches_per_substep(const sph_ctx* ctx) {
-    return ctx ? (ctx->coop ? 0 : launches_per_substep(ctx)) : 0;   // 0: one cooperative launch per tick
+    // 0: one cooperative / resident launch per tick
+    return ctx ? ((ctx->coop || ctx->exec == 3) ? 0 : launches_per_substep(ctx)) : 0;
+}
+
+int sph_launches_per_tick(const sph_ctx* ctx) {
+    if (!ctx) return 0;
+    if (ctx->exec == 3) return 1;
+    if (ctx->coop) return 2;
+    return 1 + ctx->n_sub * launches_per_substep(ctx);
+}
+
+int sph_exec_path(const sph_ctx* ctx, int* cluster_ctas, int* threads, int* slots_per_cta, int* smem_bytes) {
+    if (!ctx) return 0;
+    const bool r = ctx->exec == 3;
+    if (cluster_ctas) *cluster_ctas = r ? ctx->res.CS : 0;
+    if (threads) *threads = r ? ctx->res_nt : 0;
+    if (slots_per_cta) *slots_per_cta = r ? ctx->res.S : 0;
+    if (smem_bytes) *smem_bytes = r ? ctx->res.smem : 0;
+    return ctx->exec;
 }
 
 sph_status sph_jacobian(sph_ctx* ctx, int rollout, double* A, double* B, int ptr_on_device) {
@@ -1338,6 +1552,8 @@ void sph_destroy(sph_ctx* ctx) {
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     for (auto e : ctx->live_ev) cudaEventDestroy(e);
+    for (auto e : ctx->res_ev)
+        if (e) cudaEventDestroy(e);
     if (ctx->jac_buf) cudaFree(ctx->jac_buf);
     if (ctx->g1_buf) cudaFree(ctx->g1_buf);
     if (ctx->eig_dbuf) cudaFree(ctx->eig_dbuf);

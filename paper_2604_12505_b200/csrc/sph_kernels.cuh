@@ -1285,6 +1285,7 @@ __global__ void k_import(DevParams P, DevPtrs D, int b0, const float4* __restric
     const size_t o = (size_t)b * P.N;
     D.pv[rs->sp][o + i] = in[i];
     D.id[rs->ip][o + i] = (uint32_t)i;
+    D.skey[o + i] = 0u;   // canonical order = sorted by (cell 0, id): a valid start for k_resident
     D.aux[(size_t)b * P.NA + i] = make_float2(0.f, 0.f);
 }
 

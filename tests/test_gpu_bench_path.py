@@ -37,7 +37,7 @@ def c3_start():
     return t, pv
 
 
-@pytest.mark.parametrize("exec_path", [1])
+@pytest.mark.parametrize("exec_path", [1, 3])
 def test_c3_bench_path_three_ticks_vs_oracle_and_batch_invariance(c3_start, exec_path):
     from paper_2604_12505_b200 import SphContext
     t, pv = c3_start
