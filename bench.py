@@ -58,6 +58,9 @@ def parse():
                          "Table 3 benchmark (30 s closed loop); C2CL: the same manoeuvre on the C2 tank (configs[1]); "
                          "none of them is the north-star line")
     ap.add_argument("--rollouts", type=int, default=0, help="override rollouts per GPU")
+    ap.add_argument("--exec-path", type=int, default=0, choices=[0, 1, 2, 3],
+                    help="sph_time_params.exec_path: 0 auto, 1 per-substep kernels + CUDA graph, "
+                         "2 cooperative tick, 3 rollout-resident clusters (opt-in)")
     ap.add_argument("--rebin-every", type=int, default=0,
                     help="1: rebuild cell list + neighbour lists every substep; 0: adaptive (skin)")
     ap.add_argument("--skin", type=float, default=None,
@@ -278,7 +281,7 @@ def run_reference(a):
 # ------------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------------
-def algorithmic_bytes(kernel, N, G, B):
+def algorithmic_bytes(kernel, N, G, B, n_sub=1):
     """Bytes the method must move per launch: float32 SoA arrays
     touched once.  density: read x (8) write (rho, P/rho^2) (8) per particle + ghosts (16);
     force: read x, v (16) + aux (8), write x, v (16) per particle + ghosts (16 + 8).
@@ -287,6 +290,8 @@ def algorithmic_bytes(kernel, N, G, B):
         return B * (16 * N + 16 * G)
     if kernel == "force":
         return B * (40 * N + 24 * G)
+    if kernel == "resident":   # one launch = n_sub whole substeps (density + force) of every rollout
+        return B * n_sub * (56 * N + 40 * G)
     return None
 
 
@@ -323,7 +328,7 @@ def run_ours(a):
     u_host = inputs_for(gids, K_all)                       # [B, K_all, 3]
     skin = a.skin * sp.h if a.rebin_every == 0 else 0.0
     ctx = SphContext(sp, pv0, t.ghost_b, n_rollouts=B, rebin_every=a.rebin_every,
-                     skin=skin, device=local)
+                     skin=skin, device=local, exec_path=a.exec_path)
     u_dev = torch.from_numpy(u_host).to(dev)
     y_dev = torch.empty((B, K_all, 6), dtype=torch.float32, device=dev)
     ua_dev = torch.empty((B, K_all, 3), dtype=torch.float32, device=dev)
@@ -384,24 +389,34 @@ def run_ours(a):
     prof = ctx.profile(a.profile_substeps)
     kern = {k: v for k, v in prof.items() if k != "substep"}
     # dominant kernel and its duration per substep: live in-graph events of the timed region
-    # (k_force = the sum of its launches in a substep); isolated timings as context
-    if live["samples"]:
+    # (k_force = the sum of its launches in a substep); isolated timings as context.
+    # Resident path: the tick is ONE launch (k_resident), timed live around every launch.
+    exec_path, res_shape = ctx.exec_path()
+    if exec_path == 3:
+        top = "resident"
+        kms = live["tick"] if live["samples"] else prof["substep"] * sp.n_sub
+        kms_src = (f"live: CUDA events around every k_resident launch of the timed region "
+                   f"({live['samples']} launches = ticks)" if live["samples"] else
+                   "isolated: sph_profile_substeps after the timed region")
+    elif live["samples"]:
         top = max(("density", "force"), key=lambda k: live[k])
         kms, kms_src = live[top], f"live: CUDA event nodes in the timed tick graph, every {a.live_every}th substep ({live['samples']} samples)"
     else:
         top = max(("density", "force"), key=lambda k: kern[k])
         kms, kms_src = kern[top], "isolated: sph_profile_substeps after the timed region"
-    alg = algorithmic_bytes(top, t.n_fluid, t.n_ghost, B)
+    alg = algorithmic_bytes(top, t.n_fluid, t.n_ghost, B, sp.n_sub)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
     achieved = alg / (kms / 1e3) / 1e9
     roof = {"bound": "hbm", "kernel": f"k_{top}", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic_from_profiles(top, name),
+            "exec_path": exec_path, "resident_shape": res_shape if exec_path == 3 else None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6.65 TB/s",
             "algorithmic_bytes_per_launch": alg, "kernel_ms": kms, "kernel_ms_source": kms_src,
-            "kernel_share_of_substep": kms / live["substep"] if live["samples"] else kms / prof["substep"],
-            "live_ms": {k: live[k] for k in ("density", "force", "substep")},
+            "kernel_share_of_step": (kms * a.steps / ms_max if exec_path == 3 else
+                                     (kms / live["substep"] if live["samples"] else kms / prof["substep"])),
+            "live_ms": {k: live[k] for k in ("density", "force", "substep", "tick")},
             "isolated_ms": kern, "substep_ms_isolated": prof["substep"]}
     # the resource that binds these kernels: instruction issue.  Warp
     # instructions per launch from the committed ncu capture, over the same live time, against
@@ -413,8 +428,7 @@ def run_ours(a):
         roof["issue"] = {"bound": "issue", "achieved": ipk, "peak": ipeak, "unit": "G warp-instructions/s",
                          "frac": ipk / ipeak, "instructions_per_launch": inst,
                          "source": "smsp__inst_executed.sum per launch, profiles/traffic.json (ncu --set full)"}
-    lps = ctx.launches_per_substep()
-    launches = a.steps * (1 + (sp.n_sub * lps if lps > 0 else 1))   # 0: one cooperative launch per tick
+    launches = a.steps * ctx.launches_per_tick()
     ctx.close()
     del ctx
     # ---- e2e: the same ticks through the public API with HOST buffers ----------------------
@@ -427,7 +441,7 @@ def run_ours(a):
     y_pin = [torch.empty((B, 1, 6), dtype=torch.float32).pin_memory() for _ in range(K_e2e)]
     ua_pin = [torch.empty((B, 1, 3), dtype=torch.float32).pin_memory() for _ in range(K_e2e)]
     ctx2 = SphContext(sp, pv0, t.ghost_b, n_rollouts=B, rebin_every=a.rebin_every, skin=skin,
-                      device=local)
+                      device=local, exec_path=a.exec_path)
     if a.warmup > 1:
         ctx2.rollout(u_dev[:, :a.warmup - 1].contiguous(), y_out=y_dev[:, :a.warmup - 1].contiguous(),
                      u_applied=ua_dev[:, :a.warmup - 1].contiguous())

@@ -91,13 +91,13 @@ typedef struct {
                                  SPH_EINVAL); 2 grid-wide multi-kernel counting sort        */
     int exec_path;            /* how a slow tick runs; every path computes
                                  the same substep (Algorithm 1):
-                                 0 auto: 3 when the rollout fits a cluster's shared memory and
-                                   B >= 64, else 2 for B*N <= 65536, else 1;
+                                 0 auto: 2 for B*N <= 65536, else 1;
                                  1 per-substep kernels, one CUDA graph per tick;
                                  2 one cooperative launch per tick (k_coop);
-                                 3 rollout-resident clusters: one thread-block cluster per
-                                   rollout keeps its particles in distributed shared memory for
-                                   the whole tick (k_resident); SPH_EINVAL if it does not fit  */
+                                 3 rollout-resident clusters (opt-in; measured slower than 1
+                                   on C3): one thread-block cluster per rollout
+                                   keeps its particles in distributed shared memory for the
+                                   whole tick (k_resident); SPH_EINVAL if it does not fit     */
 } sph_time_params;
 
 /* PD attitude law tau_k = Kp (theta_ref_k - theta_k) - Kd thetadot_k, ZOH. */

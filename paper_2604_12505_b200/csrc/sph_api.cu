@@ -555,7 +555,7 @@ static bool res_layout(const DevParams& P, int CS, int smem_max, ResParams* out,
     R.HCAP = std::min(((P.nx + 3) * 8 + 31) / 32 * 32, (CS - 1) * R.S);
     R.W = R.S + 2 * R.HCAP;
     if (R.W > 65535) return false;
-    R.KR = 12;
+    R.KR = 16;
     R.KQ = R.KR / 4;
     R.MCAP = 1024;
     R.NCT = P.ncell + 2;
@@ -780,9 +780,11 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             cudaGetLastError();
         }
     }
-    // resident clusters (exec_path 3, or auto for batches that fill the GPU with clusters)
+    // resident clusters (exec_path 3, opt-in)
     ctx->exec = ctx->coop ? 2 : 1;
-    if (tp->exec_path == 3 || (tp->exec_path == 0 && P.B >= 64)) {
+    // (auto never picks it: measured slower than the per-substep kernels on C3 and C3-P0, DESIGN.md
+    // section 7b -- one 19-warp CTA per SM and two cluster barriers per substep)
+    if (tp->exec_path == 3) {
         const bool ok = res_setup(ctx);
         if (!ok && tp->exec_path == 3) {
             sph_destroy(ctx);

@@ -40,7 +40,7 @@ def test_resident_path_is_selected_and_shaped():
     assert ctx.launches_per_tick() == 1
     ctx.close()
     auto = _ctx(t, B=64, rebin_every=0, skin=0.15 * t.params.h, exec_path=0)
-    assert auto.exec_path()[0] == 3
+    assert auto.exec_path()[0] == 1      # opt-in only (measured slower)
     auto.close()
 
 
