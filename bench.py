@@ -38,7 +38,10 @@ WORKLOADS = {
     "C2": (4.0, 1, "C2: single C2 tank (9261 + 944), excitation, latency-bound"),
     "C4": (42.0, 1, "C4: single ell=42 tank (1,025,788 + 9,912)"),
     "C1": (1.0, 1, "C1: single ell=1 tank (569 + 236)"),
+    "C5": (4.0, 8192, "C5: 8192 rollouts of the C2 tank, manoeuvre profiles 1 and 2 under the PD "
+                      "law (P:364-386), sharded by global id, dataset (y, u_applied, status) gathered"),
 }
+K_TRAIN = 2200   # samples of the identification input train: the C3 horizon, 110 s
 METRIC = "particle-updates/sec (device-timed) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "particle-updates/s"
 
@@ -58,6 +61,18 @@ def parse():
                          "Table 3 benchmark (30 s closed loop); C2CL: the same manoeuvre on the C2 tank (configs[1]); "
                          "none of them is the north-star line")
     ap.add_argument("--rollouts", type=int, default=0, help="override rollouts per GPU")
+    ap.add_argument("--window-start", type=int, default=0,
+                    help="C3: first tick (within the 2200-sample train, P:431) of the warm-up; the "
+                         "timed window is ticks [start + W, start + W + K)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="C5: weak = 1024 rollouts per GPU, strong = 8192 in total")
+    ap.add_argument("--long-horizon", action="store_true",
+                    help="C3: run the whole 2200-tick train, report the rate per 100-tick window")
+    ap.add_argument("--horizon-ticks", type=int, default=2200, help="--long-horizon: ticks to run")
+    ap.add_argument("--skin-max", type=float, default=None,
+                    help="adaptive Verlet skin upper bound in units of h (DESIGN.md B5; 0 = fixed skin)")
+    ap.add_argument("--rebuild-path", type=int, default=0, choices=[0, 1, 2],
+                    help="sph_time_params.rebuild_path: 0 auto, 1 per-rollout CTA sort, 2 grid-wide kernels")
     ap.add_argument("--exec-path", type=int, default=0, choices=[0, 1, 2, 3],
                     help="sph_time_params.exec_path: 0 auto, 1 per-substep kernels + CUDA graph, "
                          "2 cooperative tick, 3 rollout-resident clusters (opt-in)")
@@ -318,18 +333,42 @@ def run_ours(a):
     from paper_2604_12505_b200 import SphContext
     name = a.workload
     ell, B, desc = WORKLOADS[name]
+    c5 = name == "C5"
+    if c5:   # strong: 8192 rollouts in total; weak: 1024 per GPU
+        n_total = B if a.scaling == "strong" else 1024 * world
+        from paper_2604_12505_b200.ensemble import shard
+        gids = list(shard(n_total, world, rank))
+        B = len(gids)
     if a.rollouts:
         B = a.rollouts
+    if not c5:
+        gids = list(range(rank * B, (rank + 1) * B))
+        n_total = world * B
     t = make_workload(name)
     sp = t.params
     pv0 = settled_start(t, a.settle_seconds, local)
-    gids = list(range(rank * B, (rank + 1) * B))
     K_all = a.warmup + a.steps
-    u_host = inputs_for(gids, K_all)                       # [B, K_all, 3]
+    w0 = a.window_start
+    th_host = None
+    if c5:   # profiles 1 / 2 from their start, PD attitude law
+        from paper_2604_12505_b200.ensemble import ensemble_inputs_for
+        u_host, th_host = ensemble_inputs_for(gids, K_all, "profiles", n_total)
+        w0 = 0
+        window = {"ticks": [a.warmup, K_all], "seconds": [a.warmup * 0.05, K_all * 0.05],
+                  "inputs": "manoeuvre profiles 1 (ids < n/2) and 2, PD law"}
+    else:    # the 2200-sample identification train; the timed window is a slice of it
+        if w0 + K_all > K_TRAIN:
+            raise SystemExit(f"window [{w0}, {w0 + K_all}) exceeds the {K_TRAIN}-sample train")
+        u_host = np.ascontiguousarray(inputs_for(gids, K_TRAIN)[:, w0:w0 + K_all])
+        window = {"ticks": [w0 + a.warmup, w0 + K_all], "train_samples": K_TRAIN,
+                  "seconds": [(w0 + a.warmup) * 0.05, (w0 + K_all) * 0.05],
+                  "inputs": "open-loop multisine + pulse train (P:430-432)"}
     skin = a.skin * sp.h if a.rebin_every == 0 else 0.0
     ctx = SphContext(sp, pv0, t.ghost_b, n_rollouts=B, rebin_every=a.rebin_every,
-                     skin=skin, device=local, exec_path=a.exec_path)
+                     skin=skin, device=local, exec_path=a.exec_path, rebuild_path=a.rebuild_path, skin_max=a.skin_max * sp.h)
     u_dev = torch.from_numpy(u_host).to(dev)
+    th_dev = torch.from_numpy(th_host).to(dev) if th_host is not None else None
+    pdkw = dict(Kp=sp.Kp, Kd=sp.Kd) if th_host is not None else {}
     y_dev = torch.empty((B, K_all, 6), dtype=torch.float32, device=dev)
     ua_dev = torch.empty((B, K_all, 3), dtype=torch.float32, device=dev)
     # live kernel timing: event-record nodes in the tick graph around density / force of every
@@ -339,10 +378,13 @@ def run_ours(a):
     # warm-up (also captures the per-tick CUDA graph)
     if a.warmup:
         ctx.rollout(u_dev[:, :a.warmup].contiguous(), y_out=y_dev[:, :a.warmup].contiguous(),
-                    u_applied=ua_dev[:, :a.warmup].contiguous())
+                    u_applied=ua_dev[:, :a.warmup].contiguous(),
+                    theta_ref=th_dev[:, :a.warmup].contiguous() if th_dev is not None else None, **pdkw)
     torch.cuda.synchronize(dev)
     ctx.live_timing(reset=True)
+    steps0, reb0 = ctx.counters()
     u_timed = u_dev[:, a.warmup:].contiguous()
+    th_timed = th_dev[:, a.warmup:].contiguous() if th_dev is not None else None
     y_timed = torch.empty((B, a.steps, 6), dtype=torch.float32, device=dev)
     ua_timed = torch.empty((B, a.steps, 3), dtype=torch.float32, device=dev)
     clocks = Clocks(local)
@@ -354,7 +396,7 @@ def run_ours(a):
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.nvtx.range_push("timed")   # ncu --nvtx-include "timed/" selects these launches
     e0.record(ctx.stream)
-    ctx.rollout(u_timed, y_out=y_timed, u_applied=ua_timed)
+    ctx.rollout(u_timed, y_out=y_timed, u_applied=ua_timed, theta_ref=th_timed, **pdkw)
     e1.record(ctx.stream)
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize(dev)
@@ -371,20 +413,23 @@ def run_ours(a):
     st = ctx.get_status()[0]
     n_failed = int((st != 0).sum())
     steps_done, rebuilds = ctx.counters()
+    win_steps, win_reb = steps_done - steps0, rebuilds - reb0   # the timed window only
     y_checksum = float(y_timed.double().abs().sum().item())   # determinism monitor
-    updates = world * B * t.n_fluid * sp.n_sub * a.steps
+    updates = n_total * t.n_fluid * sp.n_sub * a.steps
     value = updates / (ms_max / 1e3)
-    # NCCL gather of the trajectory dataset (config C5; the only collective on the path)
+    # NCCL gather of the trajectory dataset (y, u_applied, status; config C5 -- the only
+    # collective on the path), timed separately after the timed region
     gather_ms = None
     if world > 1:
         g0 = torch.cuda.Event(enable_timing=True)
         g1 = torch.cuda.Event(enable_timing=True)
-        from paper_2604_12505_b200.ensemble import gather_trajectories
+        from paper_2604_12505_b200.ensemble import gather_dataset
         g0.record()
-        out = gather_trajectories(y_timed)
+        yg, uag, stg = gather_dataset(y_timed, ua_timed, torch.from_numpy(st).to(dev))
         g1.record()
         torch.cuda.synchronize(dev)
         gather_ms = g0.elapsed_time(g1)
+        assert yg.shape[0] == n_total
     # ---- per-kernel device times (CUDA events on the context stream, same data) -----------
     prof = ctx.profile(a.profile_substeps)
     kern = {k: v for k, v in prof.items() if k != "substep"}
@@ -438,17 +483,21 @@ def run_ours(a):
     K_e2e = a.steps
     u_pin = [torch.from_numpy(np.ascontiguousarray(u_host[:, a.warmup + k:a.warmup + k + 1])).pin_memory()
              for k in range(K_e2e)]
+    th_pin = [torch.from_numpy(np.ascontiguousarray(th_host[:, a.warmup + k:a.warmup + k + 1])).pin_memory()
+              for k in range(K_e2e)] if th_host is not None else None
     y_pin = [torch.empty((B, 1, 6), dtype=torch.float32).pin_memory() for _ in range(K_e2e)]
     ua_pin = [torch.empty((B, 1, 3), dtype=torch.float32).pin_memory() for _ in range(K_e2e)]
     ctx2 = SphContext(sp, pv0, t.ghost_b, n_rollouts=B, rebin_every=a.rebin_every, skin=skin,
-                      device=local, exec_path=a.exec_path)
+                      device=local, exec_path=a.exec_path, rebuild_path=a.rebuild_path, skin_max=a.skin_max * sp.h)
     if a.warmup > 1:
         ctx2.rollout(u_dev[:, :a.warmup - 1].contiguous(), y_out=y_dev[:, :a.warmup - 1].contiguous(),
-                     u_applied=ua_dev[:, :a.warmup - 1].contiguous())
+                     u_applied=ua_dev[:, :a.warmup - 1].contiguous(),
+                     theta_ref=th_dev[:, :a.warmup - 1].contiguous() if th_dev is not None else None, **pdkw)
     if a.warmup:   # the last warm-up tick through the host-pointer path (allocates its staging)
         uw = torch.from_numpy(np.ascontiguousarray(u_host[:, a.warmup - 1:a.warmup])).pin_memory()
+        thw = (np.ascontiguousarray(th_host[:, a.warmup - 1:a.warmup]) if th_host is not None else None)
         ctx2.rollout(uw.numpy(), y_out=torch.empty((B, 1, 6)).pin_memory().numpy(),
-                     u_applied=torch.empty((B, 1, 3)).pin_memory().numpy())
+                     u_applied=torch.empty((B, 1, 3)).pin_memory().numpy(), theta_ref=thw, **pdkw)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -456,14 +505,15 @@ def run_ours(a):
     x1 = torch.cuda.Event(enable_timing=True)
     x0.record(ctx2.stream)
     for k in range(K_e2e):
-        ctx2.rollout(u_pin[k].numpy(), y_out=y_pin[k].numpy(), u_applied=ua_pin[k].numpy())
+        ctx2.rollout(u_pin[k].numpy(), y_out=y_pin[k].numpy(), u_applied=ua_pin[k].numpy(),
+                     theta_ref=th_pin[k].numpy() if th_pin is not None else None, **pdkw)
     x1.record(ctx2.stream)
     torch.cuda.synchronize(dev)
     e2e_ms = x0.elapsed_time(x1)
     e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * B * t.n_fluid * sp.n_sub * K_e2e / (float(e2e_t.item()) / 1e3)
+    e2e_value = n_total * t.n_fluid * sp.n_sub * K_e2e / (float(e2e_t.item()) / 1e3)
     y_e2e = np.concatenate([y.numpy() for y in y_pin], axis=1)
     e2e_matches = bool(np.array_equal(y_e2e, y_timed.cpu().numpy()))
     ctx2.close()
@@ -478,19 +528,20 @@ def run_ours(a):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (body f64)",
-        "data": "synthetic (seeded lattice tank, " + ("oracle-settled snapshot" if SETTLE_INFO.get("source", "").startswith("bench_data") else "GPU damped settle") + ", multisine+pulse excitation)",
+        "scaling": a.scaling if c5 else "weak", "vs_baseline": None, "dtype": "f32 (body f64)",
+        "data": "synthetic (seeded lattice tank, " + ("oracle-settled snapshot" if SETTLE_INFO.get("source", "").startswith("bench_data") else "GPU damped settle") + (", manoeuvre profiles 1/2 + PD law)" if c5 else ", multisine+pulse excitation)"),
         "config": {"workload": desc, "rollouts_per_gpu": B, "fluid_per_rollout": t.n_fluid,
                    "ghosts_per_rollout": t.n_ghost, "substeps_per_step": sp.n_sub,
-                   "dt": sp.dt, "rebin_every": a.rebin_every, "skin_h": a.skin,
+                   "dt": sp.dt, "rebin_every": a.rebin_every, "skin_h": a.skin, "skin_max_h": a.skin_max,
                    "parallelism": f"ensemble dp{world}",
                    "l2": (f"no flush: working set {ctx_bytes_gb(t, B):.2f} GB > 126 MB L2"
                           if ctx_bytes_gb(t, B) > 0.126 else
                           f"working set {ctx_bytes_gb(t, B):.3f} GB fits the 126 MB L2 (not flushed)"),
                    "failed_rollouts": n_failed, "gather_ms": gather_ms, "settle": SETTLE_INFO,
-                   "substeps_per_rebuild": float(steps_done.mean() / max(rebuilds.mean(), 1)),
+                   "timed_window": window, "rollouts_total": n_total,
+                   "substeps_per_rebuild": float(win_steps.mean() / max(win_reb.mean(), 1e-9)),
                    "y_checksum": y_checksum},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * 3 * 4,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": B * (3 + (1 if c5 else 0)) * 4,
                 "d2h_bytes_per_step": B * (6 + 3) * 4, "steps": K_e2e,
                 "same_ticks_as_timed_region": True, "y_bitwise_equal_to_timed_region": e2e_matches},
         "gpu_launches": launches,
@@ -498,6 +549,59 @@ def run_ours(a):
         "roofline": roof,
         "cpu_baseline": cpu,
     }
+    print(json.dumps(line), flush=True)
+
+
+def run_horizon(a):
+    """--long-horizon: the C3 batch over the WHOLE 2200-sample identification train (110 s,
+    P:431), timed per 100-tick window with CUDA events (one host sync per window), with the
+    rebuild count per window: how the rate moves as the excitation proceeds."""
+    import torch
+    from paper_2604_12505_b200 import SphContext
+    _, _, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ell, B, desc = WORKLOADS["C3"]
+    if a.rollouts:
+        B = a.rollouts
+    t = make_workload("C3")
+    sp = t.params
+    pv0 = settled_start(t, a.settle_seconds, local)
+    u = torch.from_numpy(inputs_for(range(B), K_TRAIN)).to(dev)
+    ctx = SphContext(sp, pv0, t.ghost_b, n_rollouts=B, rebin_every=0, skin=a.skin * sp.h,
+                     device=local, exec_path=a.exec_path, rebuild_path=a.rebuild_path, skin_max=a.skin_max * sp.h)
+    y = torch.empty((B, K_TRAIN, 6), dtype=torch.float32, device=dev)
+    ua = torch.empty((B, K_TRAIN, 3), dtype=torch.float32, device=dev)
+    win = 100
+    rows = []
+    clocks = Clocks(local)
+    clocks.start()
+    n_ticks = min(K_TRAIN, a.horizon_ticks)
+    for w0 in range(0, n_ticks, win):
+        s0, r0 = ctx.counters()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ctx.stream)
+        yw, uaw = y[:, w0:w0 + win].contiguous(), ua[:, w0:w0 + win].contiguous()
+        ctx.rollout(u[:, w0:w0 + win].contiguous(), y_out=yw, u_applied=uaw)
+        e1.record(ctx.stream)
+        torch.cuda.synchronize(dev)
+        y[:, w0:w0 + win] = yw
+        ms = e0.elapsed_time(e1)
+        s1, r1 = ctx.counters()
+        st = ctx.get_status()[0]
+        rows.append({"ticks": [w0, w0 + win], "seconds": [w0 * 0.05, (w0 + win) * 0.05],
+                     "value": B * t.n_fluid * sp.n_sub * win / (ms / 1e3), "ms_per_tick": ms / win,
+                     "substeps_per_rebuild": float((s1 - s0).mean() / max((r1 - r0).mean(), 1e-9)),
+                     "failed_rollouts": int((st != 0).sum())})
+        print(json.dumps(rows[-1]), flush=True)
+    ck = clocks.stop()
+    tot_ms = sum(r["ms_per_tick"] * win for r in rows)
+    line = {"metric": METRIC, "mode": "long-horizon", "workload": desc, "rollouts": B,
+            "train_ticks": n_ticks, "value": B * t.n_fluid * sp.n_sub * n_ticks / (tot_ms / 1e3),
+            "unit": UNIT, "exec_path": ctx.exec_path()[0], "skin_h": a.skin, "skin_max_h": a.skin_max,
+            "windows": rows,
+            "clocks": ck, "y_finite": bool(torch.isfinite(y).all().item())}
+    ctx.close()
     print(json.dumps(line), flush=True)
 
 
@@ -940,6 +1044,8 @@ def main():
     a = parse()
     if a.skin is None:
         a.skin = {"P0": 0.5, "C2CL": 0.5, "SETTLE": 0.5, "C4": 0.8}.get(a.workload, 0.15)
+    if a.skin_max is None:
+        a.skin_max = 0.0
     if a.settle_seconds is None:
         # C4: lattice start + 1,000 untimed damped warm-up substeps; dt = 1 ms / 42
         a.settle_seconds = 1000 * 1e-3 / 42.0 if a.workload == "C4" else 4.0
@@ -957,6 +1063,9 @@ def main():
         return
     if a.workload == "C4DD":
         run_dd(a)
+        return
+    if a.long_horizon:
+        run_horizon(a)
         return
     if a.impl == "reference":
         run_reference(a)

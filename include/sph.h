@@ -98,6 +98,11 @@ typedef struct {
                                    on C3): one thread-block cluster per rollout
                                    keeps its particles in distributed shared memory for the
                                    whole tick (k_resident); SPH_EINVAL if it does not fit     */
+    double skin_max;          /* 0: fixed skin.  > skin: adaptive skin per rollout (B5):
+                                 at every rebuild the skin is scaled by sqrt(8 / I), I = substeps
+                                 the previous lists lasted, within [skin, skin_max]; cells are
+                                 2h + skin_max wide.  The lists hold every pair within the
+                                 rollout's current 2h + skin, so the sums are unchanged.      */
 } sph_time_params;
 
 /* PD attitude law tau_k = Kp (theta_ref_k - theta_k) - Kd thetadot_k, ZOH. */
@@ -191,7 +196,8 @@ enum {
     SPH_TIMER_REBUILD = 0,  /* cell sort + neighbour lists of the rollouts that need it (small
                                path: also their densities)                                 */
     SPH_TIMER_DENSITY = 1, SPH_TIMER_FORCE = 2, SPH_TIMER_BODY = 3, SPH_TIMER_SUBSTEP = 4,
-    SPH_NUM_TIMERS = 5
+    SPH_TIMER_SORT = 5,     /* the cell-sort part of SPH_TIMER_REBUILD (plan + sort kernels)     */
+    SPH_NUM_TIMERS = 6
 };
 sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms);
 

@@ -149,7 +149,10 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->N = N;
     P->G = G;
     P->B = B;
-    const double Cd = 2.0 * h + (tp->rebin_every ? 0.0 : tp->skin);
+    if (!(tp->skin_max >= 0.0) || (tp->skin_max > 0.0 && tp->skin_max < tp->skin))
+        return *why = "skin_max must be 0 (fixed skin) or >= skin", false;
+    const double skin_cell = tp->rebin_every ? 0.0 : std::max(tp->skin, tp->skin_max);
+    const double Cd = 2.0 * h + skin_cell;
     P->C = (float)Cd;
     P->inv_C = 1.0f / P->C;
     const int half_cells = (int)std::ceil(R / (double)P->C) + 2;
@@ -192,9 +195,10 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->m_body = bp->m;
     P->J_body = bp->J;
     P->rebin_every = tp->rebin_every;
-    const float RL = (float)(2.0 * h + (tp->rebin_every ? 0.0 : tp->skin));
-    P->RL2 = tp->rebin_every ? P->H2 : RL * RL;      // list radius (2h + skin)^2
-    P->rebuild_disp = (float)(0.49 * tp->skin);      // < skin / 2; float rounding of the bound ~1e-4 skin
+    // list radius fl(2h + skin)^2 and rebuild threshold 0.49 skin per rollout (skin_set, B4 / B5)
+    P->h2d = 2.0 * h;
+    P->skin0 = tp->rebin_every ? 0.0f : (float)tp->skin;
+    P->skin_max = tp->rebin_every ? 0.0f : (float)tp->skin_max;
     P->NA = (N + 1) & ~1;
     {   // CTA sizes of the plain density / force / list kernels.  Small CTAs win (C3 sweeps,
         // DESIGN.md section 7): a CTA's slot frees only when its slowest warp ends, and list
@@ -1302,7 +1306,7 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
         ms[SPH_TIMER_SUBSTEP] = m / n_substeps;
         return SPH_OK;
     }
-    cudaEvent_t ev[5];
+    cudaEvent_t ev[6];   // (ev[5]: between the sort and the lists of the rebuild timer)
     for (auto& e : ev) CK(cudaEventCreate(&e));
     double acc[SPH_NUM_TIMERS] = {0};
     dim3 gp(P.ntile, P.B);
@@ -1314,6 +1318,7 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
         if (ctx->small) k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
         else launch_rebin(ctx);
+        cudaEventRecord(ev[5], s);
         launch_nlist_density(ctx, s);   // (runs after k_density in the step; same work)
         cudaEventRecord(ev[1], s);
         launch_density(ctx, s, 1);
@@ -1333,6 +1338,8 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
         float m;
         CK(cudaEventElapsedTime(&m, ev[0], ev[4]));
         acc[SPH_TIMER_SUBSTEP] += m;
+        CK(cudaEventElapsedTime(&m, ev[0], ev[5]));
+        acc[SPH_TIMER_SORT] += m;
     }
     for (int t = 0; t < SPH_NUM_TIMERS; ++t) ms[t] = (float)(acc[t] / n_substeps);
     for (auto& e : ev) cudaEventDestroy(e);

@@ -41,7 +41,9 @@ struct DevParams {
     int ghost_K, ghost_K1, ghost_full;   // ghost windows for support 2h (density) and h (force)
     float C, inv_C, half;   // cell side (2h + skin), 1/C, half extent of the grid
     float h, inv_h, H2, h2; // h, 1/h, (2h)^2, h^2 in float32 (predicates, reading A19)
-    float RL2;              // list radius^2 = (2h + skin)^2
+    double h2d;             // 2h in double (list radius 2h + skin, rounded once to float)
+    float skin0;            // Verlet skin at init (reading B4); adaptive between skin0 and
+    float skin_max;         // skin_max when skin_max > skin0 (B5), cells are 2h + skin_max wide
     float mass, m2, rho0, k, gamma1;
     float alpha2h, beta, eps_h2;
     float wcb, dwcb, dws3;  // C/h^2, C/h^3, -30/(pi h^5)
@@ -51,7 +53,6 @@ struct DevParams {
     float wall_r2;          // particles with |x - r|^2 <= wall_r2 see no ghost within 2h
     float wall1_r2;         // ... no ghost within h
     float ghost_scale;      // G / (2 pi)
-    float rebuild_disp;     // rebuild when the displacement bound reaches this (< skin / 2)
     int rebin_every;
     int NA;                 // aux row stride per rollout = N rounded up to even (16-B rows)
     int td, tf, tn;         // slots (threads) per CTA of k_density / k_force / k_nlist_density
@@ -82,7 +83,28 @@ struct RolloutState {
                          // translation since the last rebuild
     int span;            // max |j - i| over all neighbour-list entries (staging window)
     float rbx, rby;      // body position (float) at the last rebuild
+    float skin;          // Verlet skin of the current lists (B5: adapted at every rebuild)
+    float rl2;           // list radius^2 = fl(2h + skin)^2 (float32 predicate, reading A19)
+    float rdisp;         // rebuild when the displacement bound reaches 0.49 skin (< skin / 2)
+    long long last_reb;  // substep index of the last rebuild
 };
+
+// Verlet skin -> list radius^2 and rebuild threshold (the same float arithmetic everywhere)
+__device__ __forceinline__ void skin_set(const DevParams& P, float skin, float* rl2, float* rdisp) {
+    const float RL = (float)(P.h2d + (double)skin);
+    *rl2 = __fmul_rn(RL, RL);
+    *rdisp = (float)(0.49 * (double)skin);
+}
+// Adaptive skin (B5): at a rebuild that follows I substeps of the old lists, scale the
+// skin by sqrt(SKIN_TARGET / I) (a displacement bound that tripped after I substeps needs skin x
+// TARGET / I to last TARGET substeps; the square root damps the response), within
+// [skin0, skin_max].  A function of the rollout's own history only (batch-invariant bits).
+constexpr int SKIN_TARGET = 8;
+__device__ __forceinline__ float skin_adapt(const DevParams& P, float skin, long long I) {
+    if (!(P.skin_max > P.skin0)) return skin;
+    const double s = (double)skin * sqrt((double)SKIN_TARGET / (double)(I > 1 ? I : 1));
+    return (float)fmin(fmax(s, (double)P.skin0), (double)P.skin_max);
+}
 
 struct Geom {            // float copy of the body state used by the particle kernels
     float rx, ry, th;    // th = theta + angle of ghost 0 (ghost-ring lookup)

@@ -518,6 +518,7 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
     // (shift-in, bit 0 = last candidate), then only the set bits are appended, highest bit
     // first (= ascending j, the order of a plain scan).
     const int cy = (int)cell / P.nx, cx = (int)cell - cy * P.nx;
+    const float RL2 = D.rs[b].rl2;   // this rollout's list radius^2 (adaptive skin, B5)
     for (int dy = -1; dy <= 1 && !ovf; ++dy) {
         const int c0 = (cy + dy) * P.nx + cx - 1;
         const int j0 = (int)cs[c0], j1 = (int)cs[c0 + 3];
@@ -527,7 +528,7 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
             for (int k = 0; k < cnt; ++k) {
                 const float2 xj = pos((uint32_t)(base + k));
                 const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
-                m = (m << 1) | (r2 < P.RL2 ? 1u : 0u);
+                m = (m << 1) | (r2 < RL2 ? 1u : 0u);
             }
             const int self = i - base;
             if (self >= 0 && self < cnt) m &= ~(1u << (cnt - 1 - self));
@@ -1173,7 +1174,14 @@ __device__ __forceinline__ void body_step(const DevParams& P, const DevPtrs& D, 
         const double d = sqrt(f.w) + P.dtd * sqrt(bd[3] * bd[3] + bd[4] * bd[4]);
         const float disp = (float)d;
         rs->disp = disp;
-        rs->need_rebin = P.rebin_every ? 1 : (disp >= P.rebuild_disp ? 1 : 0);
+        const int nrb = P.rebin_every ? 1 : (disp >= rs->rdisp ? 1 : 0);
+        rs->need_rebin = nrb;
+        if (nrb && !P.rebin_every) {   // the next substep rebuilds: adapt the skin (B5)
+            const float sk = skin_adapt(P, rs->skin, rs->step + 1 - rs->last_reb);
+            rs->skin = sk;
+            skin_set(P, sk, &rs->rl2, &rs->rdisp);
+            rs->last_reb = rs->step + 1;
+        }
         rs->step += 1;
         if (r_status) rs->frozen = 1;
     }
@@ -1351,6 +1359,10 @@ __global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angl
             rs->bad_particle = -1;
         }
         rs->disp = 0.f;
+        rs->skin = P.skin0;
+        skin_set(P, P.skin0, &rs->rl2, &rs->rdisp);
+        if (P.rebin_every) rs->rl2 = P.H2;
+        rs->last_reb = rs->step;
         const double* body = D.body + (size_t)b * 6;
         for (int c = 0; c < 6; ++c) sbody[c] = body[c];
         sincos(body[2], &sbody[7], &sbody[6]);

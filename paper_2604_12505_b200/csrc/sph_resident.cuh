@@ -62,6 +62,8 @@ struct ResMisc {
     float u[3];
     float rbx, rby;          // body position (float) at the last rebuild (Verlet criterion)
     float disp;
+    float skin, rl2, rdisp;  // adaptive Verlet skin of the current lists (B5)
+    long long last_reb;
     int need_rebin, stop, n_reb, it_done;
     int wlo, whi, cbase, cend;
     int nm, mv;              // this CTA's non-mover / mover counts (read by the other CTAs)
@@ -462,6 +464,7 @@ __device__ __noinline__ void res_window(const DevParams& P, const ResParams& R, 
     __syncthreads();
     // window positions of the list predicate: current state (rebuild) or rebuild-time xb (reload)
     const float2* __restrict__ wpos = FROM_XB ? s.aux : reinterpret_cast<const float2*>(s.pv);
+    const float RL2 = m->rl2;   // list radius^2 of these lists (adaptive skin, B5)
     const int ws = FROM_XB ? 1 : 2;
     // Verlet lists of own slots: every window slot of the 3 x 3 cell block within 2h + skin
     // (canonical float32 predicate, reading A19), ascending window index; the partial last quad
@@ -480,7 +483,7 @@ __device__ __noinline__ void res_window(const DevParams& P, const ResParams& R, 
             for (int w = w0; w < w1; ++w) {
                 if (w == li) continue;
                 const float2 xj = wpos[ws * w];
-                if (dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y)) < P.RL2) {
+                if (dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y)) < RL2) {
                     if (n >= R.KR) {
                         ovf = true;
                         continue;
@@ -716,6 +719,10 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
         m->n_reb = 0;
         m->it_done = 0;
         m->disp = rs->disp;
+        m->skin = rs->skin;
+        m->rl2 = rs->rl2;
+        m->rdisp = rs->rdisp;
+        m->last_reb = rs->last_reb;
     }
     if (tid < RES_MAXCS) m->bad_all[tid] = 0;
     // lists of the last rebuild still valid (rs->need_rebin == 0): reload them instead of
@@ -837,7 +844,14 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
                 sincos(bd[2], &bd[7], &bd[6]);
                 const double d = sqrt(f.w) + P.dtd * sqrt(bd[3] * bd[3] + bd[4] * bd[4]);
                 m->disp = (float)d;
-                m->need_rebin = P.rebin_every ? 1 : ((float)d >= P.rebuild_disp ? 1 : 0);
+                const int nrb = P.rebin_every ? 1 : ((float)d >= m->rdisp ? 1 : 0);
+                m->need_rebin = nrb;
+                if (nrb && !P.rebin_every) {   // next substep rebuilds: adapt the skin (B5)
+                    const float sk = skin_adapt(P, m->skin, step + 1 - m->last_reb);
+                    m->skin = sk;
+                    skin_set(P, sk, &m->rl2, &m->rdisp);
+                    m->last_reb = step + 1;
+                }
                 m->it_done = it + 1;
                 m->stop = stop;
             }
@@ -874,6 +888,10 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
             rs->rbx = m->rbx;
             rs->rby = m->rby;
             rs->disp = m->disp;
+            rs->skin = m->skin;
+            rs->rl2 = m->rl2;
+            rs->rdisp = m->rdisp;
+            rs->last_reb = m->last_reb;
             if (m->stop) rs->frozen = 1;
         }
     }
