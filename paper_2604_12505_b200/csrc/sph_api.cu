@@ -385,6 +385,11 @@ static cudaError_t add_conditional_rebin(sph_ctx* ctx) {
                                            cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
         return e;
     launch_rebin(ctx, ctx->side);
+    // lists + densities of the rebuilt rollouts inside the IF body too: substeps without a
+    // rebuild then launch no list kernel at all (C4: one launch of ~8,000 empty CTAs less per
+    // substep); they only touch rebuilt rollouts, k_density the others (disjoint), so running
+    // them before k_density changes nothing
+    launch_nlist_density(ctx, ctx->side);
     return cudaStreamEndCapture(ctx->side, &body);
 }
 
@@ -445,6 +450,7 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
         live_mark(ev, LV_DEN0, s);
         launch_density(ctx, s, 1, false);   // (follows the IF node / the rebuild kernels)
         live_mark(ev, LV_DEN1, s);
+        if (capturing) return cudaSuccess;   // (lists inside the IF body, add_conditional_rebin)
     }
     launch_nlist_density(ctx, s, np);
     return cudaSuccess;
