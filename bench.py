@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--horizon-ticks", type=int, default=2200, help="--long-horizon: ticks to run")
     ap.add_argument("--skin-max", type=float, default=None,
                     help="adaptive Verlet skin upper bound in units of h (DESIGN.md B5; 0 = fixed skin)")
+    ap.add_argument("--skin-mode", type=int, default=None, choices=[0, 1],
+                    help="with --skin-max > --skin: 0 per-rollout adaptive skin (B5), 1 per-particle (B6)")
     ap.add_argument("--rebuild-path", type=int, default=0, choices=[0, 1, 2],
                     help="sph_time_params.rebuild_path: 0 auto, 1 per-rollout CTA sort, 2 grid-wide kernels")
     ap.add_argument("--exec-path", type=int, default=0, choices=[0, 1, 2, 3],
@@ -365,7 +367,7 @@ def run_ours(a):
                   "inputs": "open-loop multisine + pulse train (P:430-432)"}
     skin = a.skin * sp.h if a.rebin_every == 0 else 0.0
     ctx = SphContext(sp, pv0, t.ghost_b, n_rollouts=B, rebin_every=a.rebin_every,
-                     skin=skin, device=local, exec_path=a.exec_path, rebuild_path=a.rebuild_path, skin_max=a.skin_max * sp.h)
+                     skin=skin, device=local, exec_path=a.exec_path, rebuild_path=a.rebuild_path, skin_max=a.skin_max * sp.h, skin_mode=a.skin_mode)
     u_dev = torch.from_numpy(u_host).to(dev)
     th_dev = torch.from_numpy(th_host).to(dev) if th_host is not None else None
     pdkw = dict(Kp=sp.Kp, Kd=sp.Kd) if th_host is not None else {}
@@ -488,7 +490,7 @@ def run_ours(a):
     y_pin = [torch.empty((B, 1, 6), dtype=torch.float32).pin_memory() for _ in range(K_e2e)]
     ua_pin = [torch.empty((B, 1, 3), dtype=torch.float32).pin_memory() for _ in range(K_e2e)]
     ctx2 = SphContext(sp, pv0, t.ghost_b, n_rollouts=B, rebin_every=a.rebin_every, skin=skin,
-                      device=local, exec_path=a.exec_path, rebuild_path=a.rebuild_path, skin_max=a.skin_max * sp.h)
+                      device=local, exec_path=a.exec_path, rebuild_path=a.rebuild_path, skin_max=a.skin_max * sp.h, skin_mode=a.skin_mode)
     if a.warmup > 1:
         ctx2.rollout(u_dev[:, :a.warmup - 1].contiguous(), y_out=y_dev[:, :a.warmup - 1].contiguous(),
                      u_applied=ua_dev[:, :a.warmup - 1].contiguous(),
@@ -569,7 +571,7 @@ def run_horizon(a):
     pv0 = settled_start(t, a.settle_seconds, local)
     u = torch.from_numpy(inputs_for(range(B), K_TRAIN)).to(dev)
     ctx = SphContext(sp, pv0, t.ghost_b, n_rollouts=B, rebin_every=0, skin=a.skin * sp.h,
-                     device=local, exec_path=a.exec_path, rebuild_path=a.rebuild_path, skin_max=a.skin_max * sp.h)
+                     device=local, exec_path=a.exec_path, rebuild_path=a.rebuild_path, skin_max=a.skin_max * sp.h, skin_mode=a.skin_mode)
     y = torch.empty((B, K_TRAIN, 6), dtype=torch.float32, device=dev)
     ua = torch.empty((B, K_TRAIN, 3), dtype=torch.float32, device=dev)
     win = 100
@@ -1043,9 +1045,14 @@ def run_dd(a):
 def main():
     a = parse()
     if a.skin is None:
-        a.skin = {"P0": 0.5, "C2CL": 0.5, "SETTLE": 0.5, "C4": 0.8}.get(a.workload, 0.15)
+        a.skin = {"P0": 0.5, "C2CL": 0.5, "SETTLE": 0.5}.get(a.workload, 0.15)
+    # Verlet skin policy (B4-B6): C3/C5 per-rollout adaptive skin 0.15h -> 0.5h (B5;
+    # calm start and sloshing steady state of the 110 s train, profiles/horizon*_r02*); C4
+    # per-particle half-skins 0.15h / 0.8h (B6: the bulk keeps short lists, the wall layer wide)
     if a.skin_max is None:
-        a.skin_max = 0.0
+        a.skin_max = {"C3": 0.5, "C5": 0.5, "C4": 0.8}.get(a.workload, 0.0) if a.skin == 0.15 or a.workload == "C4" else 0.0
+    if a.skin_mode is None:
+        a.skin_mode = 1 if a.workload == "C4" else 0
     if a.settle_seconds is None:
         # C4: lattice start + 1,000 untimed damped warm-up substeps; dt = 1 ms / 42
         a.settle_seconds = 1000 * 1e-3 / 42.0 if a.workload == "C4" else 4.0

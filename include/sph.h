@@ -103,6 +103,12 @@ typedef struct {
                                  the previous lists lasted, within [skin, skin_max]; cells are
                                  2h + skin_max wide.  The lists hold every pair within the
                                  rollout's current 2h + skin, so the sums are unchanged.      */
+    int skin_mode;            /* with skin_max > skin: 0 per-rollout adaptive skin (B5);
+                                 1 per-particle half-skins (B6): at every rebuild
+                                 particle i gets hs_i = clamp(10 dt |v_i - v_body|, skin / 2,
+                                 skin_max / 2), pair (i, j) is listed within 2h + hs_i + hs_j,
+                                 and the lists are rebuilt when some particle's displacement
+                                 reaches 0.98 hs_i (exec_path 3: mode 0 only).                */
 } sph_time_params;
 
 /* PD attitude law tau_k = Kp (theta_ref_k - theta_k) - Kd thetadot_k, ZOH. */

@@ -34,7 +34,7 @@ class BodyParams(C.Structure):
 class TimeParams(C.Structure):
     _fields_ = [("dt", C.c_double), ("substeps_per_sample", C.c_int), ("rebin_every", C.c_int),
                 ("skin", C.c_double), ("rebuild_path", C.c_int), ("exec_path", C.c_int),
-                ("skin_max", C.c_double)]
+                ("skin_max", C.c_double), ("skin_mode", C.c_int)]
 
 
 class PdAttitude(C.Structure):
@@ -123,9 +123,9 @@ def body_params(sp) -> BodyParams:
 
 
 def time_params(sp, rebin_every: int = 1, skin: float = 0.0, rebuild_path: int = 0,
-                exec_path: int = 0, skin_max: float = 0.0) -> TimeParams:
+                exec_path: int = 0, skin_max: float = 0.0, skin_mode: int = 0) -> TimeParams:
     return TimeParams(sp.dt, int(sp.n_sub), int(rebin_every), float(skin), int(rebuild_path),
-                      int(exec_path), float(skin_max))
+                      int(exec_path), float(skin_max), int(skin_mode))
 
 
 def _ptr(a):
@@ -145,13 +145,13 @@ class SphContext:
 
     def __init__(self, sp, fluid_pv, ghost_b, n_rollouts: int = 1, rebin_every: int = 1,
                  skin: float = 0.0, device: int = 0, rebuild_path: int = 0, exec_path: int = 0,
-                 skin_max: float = 0.0):
+                 skin_max: float = 0.0, skin_mode: int = 0):
         import torch
         self.torch = torch
         self.L = lib()
         self.device = torch.device("cuda", device)
         self.fp, self.bp = fluid_params(sp), body_params(sp)
-        self.tp = time_params(sp, rebin_every, skin, rebuild_path, exec_path, skin_max)
+        self.tp = time_params(sp, rebin_every, skin, rebuild_path, exec_path, skin_max, skin_mode)
         pv = _host(fluid_pv, np.float32).reshape(-1, 4)
         gb = _host(ghost_b, np.float64).reshape(-1, 2)
         self.N, self.G, self.B = pv.shape[0], gb.shape[0], int(n_rollouts)

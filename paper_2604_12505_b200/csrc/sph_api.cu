@@ -151,6 +151,8 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->B = B;
     if (!(tp->skin_max >= 0.0) || (tp->skin_max > 0.0 && tp->skin_max < tp->skin))
         return *why = "skin_max must be 0 (fixed skin) or >= skin", false;
+    if (tp->skin_mode < 0 || tp->skin_mode > 1) return *why = "skin_mode must be 0 or 1", false;
+    const bool perpart = !tp->rebin_every && tp->skin_mode == 1 && tp->skin_max > tp->skin;
     const double skin_cell = tp->rebin_every ? 0.0 : std::max(tp->skin, tp->skin_max);
     const double Cd = 2.0 * h + skin_cell;
     P->C = (float)Cd;
@@ -199,6 +201,11 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     P->h2d = 2.0 * h;
     P->skin0 = tp->rebin_every ? 0.0f : (float)tp->skin;
     P->skin_max = tp->rebin_every ? 0.0f : (float)tp->skin_max;
+    P->perpart = perpart ? 1 : 0;                    // per-particle half-skins (B6)
+    P->Hf = H;
+    P->hs_min = (float)(0.5 * tp->skin);
+    P->hs_max = (float)(0.5 * tp->skin_max);
+    P->hs_k = (float)(HS_TARGET * tp->dt);
     P->NA = (N + 1) & ~1;
     {   // CTA sizes of the plain density / force / list kernels.  Small CTAs win (C3 sweeps,
         // DESIGN.md section 7): a CTA's slot frees only when its slowest warp ends, and list
@@ -257,6 +264,7 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     put(d.aux, (size_t)P.B * P.NA * 8);   // rows of NA (even) elements: 16-B aligned
     put(d.skey, BN * 4);
     put(d.xb, BN * 8);
+    put(d.hs, P.perpart ? BN * 4 : 4);
     put(d.nbr, BN * KQ * 8);
     put(d.ncnt, BN);
     put(d.key, BN * 4);
@@ -545,7 +553,7 @@ static sph_status all_failed(sph_ctx* ctx) {
 // ---------------------------------------------------------------------------------------
 // Cluster shape and shared-memory carve-up for CS CTAs per rollout; false if it does not fit.
 static bool res_layout(const DevParams& P, int CS, int smem_max, ResParams* out, int* nt_out) {
-    if (P.N <= 0 || P.N >= 65536) return false;
+    if (P.N <= 0 || P.N >= 65536 || P.perpart) return false;   // (uniform / B5 skins only)
     ResParams R{};
     R.CS = CS;
     R.S = ((P.N + CS - 1) / CS + 31) / 32 * 32;

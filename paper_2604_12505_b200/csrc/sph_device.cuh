@@ -44,6 +44,11 @@ struct DevParams {
     double h2d;             // 2h in double (list radius 2h + skin, rounded once to float)
     float skin0;            // Verlet skin at init (reading B4); adaptive between skin0 and
     float skin_max;         // skin_max when skin_max > skin0 (B5), cells are 2h + skin_max wide
+    int perpart;            // 1: per-particle half-skins instead (B6): pair (i, j) is listed within
+                            //    2h + hs_i + hs_j, rebuild when some |d_i| reaches 0.98 hs_i
+    float Hf;               // fl(2h)
+    float hs_min, hs_max;   // B6: half-skin bounds (skin / 2, skin_max / 2)
+    float hs_k;             // B6: hs_i = clamp(hs_k |v_i - v_body|, hs_min, hs_max), hs_k = 10 dt
     float mass, m2, rho0, k, gamma1;
     float alpha2h, beta, eps_h2;
     float wcb, dwcb, dws3;  // C/h^2, C/h^3, -30/(pi h^5)
@@ -101,7 +106,7 @@ __device__ __forceinline__ void skin_set(const DevParams& P, float skin, float* 
 // [skin0, skin_max].  A function of the rollout's own history only (batch-invariant bits).
 constexpr int SKIN_TARGET = 8;
 __device__ __forceinline__ float skin_adapt(const DevParams& P, float skin, long long I) {
-    if (!(P.skin_max > P.skin0)) return skin;
+    if (!(P.skin_max > P.skin0) || P.perpart) return skin;
     const double s = (double)skin * sqrt((double)SKIN_TARGET / (double)(I > 1 ? I : 1));
     return (float)fmin(fmax(s, (double)P.skin0), (double)P.skin_max);
 }
@@ -112,12 +117,25 @@ struct Geom {            // float copy of the body state used by the particle ke
     float pad[3];
 };
 
+// Per-particle half-skin (B6), set at every rebuild from the particle's speed relative
+// to the body translation: the skin it needs to last ~10 substeps, within [hs_min, hs_max].  For
+// a large tank whose wall layer moves 10-50x faster than the bulk (C4), a uniform skin sized for
+// the wall makes every list long; a per-particle one keeps the bulk's lists short.
+constexpr int HS_TARGET = 10;
+// (Measured alternative, not kept: raising the floor per rollout with the B5 rule pushes every
+// particle's skin up to outlast the few that trip early -- C4 8.5 vs 9.6 G/s.)
+__device__ __forceinline__ float half_skin(const DevParams& P, float4 x, const Geom& gm) {
+    const float vx = x.z - gm.vx, vy = x.w - gm.vy;
+    return fminf(fmaxf(P.hs_k * sqrtf(vx * vx + vy * vy), P.hs_min), P.hs_max);
+}
+
 struct DevPtrs {
     float4* pv[2];       // [B][N] sorted-by-cell particle state (x, y, vx, vy), double buffered
     uint32_t* id[2];     // [B][N] canonical id of each slot
     float2* aux;         // [B][N] (rho, P / rho^2)
     uint32_t* skey;      // [B][N] cell of each slot at the last rebuild
     float2* xb;          // [B][N] position of each slot at the last rebuild (Verlet criterion)
+    float* hs;           // [B][N] half-skin of each slot (B6; per-particle skin mode only)
     uint2* nbr;          // [B][KQ][N] neighbour candidates: 4 int16 slot offsets j - i per uint2
     uint8_t* ncnt;       // [B][N] list length (NL_OVERFLOW: scan the cells instead)
     uint32_t* key;       // [B][N] rebuild scratch: cell of each (unsorted) slot

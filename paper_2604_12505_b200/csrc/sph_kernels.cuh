@@ -217,6 +217,7 @@ __device__ __forceinline__ void gather_blk(const DevParams& P, const DevPtrs& D,
     D.skey[o + d] = D.key[o + src];
     const float4 x = D.pv[sp ^ 1][o + d];
     D.xb[o + d] = make_float2(x.x, x.y);   // positions at this rebuild (Verlet criterion)
+    if (P.perpart) D.hs[o + d] = half_skin(P, x, D.geom[b]);
 }
 __global__ void __launch_bounds__(TILE) k_gather(DevParams P, DevPtrs D) { gather_blk(P, D, blockIdx.x, blockIdx.y); }
 
@@ -518,7 +519,9 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
     // (shift-in, bit 0 = last candidate), then only the set bits are appended, highest bit
     // first (= ascending j, the order of a plain scan).
     const int cy = (int)cell / P.nx, cx = (int)cell - cy * P.nx;
-    const float RL2 = D.rs[b].rl2;   // this rollout's list radius^2 (adaptive skin, B5)
+    const float RL2u = D.rs[b].rl2;  // this rollout's list radius^2 (uniform / B5 skin)
+    const float* __restrict__ hs = D.hs + o;
+    const float hsi = P.perpart ? hs[i] : 0.0f;
     for (int dy = -1; dy <= 1 && !ovf; ++dy) {
         const int c0 = (cy + dy) * P.nx + cx - 1;
         const int j0 = (int)cs[c0], j1 = (int)cs[c0 + 3];
@@ -528,6 +531,12 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
             for (int k = 0; k < cnt; ++k) {
                 const float2 xj = pos((uint32_t)(base + k));
                 const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+                // list radius: 2h + skin, or 2h + hs_i + hs_j (per-particle skins, B6)
+                float RL2 = RL2u;
+                if (P.perpart) {
+                    const float RL = __fadd_rn(P.Hf, __fadd_rn(hsi, hs[base + k]));
+                    RL2 = __fmul_rn(RL, RL);
+                }
                 m = (m << 1) | (r2 < RL2 ? 1u : 0u);
             }
             const int self = i - base;
@@ -669,6 +678,7 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
             const uint32_t c = s_key[src];
             D.skey[o + d] = c;
             D.xb[o + d] = make_float2(v.x, v.y);   // positions at this rebuild (Verlet)
+            if (P.perpart) D.hs[o + d] = half_skin(P, v, gm);
         }
         __syncthreads();
         // lists + densities follow in k_nlist_density (grid-wide)
@@ -914,6 +924,10 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
     const float2 xb = ld<NC>(D.xb + o + i);
     const float ddx = (xn.x - xb.x) - (gm.rx - rs->rbx), ddy = (xn.y - xb.y) - (gm.ry - rs->rby);
     acc.vmax = ddx * ddx + ddy * ddy;
+    if (P.perpart) {   // (|d_i| / hs_i)^2 (B6)
+        const float ih = __frcp_rn(ld<NC>(D.hs + o + i));
+        acc.vmax *= ih * ih;
+    }
     // one test for the common case: the abs-sum is NaN / inf for any non-finite element and
     // exceeds 1e9 whenever an element does; classify only in the rare branch
     const float mag = fabsf(xn.x) + fabsf(xn.y) + fabsf(xn.z) + fabsf(xn.w);
@@ -1171,7 +1185,11 @@ __device__ __forceinline__ void body_step(const DevParams& P, const DevPtrs& D, 
         // max over particles of |(x_i - x_i^build) - (r_n - r^build)| (from k_force) plus the
         // body's drift in this substep: a strict bound on every particle's displacement
         // relative to the body translation since the last rebuild (Verlet criterion)
-        const double d = sqrt(f.w) + P.dtd * sqrt(bd[3] * bd[3] + bd[4] * bd[4]);
+        // uniform skin: d = that bound in metres.  Per-particle half-skins (B6): f.w is the
+        // largest (|d_i| / hs_i)^2 and the body drift enters over the smallest half-skin, so
+        // d >= rdisp = 0.98 whenever some |d_i| + drift may reach 0.98 hs_i
+        const double drift = P.dtd * sqrt(bd[3] * bd[3] + bd[4] * bd[4]);
+        const double d = sqrt(f.w) + (P.perpart ? drift / (double)P.hs_min : drift);
         const float disp = (float)d;
         rs->disp = disp;
         const int nrb = P.rebin_every ? 1 : (disp >= rs->rdisp ? 1 : 0);
@@ -1180,6 +1198,7 @@ __device__ __forceinline__ void body_step(const DevParams& P, const DevPtrs& D, 
             const float sk = skin_adapt(P, rs->skin, rs->step + 1 - rs->last_reb);
             rs->skin = sk;
             skin_set(P, sk, &rs->rl2, &rs->rdisp);
+            if (P.perpart) rs->rdisp = 0.98f;   // (B6: the bound is relative to hs_i)
             rs->last_reb = rs->step + 1;
         }
         rs->step += 1;
@@ -1362,6 +1381,7 @@ __global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angl
         rs->skin = P.skin0;
         skin_set(P, P.skin0, &rs->rl2, &rs->rdisp);
         if (P.rebin_every) rs->rl2 = P.H2;
+        if (P.perpart) rs->rdisp = 0.98f;
         rs->last_reb = rs->step;
         const double* body = D.body + (size_t)b * 6;
         for (int c = 0; c < 6; ++c) sbody[c] = body[c];

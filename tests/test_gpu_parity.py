@@ -491,3 +491,46 @@ def test_closed_loop_profile1_speed_statistics_match_oracle():
 def SphContext_(t, pv0):
     from paper_2604_12505_b200 import SphContext
     return SphContext(t.params, pv0, t.ghost_b, n_rollouts=1, rebin_every=0, skin=0.15 * t.params.h)
+
+
+@pytest.mark.parametrize("mode,skin,skin_max", [(0, 0.1, 0.5), (1, 0.1, 0.8)],
+                         ids=["per_rollout_adaptive_B5", "per_particle_B6"])
+def test_adaptive_skin_policies_keep_every_pair_listed(mode, skin, skin_max):
+    """Skin policies B5 (per-rollout adaptive skin) and B6 (per-particle half-skins) only change
+    WHEN the Verlet lists are rebuilt and how long they are; every pair within 2h must still be
+    listed at every substep.  A strongly forced, unsettled C1 tank (violent flow: the trajectory
+    itself is chaotic) runs 300 substeps; every 25 substeps the state is exported and ONE more
+    substep -- taken with the policy's current, possibly stale lists -- is compared with the
+    float64 oracle stepped from the same exported state (1e-5, the north star's one-step bar: a
+    missed pair within 2h would cost far more).  Rebuilds must be rarer than with the fixed small
+    skin, and the 2h neighbour sets of the final state bit-exact."""
+    t = si.moving_tank(1.0, seed=6, vel=0.05)
+    sp = t.params
+    u = (40.0, -25.0, 3.0)
+    ua = np.array([u], np.float32)
+    a = _ctx(t, rebin_every=0, skin=skin * sp.h, skin_max=skin_max * sp.h, skin_mode=mode)
+    f = _ctx(t, rebin_every=0, skin=skin * sp.h)        # fixed small skin
+    vfloor = sp.dt * sp.k / sp.h
+    for _ in range(12):
+        a.step(ua, 24)
+        f.step(ua, 25)
+        pv = a.get_particles(0).astype(np.float64)
+        body = a.get_body_state()[0]
+        ref = O.State(sp, pv[:, :2], pv[:, 2:], t.ghost_b, body)
+        ref.step(u)
+        a.step(ua, 1)
+        p1 = a.get_particles(0)
+        assert _rel(p1[:, :2], ref.pos) <= 1e-5
+        assert _rel(p1[:, 2:], ref.vel, vfloor) <= 1e-5
+        b1 = a.get_body_state()[0]
+        for sl in (slice(0, 2), slice(2, 3), slice(3, 5), slice(5, 6)):
+            assert _rel(b1[sl], ref.body[sl], 1e-12) <= 1e-5
+    assert a.get_status()[0][0] == 0
+    reb_a, reb_f = a.counters()[1][0], f.counters()[1][0]
+    assert 1 <= reb_a < reb_f, (reb_a, reb_f)
+    nf, g2, g1 = a.debug_neighbours(0)
+    p32 = np.ascontiguousarray(a.get_particles(0)[:, :2])
+    H = np.float32(2 * sp.h)
+    assert _csr_sets(*nf) == _csr_sets(*O.neighbours_f32(p32, H * H))
+    for c in (a, f):
+        c.close()
