@@ -313,13 +313,10 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
     pdl = pdl && ctx->pdl;
     const DevParams& P = ctx->P;
     const int gy = mode == 2 ? std::min(P.B, 64) : P.B;
-    switch (P.tf) {
-            case 1024: launch_k(pdl, k_force<1024>, dim3(std::max(1, (P.own_n + 1023) / 1024), gy), dim3(1024), 0, s, P, ctx->D, damping, mode); break;
-            case 512: launch_k(pdl, k_force<512>, dim3(std::max(1, (P.own_n + 511) / 512), gy), dim3(512), 0, s, P, ctx->D, damping, mode); break;
-            case 128: launch_k(pdl, k_force<128>, dim3(std::max(1, (P.own_n + 127) / 128), gy), dim3(128), 0, s, P, ctx->D, damping, mode); break;
-            case 64: launch_k(pdl, k_force<64>, dim3(std::max(1, (P.own_n + 63) / 64), gy), dim3(64), 0, s, P, ctx->D, damping, mode); break;
-            default: launch_k(pdl, k_force<256>, dim3(std::max(1, (P.own_n + 255) / 256), gy), dim3(256), 0, s, P, ctx->D, damping, mode); break;
-        }
+    // 64-slot CTAs; the per-particle-skin epilogue (B6) only in its own instance
+    const dim3 g(std::max(1, (P.own_n + 63) / 64), gy);
+    if (P.perpart) launch_k(pdl, k_force<64, true>, g, dim3(64), 0, s, P, ctx->D, damping, mode);
+    else launch_k(pdl, k_force<64, false>, g, dim3(64), 0, s, P, ctx->D, damping, mode);
 }
 
 static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0, bool pdl = false) {

@@ -856,7 +856,7 @@ struct BodyAcc {
 // pvj(d) / axj(d) read list neighbour i + d; pv / aux are the rollout's global
 // rows (cell-scan fallback of overflowing lists).  The body geometry is loaded after the list
 // walk so it does not occupy registers during it.
-template <bool NC = true, class PV, class AX>
+template <bool NC = true, bool PP = true, class PV, class AX>
 __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs& D, float damping,
                                                int b, int i, int cur, const RolloutState* rs,
                                                float4 xi, float2 ai,
@@ -924,7 +924,7 @@ __device__ __forceinline__ void force_particle(const DevParams& P, const DevPtrs
     const float2 xb = ld<NC>(D.xb + o + i);
     const float ddx = (xn.x - xb.x) - (gm.rx - rs->rbx), ddy = (xn.y - xb.y) - (gm.ry - rs->rby);
     acc.vmax = ddx * ddx + ddy * ddy;
-    if (P.perpart) {   // (|d_i| / hs_i)^2 (B6)
+    if (PP && P.perpart) {   // (|d_i| / hs_i)^2 (B6; PP = false: compiled out of the C3 kernel)
         const float ih = __frcp_rn(ld<NC>(D.hs + o + i));
         acc.vmax *= ih * ih;
     }
@@ -973,7 +973,7 @@ __device__ __forceinline__ void list_head(const DevParams& P, const DevPtrs& D, 
     }
 }
 
-template <int TF, bool NC = true>
+template <int TF, bool NC = true, bool PP = true>
 __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D, float damping,
                                            int b, int tile) {
     const int i = tile * TF + threadIdx.x;
@@ -989,7 +989,7 @@ __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D,
     if (i < P.N) {
         const float4* __restrict__ pvi = opaque(pv + i);
         const float2* __restrict__ axi = opaque(aux + i);
-        force_particle<NC>(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
+        force_particle<NC, PP>(P, D, damping, b, i, cur, rs, *pvi, *axi, pv, aux,
                            [&](int d) { return ld<NC>(pvi + d); },
                            [&](int d) { return ld<NC>(axi + d); }, acc, q0, n);
     }
@@ -1003,7 +1003,7 @@ __device__ __forceinline__ void force_tile(const DevParams& P, const DevPtrs& D,
 // The slot window (own_lo, own_n) of a domain-decomposition launch is a runtime tile offset;
 // the same offset in every launch measures 3.9 % faster on C3 than a specialised offset-free
 // instantiation (A/B on one box; its list loop is 8 SASS shorter, but the kernel is slower).
-template <int TF>
+template <int TF, bool PP>
 __global__ void __launch_bounds__(TF, SPH_FORCE_MINB * TILE / TF) k_force(DevParams P, DevPtrs D,
                                                                           float damping, int mode) {
     pdl_wait();
@@ -1012,14 +1012,14 @@ __global__ void __launch_bounds__(TF, SPH_FORCE_MINB * TILE / TF) k_force(DevPar
     if (mode == 2) {
         const int count = *D.rcount;
         for (int w = blockIdx.y; w < count; w += gridDim.y)
-            force_tile<TF>(P, D, damping, D.rlist[w], tile);
+            force_tile<TF, true, PP>(P, D, damping, D.rlist[w], tile);
         return;
     }
     // snake order: k_density walks the rollouts first to last, k_force last to first, so the
     // first force CTAs find the rollouts k_density touched last still in L2
     const int b = P.snake ? (int)gridDim.y - 1 - (int)blockIdx.y : (int)blockIdx.y;
     if (mode == 1 && D.rs[b].need_rebin) return;   // CTA-uniform
-    force_tile<TF>(P, D, damping, b, tile);
+    force_tile<TF, true, PP>(P, D, damping, b, tile);
     prefetch_ahead<true>(P, D, TF, P.pf_f, P.snake != 0);
 }
 
