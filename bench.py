@@ -729,7 +729,8 @@ def run_p0(a, closed_loop_c2=False):
         ctx.settle(math.exp(-10.0 * sp.dt), int(2.0 / sp.dt))
         pv0 = ctx.get_particles(0)
         ctx.close()
-    ctx = SphContext(sp, pv0, t.ghost_b, n_rollouts=1, rebin_every=0, skin=a.skin * sp.h, device=local)
+    ctx = SphContext(sp, pv0, t.ghost_b, n_rollouts=1, rebin_every=0, skin=a.skin * sp.h, device=local,
+                     exec_path=a.exec_path)
     dev = torch.device("cuda", local)
     ud, thd = torch.from_numpy(u).to(dev), torch.from_numpy(th).to(dev)
     y = torch.empty((1, K, 6), dtype=torch.float32, device=dev)

@@ -91,11 +91,14 @@ typedef struct {
                                  SPH_EINVAL); 2 grid-wide multi-kernel counting sort        */
     int exec_path;            /* how a slow tick runs; every path computes
                                  the same substep (Algorithm 1):
-                                 0 auto: 2 for B*N <= 65536, else 1;
+                                 0 auto: 3 when B x 16 <= the SM count and the rollout fits
+                                   (latency-bound single tanks), else 2 for B*N <= 65536,
+                                   else 1;
                                  1 per-substep kernels, one CUDA graph per tick;
                                  2 one cooperative launch per tick (k_coop);
-                                 3 rollout-resident clusters (opt-in; measured slower than 1
-                                   on C3): one thread-block cluster per rollout
+                                 3 rollout-resident clusters (1.5-1.9x the
+                                   cooperative tick for single tanks, 0.45x path 1 on C3):
+                                   one thread-block cluster per rollout
                                    keeps its particles in distributed shared memory for the
                                    whole tick (k_resident); SPH_EINVAL if it does not fit     */
     double skin_max;          /* 0: fixed skin.  > skin: adaptive skin per rollout (B5):

@@ -638,10 +638,16 @@ static TickArgs hold_args(const sph_ctx* ctx, int n, float damping, int pin) {
 // Resident-path eligibility at init: the smallest cluster (1, 2, 4, 8, 16 CTAs per rollout)
 // whose carve-up fits one CTA's shared memory and that the device can co-schedule.
 static bool res_setup(sph_ctx* ctx) {
-    int dev = 0, optin = 0;
+    int dev = 0, optin = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    for (int CS = 1; CS <= RES_MAXCS; CS *= 2) {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    // latency-bound small batches (B x 16 CTAs fit the SMs): the widest cluster that fits, so a
+    // substep's work spreads over the most SMs; otherwise the narrowest (least halo, fewest
+    // barriers per particle)
+    const bool wide = ctx->P.B * RES_MAXCS <= nsm;
+    for (int k = 0; k < 5; ++k) {
+        const int CS = wide ? (RES_MAXCS >> k) : (1 << k);
         ResParams R;
         int nt = 0;
         if (!res_layout(ctx->P, CS, optin, &R, &nt)) continue;
@@ -797,9 +803,14 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
     }
     // resident clusters (exec_path 3, opt-in)
     ctx->exec = ctx->coop ? 2 : 1;
-    // (auto never picks it: measured slower than the per-substep kernels on C3 and C3-P0, DESIGN.md
-    // section 7b -- one 19-warp CTA per SM and two cluster barriers per substep)
-    if (tp->exec_path == 3) {
+    // auto picks it for latency-bound small batches whose clusters all fit the GPU at once (B x
+    // 16 CTAs <= SMs): C1 / C2 single tanks and P0 run 1.5-1.9x faster than the cooperative tick
+    // (DESIGN.md 7b); for large batches the per-substep kernels win (one 19-warp CTA per SM and two
+    // cluster barriers per substep cannot match their 40+ warps per SM)
+    int nsm_ = 148, dev_ = 0;
+    cudaGetDevice(&dev_);
+    cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, dev_);
+    if (tp->exec_path == 3 || (tp->exec_path == 0 && (long long)P.B * RES_MAXCS <= nsm_)) {
         const bool ok = res_setup(ctx);
         if (!ok && tp->exec_path == 3) {
             sph_destroy(ctx);

@@ -14,7 +14,11 @@ BODY = [0.01, -0.02, 0.3, 0.02, -0.01, 0.05]
 
 
 def _ctx(t, **kw):
+    """Single-rollout context on the per-substep kernel path (exec_path 1): the decomposition
+    reuses those kernels, so the undecomposed reference must run them too (auto would pick the
+    resident clusters for one rollout, whose float32 summation order differs)."""
     from paper_2604_12505_b200 import SphContext
+    kw.setdefault("exec_path", 1)
     c = SphContext(t.params, t.pv32(), t.ghost_b, n_rollouts=1, **kw)
     c.set_body_state(np.array([t.body]))
     return c

@@ -40,8 +40,12 @@ def test_resident_path_is_selected_and_shaped():
     assert ctx.launches_per_tick() == 1
     ctx.close()
     auto = _ctx(t, B=64, rebin_every=0, skin=0.15 * t.params.h, exec_path=0)
-    assert auto.exec_path()[0] == 1      # opt-in only (measured slower)
+    assert auto.exec_path()[0] != 3      # large batches: the per-substep kernels
     auto.close()
+    one = _ctx(t, B=1, rebin_every=0, skin=0.15 * t.params.h, exec_path=0)
+    path, shape = one.exec_path()
+    assert path == 3 and shape["cluster_ctas"] == 16   # latency-bound: the widest cluster
+    one.close()
 
 
 @pytest.mark.parametrize("ell,jitter", [(1.0, 0.05), (4.0, 0.05)])
