@@ -584,6 +584,7 @@ static bool res_layout(const DevParams& P, int CS, int smem_max, ResParams* out,
     put(&R.o_rpv, 16ll * R.S);
     put(&R.o_gst, 16ll * std::max(P.G, 1));
     put(&R.o_glo, 16ll * std::max(P.G, 1));
+    put(&R.o_ghb, 16ll * std::max(P.G, 1));
     put(&R.o_part, 32ll * R.npart);
     put(&R.o_aux, 8ll * R.W);
     put(&R.o_xb, 8ll * R.S);
@@ -621,7 +622,29 @@ static cudaError_t launch_resident(sph_ctx* ctx, const TickArgs& T) {
     cfg.numAttrs = 1;
     const bool timed = ctx->live_every > 0 && T.u_seq != nullptr;
     if (timed) cudaEventRecord(ctx->res_ev[0], ctx->stream);
+#ifdef SPH_RES_TIMING
+    // diagnostic build: per-CTA phase timestamps of this launch appended to $SPH_RES_TIMING_FILE
+    // as [B * CS][n_sub][8] uint64 ns (header: CTAs, n_sub)
+    TickArgs Tt = T;
+    const size_t nclk = (size_t)P.B * ctx->res.CS * T.n_sub * 8;
+    cudaMalloc(&Tt.clk, nclk * 8);
+    cudaMemsetAsync(Tt.clk, 0, nclk * 8, ctx->stream);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_resident, P, ctx->D, ctx->res, Tt);
+    std::vector<unsigned long long> h(nclk);
+    cudaMemcpyAsync(h.data(), Tt.clk, nclk * 8, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(Tt.clk);
+    if (const char* fn = std::getenv("SPH_RES_TIMING_FILE")) {
+        if (FILE* f = std::fopen(fn, "ab")) {
+            const unsigned long long hdr[2] = {(unsigned long long)P.B * ctx->res.CS, (unsigned long long)T.n_sub};
+            std::fwrite(hdr, 8, 2, f);
+            std::fwrite(h.data(), 8, nclk, f);
+            std::fclose(f);
+        }
+    }
+#else
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_resident, P, ctx->D, ctx->res, T);
+#endif
     if (timed) cudaEventRecord(ctx->res_ev[1], ctx->stream);
     return e;
 }

@@ -38,7 +38,7 @@ struct ResParams {
     int CS, S, HCAP, W, KR, KQ, IDB, MCAP, NCT, npart;
     uint32_t idmask;
     // dynamic shared memory carve-up (byte offsets, 16-byte aligned)
-    int o_pv, o_rpv, o_gst, o_glo, o_part, o_aux, o_xb, o_nbr, o_key, o_rkey, o_nmk, o_obk, o_mkg,
+    int o_pv, o_rpv, o_gst, o_glo, o_ghb, o_part, o_aux, o_xb, o_nbr, o_key, o_rkey, o_nmk, o_obk, o_mkg,
         o_mks, o_wcs, o_obj, o_ncnt, o_misc;
     int smem;
 };
@@ -55,6 +55,7 @@ struct TickArgs {
     float damping;
     int pin;
     float ghost_angle0;
+    unsigned long long* clk;   // diagnostic build only (SPH_RES_TIMING); nullptr otherwise
 };
 
 struct ResMisc {
@@ -97,6 +98,21 @@ __device__ __forceinline__ T* cl_map(T* p, int rank) {
     asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"((uint64_t)p), "r"(rank));
     return reinterpret_cast<T*>(out);
 }
+
+// Phase timestamps of a diagnostic build (-DSPH_RES_TIMING): thread 0 of every CTA records
+// %globaltimer at 8 points of each substep into TickArgs::clk [cta][substep][8] (nanoseconds).
+#ifdef SPH_RES_TIMING
+#define RES_MARK(T_, ph_, it_)                                                                    \
+    do {                                                                                         \
+        if (threadIdx.x == 0 && (T_).clk) {                                                      \
+            unsigned long long t_;                                                               \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+            (T_).clk[((size_t)blockIdx.x * (T_).n_sub + (it_)) * 8 + (ph_)] = t_;                \
+        }                                                                                        \
+    } while (0)
+#else
+#define RES_MARK(T_, ph_, it_) do { } while (0)
+#endif
 
 __device__ __forceinline__ void set_status_at(RolloutState* rs, int code, int particle, long long step) {
     if (atomicCAS(&rs->status, 0, code) == 0) {
@@ -151,6 +167,7 @@ struct ResSmem {
                        //     written by the force pass (the halo of the other CTAs pulls it)
     float4* gst;       // [G] ghost world state (x_hi, y_hi, vx, vy)
     float4* glo;       // [G] (x_lo, y_lo, arm_x, arm_y)
+    double2* ghb;      // [G] body-frame ghost positions (constant; copied once per launch)
     double4* part;     // [npart] per-warp body partials of the whole rollout (written remotely)
     float2* aux;       // [W] (rho, P / rho^2)
     float2* xb;        // [S] own positions at the last rebuild
@@ -173,6 +190,7 @@ __device__ __forceinline__ ResSmem res_smem(const ResParams& R, unsigned char* b
     s.rpv = reinterpret_cast<float4*>(base + R.o_rpv);
     s.gst = reinterpret_cast<float4*>(base + R.o_gst);
     s.glo = reinterpret_cast<float4*>(base + R.o_glo);
+    s.ghb = reinterpret_cast<double2*>(base + R.o_ghb);
     s.part = reinterpret_cast<double4*>(base + R.o_part);
     s.aux = reinterpret_cast<float2*>(base + R.o_aux);
     s.xb = reinterpret_cast<float2*>(base + R.o_xb);
@@ -201,7 +219,7 @@ __device__ __forceinline__ void res_ghosts(const DevParams& P, const DevPtrs& D,
     const double* bd = s.m->body;
     const double c = bd[6], sn = bd[7], r0 = bd[0], r1 = bd[1], v0 = bd[3], v1 = bd[4], w = bd[5];
     for (int g = threadIdx.x; g < P.G; g += blockDim.x) {
-        const double2 q = __ldg(D.ghost_b + g);
+        const double2 q = s.ghb[g];
         const double ax = c * q.x - sn * q.y, ay = sn * q.x + c * q.y;
         const double wx = ax + r0, wy = ay + r1;
         const double vx = v0 - w * (wy - r1);
@@ -745,6 +763,7 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
         m->rby = rs->rby;
         m->need_rebin = 0;
     }
+    for (int g = tid; g < P.G; g += NT) s.ghb[g] = __ldg(D.ghost_b + g);
     __syncthreads();
     res_ghosts(P, D, s);
     cl_sync();   // bad_all initialised in every CTA before anyone may write it remotely
@@ -752,13 +771,17 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
     const int q0 = lo >> 5;   // global 32-slot group of own unit 0
     for (int it = 0; it < T.n_sub; ++it) {
         const long long step = step0 + it;
+        RES_MARK(T, 0, it);
         if (m->need_rebin) res_rebuild(P, R, s, rs, r, lo, n_own, step);
+        RES_MARK(T, 1, it);
         const Geom gm = res_geom(m, T.ghost_angle0);
         for (int u = warp; u < nunit; u += nwarp) {
             const int j = u * 32 + lane;
             if (j < n_own) res_density(P, R, s, gm, j);
         }
+        RES_MARK(T, 2, it);
         cl_sync();   // A: every CTA's own (rho, P/rho^2) written
+        RES_MARK(T, 3, it);
         const int wlo = m->wlo, whi = m->whi, nlow = lo - wlo, nhigh = whi - hi;
         for (int q = tid; q < nlow + nhigh; q += NT) {
             const int g = q < nlow ? wlo + q : hi + (q - nlow);
@@ -793,14 +816,17 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
         }
         if (bad)
             for (int t = 0; t < R.CS; ++t) cl_map(m->bad_all + r, t)[0] = bad;
+        RES_MARK(T, 4, it);
         cl_sync();   // B: every CTA's new own state, partials and flags written
-        for (int q = tid; q < nlow + nhigh; q += NT) {
-            const int g = q < nlow ? wlo + q : hi + (q - nlow);
-            const int ow = g / R.S;
-            s.pv[R.HCAP + (g - lo)] = cl_map(s.rpv, ow)[g - ow * R.S];
-        }
-        for (int j = tid; j < n_own; j += NT) s.pv[R.HCAP + j] = s.rpv[j];
-        if (warp == 0) {
+        RES_MARK(T, 5, it);
+        if (warp != 0) {   // halo state pull + own copy, overlapping warp 0's body step
+            for (int q = tid - 32; q < nlow + nhigh; q += NT - 32) {
+                const int g = q < nlow ? wlo + q : hi + (q - nlow);
+                const int ow = g / R.S;
+                s.pv[R.HCAP + (g - lo)] = cl_map(s.rpv, ow)[g - ow * R.S];
+            }
+            for (int j = tid - 32; j < n_own; j += NT - 32) s.pv[R.HCAP + j] = s.rpv[j];
+        } else {
             // fixed-order fp64 reduction of all npart warp partials (identical in every CTA)
             double4 f = make_double4(0, 0, 0, 0);
             for (int q = lane; q < R.npart; q += 32) {
@@ -857,9 +883,11 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
             }
         }
         __syncthreads();
+        RES_MARK(T, 6, it);
         if (m->stop) break;
         res_ghosts(P, D, s);
         __syncthreads();
+        RES_MARK(T, 7, it);
     }
     // ---- tick end: state out (sorted slots, canonical ids, rebuild-time cells) ----
     for (int j = tid; j < n_own; j += NT) {
