@@ -278,6 +278,7 @@ static size_t carve(const DevParams& P, char* base, DevPtrs* D) {
     put(d.garm, BG * 8);
     put(d.ghost_b, (size_t)std::max(P.G, 1) * 16);
     put(d.body, (size_t)P.B * 48);
+    put(d.body_cs, (size_t)P.B * 16);
     put(d.u_cur, (size_t)P.B * 12);
     put(d.part, (size_t)P.B * P.npart * 32);
     put(d.part2, (size_t)P.B * P.bsplit * 32);
@@ -325,8 +326,12 @@ static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle
         k_body_reduce<<<dim3(ctx->P.bsplit, ctx->P.B), BRED_T, 0, s>>>(ctx->P, ctx->D);
         pdl = false;
     }
+    // large tanks in small batches (C4): the ghost update spread over k_ghosts' CTAs
+    const int split = (ctx->P.B < 148 && ctx->P.G >= 4 * ctx->body_threads) ? 1 : 0;
     launch_k(pdl, k_body, dim3(ctx->P.B), dim3(ctx->body_threads), (size_t)ctx->body_threads * sizeof(double4),
-             s, ctx->P, ctx->D, pin, ghost_angle0);
+             s, ctx->P, ctx->D, pin, ghost_angle0, split ^ 1);
+    if (split)
+        launch_k(pdl, k_ghosts, dim3((ctx->P.G + GH_T - 1) / GH_T, ctx->P.B), dim3(GH_T), 0, s, ctx->P, ctx->D);
 }
 
 // Grid-wide counting sort by cell of every rollout with need_rebin (7 kernels); with_nlist adds
@@ -517,7 +522,8 @@ static int live_samples(const sph_ctx* ctx) {
 // kernels per substep: small path 5 (plan, rebuild_small, density, force, body); multi-kernel
 // path 4 + 8 rebuild kernels (the 8 run only in substeps where some rollout rebuilds).
 static int launches_per_substep(const sph_ctx* ctx) {
-    return (ctx->small ? (ctx->fork ? 7 : 6) : 12) + (ctx->P.bsplit > 1 ? 1 : 0);
+    return (ctx->small ? (ctx->fork ? 7 : 6) : 12) + (ctx->P.bsplit > 1 ? 1 : 0) +
+           ((ctx->P.B < 148 && ctx->P.G >= 4 * ctx->body_threads) ? 1 : 0);
 }
 
 static sph_status check_launch(sph_ctx* ctx) {

@@ -150,6 +150,7 @@ struct DevPtrs {
     float2* garm;        // [B][G] ghost arm r_g - r (world frame)
     double2* ghost_b;    // [G] body-frame ghost positions
     double* body;        // [B][6] r_x r_y theta rd_x rd_y thd
+    double2* body_cs;    // [B] (cos theta, sin theta) of the current body state (k_ghosts)
     float* u_cur;        // [B][3] current ZOH input
     double4* part;       // [B][npart] per-warp (F_x, F_y, T, max relative speed) partials
     double4* part2;      // [B][bsplit] chunk sums of part (bsplit > 1)

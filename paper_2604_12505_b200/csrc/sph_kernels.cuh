@@ -1102,8 +1102,10 @@ __global__ void __launch_bounds__(BRED_T) k_body_reduce(DevParams P, DevPtrs D) 
 // the first nt threads (nt = k_body's block size, chosen from N only, so the bits never depend on
 // the launch shape), Newton-Euler kick-then-drift, status, parity flips, rebuild decision, then
 // the ghosts of the next substep by every thread.  red: shared memory [>= nt].  CTA-uniform.
+// ghosts_here = 0 (large tanks, ghost_split): the ghost update of the next substep is left to
+// k_ghosts, spread over many CTAs (cos / sin of theta handed over in D.body_cs)
 __device__ __forceinline__ void body_step(const DevParams& P, const DevPtrs& D, int b, int pin,
-                                          float ghost_angle0, double4* red, int nt) {
+                                          float ghost_angle0, double4* red, int nt, int ghosts_here = 1) {
     RolloutState* rs = D.rs + b;
     __shared__ double sbody[8];
     // thread 0's state loads, all issued before the reduction (independent; they complete while
@@ -1203,22 +1205,41 @@ __device__ __forceinline__ void body_step(const DevParams& P, const DevPtrs& D, 
         }
         rs->step += 1;
         if (r_status) rs->frozen = 1;
+        D.body_cs[b] = make_double2(sbody[6], sbody[7]);
     }
     __syncthreads();
-    ghost_update(P, D, b, sbody, threadIdx.x, blockDim.x);
+    if (ghosts_here) ghost_update(P, D, b, sbody, threadIdx.x, blockDim.x);
     __syncthreads();   // sbody / red reusable by the caller's next rollout
 }
 
 // blockDim.x = a power of two <= 1024, chosen from N only (so the reduction order, and hence
 // the bits, never depend on the batch size).
 __global__ void __launch_bounds__(1024) k_body(DevParams P, DevPtrs D, int pin,
-                                               float ghost_angle0) {
+                                               float ghost_angle0, int ghosts_here) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ double4 red[];   // [blockDim.x]
     const int b = blockIdx.x;
     if (D.rs[b].frozen) return;        // CTA-uniform
-    body_step(P, D, b, pin, ghost_angle0, red, blockDim.x);
+    body_step(P, D, b, pin, ghost_angle0, red, blockDim.x, ghosts_here);
+}
+
+// Eq. kinematicghost for large tanks (G >= 4 x k_body's threads: C4 has 9,912 ghosts on one
+// rollout, which one k_body CTA updated in ~10 us): grid (ceil(G / 256), B), the same
+// ghost_update arithmetic from the body state and (cos, sin) k_body left -- identical bits.
+constexpr int GH_T = 256;
+__global__ void __launch_bounds__(GH_T) k_ghosts(DevParams P, DevPtrs D) {
+    pdl_wait();
+    pdl_trigger();
+    const int b = blockIdx.y;
+    double bd[8];
+    const double* body = D.body + (size_t)b * 6;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) bd[c] = body[c];
+    const double2 cs = D.body_cs[b];
+    bd[6] = cs.x;
+    bd[7] = cs.y;
+    ghost_update(P, D, b, bd, blockIdx.x * GH_T + threadIdx.x, gridDim.x * GH_T);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1386,6 +1407,7 @@ __global__ void k_reset_rollout(DevParams P, DevPtrs D, int b0, float ghost_angl
         const double* body = D.body + (size_t)b * 6;
         for (int c = 0; c < 6; ++c) sbody[c] = body[c];
         sincos(body[2], &sbody[7], &sbody[6]);
+        D.body_cs[b] = make_double2(sbody[6], sbody[7]);
         D.geom[b] = Geom{(float)body[0], (float)body[1], (float)(body[2] + ghost_angle0),
                          (float)body[3], (float)body[4], {0.f, 0.f, 0.f}};
     }
