@@ -67,6 +67,40 @@ def test_gloo_gather_matches_single_rank(n_total):
     assert np.array_equal(got, np.concatenate([u, 2 * u], axis=2))
 
 
+def _ds_worker(rank, world, port, n_total, K, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_12505_b200.ensemble import gather_dataset
+    ids = list(shard(n_total, world, rank))
+    u = torch.from_numpy(si.ensemble_inputs(ids, K)[0]) if ids else torch.zeros((0, K, 3))
+    y = torch.cat([u, -u], dim=2)                      # stand-in y [B, K, 6], u_applied = u
+    st = torch.tensor([g % 3 for g in ids], dtype=torch.int32)
+    yg, ug, sg = gather_dataset(y, u, st)
+    if rank == 0:
+        q.put((yg.numpy(), ug.numpy(), sg.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_gather_dataset_y_u_status():
+    """The dataset gather of the C5 path (y, u_applied and the per-rollout status in one
+    collective) returns every rank's rows in global-id order."""
+    n_total, K, world = 7, 4, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ds_worker, args=(r, world, port, n_total, K, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    yg, ug, sg = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    u = si.ensemble_inputs(range(n_total), K)[0]
+    assert np.array_equal(yg, np.concatenate([u, -u], axis=2)) and np.array_equal(ug, u)
+    assert sg.tolist() == [g % 3 for g in range(n_total)]
+
+
 # ---- domain decomposition (SURVEY 8(f) f2): slab ranges and the in-place padded all-gather ----
 
 def test_slab_ranges():
