@@ -551,6 +551,17 @@ static sph_status all_failed(sph_ctx* ctx) {
     return fail(ctx, SPH_EBLOWUP, "every rollout has a non-zero numerical status");
 }
 
+// Raise (never lower) a kernel's dynamic shared-memory limit: the attribute is per function and
+// process-wide, so a context must not shrink it under another context that needs more.
+template <class K>
+static cudaError_t raise_smem_limit(K kern, size_t bytes) {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    if ((size_t)fa.maxDynamicSharedSizeBytes >= bytes) return cudaSuccess;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 // ---------------------------------------------------------------------------------------
 // Resident path (k_resident, sph_resident.cuh)
 // ---------------------------------------------------------------------------------------
@@ -680,7 +691,7 @@ static bool res_setup(sph_ctx* ctx) {
         ResParams R;
         int nt = 0;
         if (!res_layout(ctx->P, CS, optin, &R, &nt)) continue;
-        if (cudaFuncSetAttribute(k_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, R.smem) != cudaSuccess) {
+        if (raise_smem_limit(k_resident, R.smem) != cudaSuccess) {
             cudaGetLastError();
             continue;
         }
@@ -798,8 +809,7 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             sph_destroy(ctx);
             return fail(nullptr, SPH_EINVAL, "rebuild_path = 1 but the rollout does not fit in shared memory");
         }
-        if (want && cudaFuncSetAttribute(k_rebuild_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem) != cudaSuccess) {
+        if (want && raise_smem_limit(k_rebuild_small, smem) != cudaSuccess) {
             cudaGetLastError();
             want = false;
         }

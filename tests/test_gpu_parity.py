@@ -534,3 +534,24 @@ def test_adaptive_skin_policies_keep_every_pair_listed(mode, skin, skin_max):
     assert _csr_sets(*nf) == _csr_sets(*O.neighbours_f32(p32, H * H))
     for c in (a, f):
         c.close()
+
+
+def test_contexts_of_different_sizes_coexist():
+    """Kernel shared-memory limits are process-wide attributes: a context created after another
+    with a smaller rollout must not shrink the limit the first one's kernels need (C2 batch on the
+    per-rollout rebuild path and the resident path, then a C1 context, then the C2 contexts
+    again)."""
+    big = si.make_tank(4.0)
+    small = si.make_tank(1.0)
+    kw = dict(rebin_every=0, skin=0.15 * big.params.h)
+    a = _ctx(big, B=2, rebuild_path=1, exec_path=1, **kw)
+    r = _ctx(big, B=1, exec_path=3, **kw)
+    c = _ctx(small, B=1, rebin_every=0, skin=0.15 * small.params.h, rebuild_path=1, exec_path=3)
+    u = np.array([[2.0, 1.0, 0.5]], np.float32)
+    c.step(u, 5)
+    a.step(np.repeat(u, 2, 0), 5)
+    r.step(u, 5)
+    assert a.get_status()[0].max() == 0 and r.get_status()[0].max() == 0
+    assert a.counters()[1].min() >= 1 and r.counters()[1][0] >= 1
+    for x in (a, r, c):
+        x.close()
