@@ -108,7 +108,7 @@ typedef struct {
                                  rollout's current 2h + skin, so the sums are unchanged.      */
     int skin_mode;            /* with skin_max > skin: 0 per-rollout adaptive skin (B5);
                                  1 per-particle half-skins (B6): at every rebuild
-                                 particle i gets hs_i = clamp(10 dt |v_i - v_body|, skin / 2,
+                                 particle i gets hs_i = clamp(20 dt |v_i - v_body|, skin / 2,
                                  skin_max / 2), pair (i, j) is listed within 2h + hs_i + hs_j,
                                  and the lists are rebuilt when some particle's displacement
                                  reaches 0.98 hs_i (exec_path 3: mode 0 only).                */
