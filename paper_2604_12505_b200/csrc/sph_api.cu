@@ -722,6 +722,8 @@ static bool res_setup(sph_ctx* ctx) {
     return false;
 }
 
+__global__ void k_force_rebin(RolloutState* rs, int b) { rs[b].need_rebin = 1; }
+
 // ---------------------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------------------
@@ -987,6 +989,9 @@ sph_status sph_set_domain(sph_ctx* ctx, int slot_lo, int slot_hi) {
     P.pf_d = P.pf_f = 0;
     ctx->coop = false;
     ctx->small = false;
+    // the resident path persists its Verlet lists in shared memory only (rs->need_rebin may be 0
+    // with no lists in global memory): the kernel path starts with a rebuild
+    if (ctx->exec == 3) k_force_rebin<<<1, 1, 0, ctx->stream>>>(ctx->D.rs, 0);
     ctx->exec = 1;
     if (ctx->tick_graph) {
         cudaGraphExecDestroy(ctx->tick_graph);
@@ -1301,7 +1306,6 @@ sph_status sph_debug_cells(sph_ctx* ctx, int rollout, int32_t* cells, float* gri
     return SPH_OK;
 }
 
-__global__ void k_force_rebin(RolloutState* rs, int b) { rs[b].need_rebin = 1; }
 
 sph_status sph_debug_neighbours(sph_ctx* ctx, int rollout, int64_t* nf_off, int32_t* nf_idx,
                                 int64_t nf_cap, int64_t* g2_off, int32_t* g2_idx,
