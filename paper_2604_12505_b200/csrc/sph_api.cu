@@ -641,9 +641,9 @@ static cudaError_t launch_resident(sph_ctx* ctx, const TickArgs& T) {
     if (timed) cudaEventRecord(ctx->res_ev[0], ctx->stream);
 #ifdef SPH_RES_TIMING
     // diagnostic build: per-CTA phase timestamps of this launch appended to $SPH_RES_TIMING_FILE
-    // as [B * CS][n_sub][8] uint64 ns (header: CTAs, n_sub)
+    // as [B * CS][n_sub][RES_NMARK] uint64 ns (header: CTAs, n_sub, RES_NMARK)
     TickArgs Tt = T;
-    const size_t nclk = (size_t)P.B * ctx->res.CS * T.n_sub * 8;
+    const size_t nclk = (size_t)P.B * ctx->res.CS * T.n_sub * RES_NMARK;
     cudaMalloc(&Tt.clk, nclk * 8);
     cudaMemsetAsync(Tt.clk, 0, nclk * 8, ctx->stream);
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_resident, P, ctx->D, ctx->res, Tt);
@@ -653,8 +653,9 @@ static cudaError_t launch_resident(sph_ctx* ctx, const TickArgs& T) {
     cudaFree(Tt.clk);
     if (const char* fn = std::getenv("SPH_RES_TIMING_FILE")) {
         if (FILE* f = std::fopen(fn, "ab")) {
-            const unsigned long long hdr[2] = {(unsigned long long)P.B * ctx->res.CS, (unsigned long long)T.n_sub};
-            std::fwrite(hdr, 8, 2, f);
+            const unsigned long long hdr[3] = {(unsigned long long)P.B * ctx->res.CS, (unsigned long long)T.n_sub,
+                                               (unsigned long long)RES_NMARK};
+            std::fwrite(hdr, 8, 3, f);
             std::fwrite(h.data(), 8, nclk, f);
             std::fclose(f);
         }

@@ -100,18 +100,36 @@ __device__ __forceinline__ T* cl_map(T* p, int rank) {
 }
 
 // Phase timestamps of a diagnostic build (-DSPH_RES_TIMING): thread 0 of every CTA records
-// %globaltimer at 8 points of each substep into TickArgs::clk [cta][substep][8] (nanoseconds).
+// %globaltimer at RES_NMARK points of each substep into TickArgs::clk [cta][substep][RES_NMARK]
+// (nanoseconds): 0 start, 1 after rebuild, 2 after density, 3 after barrier A, 4 after aux pull +
+// forces, 5 after barrier B, 6 after the partial loads (warp 0), 7 after the warp reduction,
+// 8 after the body update (lane 0), 9 after the pv pull (block barrier), 10 after the ghosts.
+// RES_MARKD: the same, ordered after the computation of the double v (a register dependency).
+// The stamps perturb the code they bracket: the diagnostic build runs a C2 substep in 14.0 us
+// against 9.3 us without them, 4.5 us of it in warp 0's fp64 butterfly right after a stamp store
+// (a shared-memory reduction there brings the build to 9.9 us; the product build is slower with
+// it) -- read phase SHARES and per-CTA spreads from it, not absolute times.
+constexpr int RES_NMARK = 11;
 #ifdef SPH_RES_TIMING
 #define RES_MARK(T_, ph_, it_)                                                                    \
     do {                                                                                         \
         if (threadIdx.x == 0 && (T_).clk) {                                                      \
             unsigned long long t_;                                                               \
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
-            (T_).clk[((size_t)blockIdx.x * (T_).n_sub + (it_)) * 8 + (ph_)] = t_;                \
+            (T_).clk[((size_t)blockIdx.x * (T_).n_sub + (it_)) * RES_NMARK + (ph_)] = t_;        \
+        }                                                                                        \
+    } while (0)
+#define RES_MARKD(T_, ph_, it_, v_)                                                               \
+    do {                                                                                         \
+        if (threadIdx.x == 0 && (T_).clk) {                                                      \
+            unsigned long long t_;                                                               \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_) : "d"(v_));                     \
+            (T_).clk[((size_t)blockIdx.x * (T_).n_sub + (it_)) * RES_NMARK + (ph_)] = t_;        \
         }                                                                                        \
     } while (0)
 #else
 #define RES_MARK(T_, ph_, it_) do { } while (0)
+#define RES_MARKD(T_, ph_, it_, v_) do { } while (0)
 #endif
 
 __device__ __forceinline__ void set_status_at(RolloutState* rs, int code, int particle, long long step) {
@@ -836,6 +854,7 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
                 f.z += v.z;
                 f.w = fmax(f.w, v.w);
             }
+            RES_MARKD(T, 6, it, f.x + f.y + f.z + f.w);
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) {
                 f.x += __shfl_xor_sync(0xffffffffu, f.x, d);
@@ -843,6 +862,7 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
                 f.z += __shfl_xor_sync(0xffffffffu, f.z, d);
                 f.w = fmax(f.w, __shfl_xor_sync(0xffffffffu, f.w, d));
             }
+            RES_MARKD(T, 7, it, f.x + f.y + f.z + f.w);
             if (lane == 0) {
                 double* bd = m->body;
                 if (!T.pin) {
@@ -880,14 +900,15 @@ __global__ void __launch_bounds__(RES_MAXT, 1) k_resident(DevParams P, DevPtrs D
                 }
                 m->it_done = it + 1;
                 m->stop = stop;
+                RES_MARKD(T, 8, it, bd[2]);
             }
         }
         __syncthreads();
-        RES_MARK(T, 6, it);
+        RES_MARK(T, 9, it);
         if (m->stop) break;
         res_ghosts(P, D, s);
         __syncthreads();
-        RES_MARK(T, 7, it);
+        RES_MARK(T, 10, it);
     }
     // ---- tick end: state out (sorted slots, canonical ids, rebuild-time cells) ----
     for (int j = tid; j < n_own; j += NT) {
