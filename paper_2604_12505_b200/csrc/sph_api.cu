@@ -43,6 +43,7 @@ struct sph_ctx {
     size_t small_smem = 0;
     int small_grid = 0;
     cudaStream_t side = nullptr;
+    cudaStream_t side2 = nullptr;   // capture of the IF node's body (multi-kernel path)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool fork = true;   // small path: rebuild branch concurrent with density/forces
     bool pdl = true;    // programmatic dependent launch on the substep chain
@@ -322,7 +323,7 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
 
 static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0, bool pdl = false) {
     pdl = pdl && ctx->pdl;
-    if (ctx->P.bsplit > 1) {
+    if (ctx->P.bsplit > 1) {   // (with PDL measured slower on C4: 207.5 vs 204.6 ms / tick)
         k_body_reduce<<<dim3(ctx->P.bsplit, ctx->P.B), BRED_T, 0, s>>>(ctx->P, ctx->D);
         pdl = false;
     }
@@ -369,8 +370,7 @@ static void launch_nlist_density(sph_ctx* ctx, cudaStream_t s, bool pdl = false)
 // Multi-kernel path inside a graph capture: the plan kernel sets a conditional handle and the
 // eight grid-wide rebuild kernels sit in the body of an IF node (skipped when no rollout of
 // the batch needs a rebuild this substep).
-static cudaError_t add_conditional_rebin(sph_ctx* ctx) {
-    cudaStream_t s = ctx->stream;
+static cudaError_t add_conditional_rebin(sph_ctx* ctx, cudaStream_t s) {
     cudaStreamCaptureStatus st;
     cudaGraph_t g;
     const cudaGraphNode_t* deps = nullptr;
@@ -391,16 +391,16 @@ static cudaError_t add_conditional_rebin(sph_ctx* ctx) {
     if ((e = cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies)) != cudaSuccess)
         return e;
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    if ((e = cudaStreamBeginCaptureToGraph(ctx->side, body, nullptr, nullptr, 0,
+    if ((e = cudaStreamBeginCaptureToGraph(ctx->side2, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
         return e;
-    launch_rebin(ctx, ctx->side);
+    launch_rebin(ctx, ctx->side2);
     // lists + densities of the rebuilt rollouts inside the IF body too: substeps without a
     // rebuild then launch no list kernel at all (C4: one launch of ~8,000 empty CTAs less per
     // substep); they only touch rebuilt rollouts, k_density the others (disjoint), so running
     // them before k_density changes nothing
-    launch_nlist_density(ctx, ctx->side);
-    return cudaStreamEndCapture(ctx->side, &body);
+    launch_nlist_density(ctx, ctx->side2);
+    return cudaStreamEndCapture(ctx->side2, &body);
 }
 
 // Rebuild (only rollouts that need it) + densities.  Small path: the plan kernel builds the
@@ -451,8 +451,19 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
         return cudaSuccess;
     } else {
         if (capturing) {
-            cudaError_t e = add_conditional_rebin(ctx);
+            // plan + IF node on a forked branch, concurrent with the densities of the rollouts
+            // that do not rebuild (disjoint rollouts, as on the small path): the IF node's own
+            // scheduling cost (~7 us per substep, tools/micro/ifnode.cu) hides under k_density
+            cudaEventRecord(ctx->ev_fork, s);
+            cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+            cudaError_t e = add_conditional_rebin(ctx, ctx->side);
             if (e != cudaSuccess) return e;
+            cudaEventRecord(ctx->ev_join, ctx->side);
+            live_mark(ev, LV_DEN0, s);
+            launch_density(ctx, s, 1, np);
+            live_mark(ev, LV_DEN1, s);
+            cudaStreamWaitEvent(s, ctx->ev_join, 0);
+            return cudaSuccess;
         } else {
             k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
             launch_rebin(ctx);
@@ -822,6 +833,7 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             ctx->small_grid = std::max(1, std::min(P.B, nsm));
         }
         if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
             (e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming)) != cudaSuccess)
             return bail("side stream", e);
@@ -1624,6 +1636,7 @@ void sph_destroy(sph_ctx* ctx) {
     if (ctx->stage) cudaFree(ctx->stage);
     if (ctx->dbg_buf) cudaFree(ctx->dbg_buf);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->side2) cudaStreamDestroy(ctx->side2);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     for (auto e : ctx->live_ev) cudaEventDestroy(e);
