@@ -432,10 +432,11 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
         return cudaSuccess;
     }
     if (ctx->small) {   // (forces are launched by launch_substep, see there)
-        launch_k(first_pdl && np && ctx->pdl, k_rebuild_plan, dim3(1), dim3(RB_T), 0, s, P, ctx->D,
-                 (cudaGraphConditionalHandle)0, 0);
+        // the plan kernel heads the rebuild branch: k_density / mode-1 forces read need_rebin
+        // themselves, only the branch needs the work list
         cudaEventRecord(ctx->ev_fork, s);
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+        k_rebuild_plan<<<1, RB_T, 0, ctx->side>>>(P, ctx->D, (cudaGraphConditionalHandle)0, 0);
         k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
         launch_nlist_density(ctx, ctx->side, true);
         if (ctx->m2side) {   // (timing nodes on the side stream: the force time is the sum
