@@ -597,11 +597,13 @@ def run_horizon(a):
                      "failed_rollouts": int((st != 0).sum())})
         print(json.dumps(rows[-1]), flush=True)
     ck = clocks.stop()
+    # isolated per-kernel times in the state the horizon ends in (after the timed windows)
+    prof_end = ctx.profile(a.profile_substeps)
     tot_ms = sum(r["ms_per_tick"] * win for r in rows)
     line = {"metric": METRIC, "mode": "long-horizon", "workload": desc, "rollouts": B,
             "train_ticks": n_ticks, "value": B * t.n_fluid * sp.n_sub * n_ticks / (tot_ms / 1e3),
             "unit": UNIT, "exec_path": ctx.exec_path()[0], "skin_h": a.skin, "skin_max_h": a.skin_max,
-            "windows": rows,
+            "windows": rows, "isolated_ms_at_end": prof_end,
             "clocks": ck, "y_finite": bool(torch.isfinite(y).all().item())}
     ctx.close()
     print(json.dumps(line), flush=True)

@@ -356,11 +356,18 @@ static void launch_nlist_density(sph_ctx* ctx, cudaStream_t s, bool pdl = false)
     const DevParams& P = ctx->P;
     const int gy = std::min(P.B, 64);
     pdl = pdl && ctx->pdl;
+    // the per-particle half-skin list radius (B6) only in its own instances
+#define SPH_NLD(TN)                                                                                 \
+    (P.perpart ? launch_k(pdl, k_nlist_density<TN, true>, dim3(std::max(1, (P.own_n + TN - 1) / TN), gy), \
+                          dim3(TN), 0, s, P, ctx->D)                                                \
+               : launch_k(pdl, k_nlist_density<TN, false>, dim3(std::max(1, (P.own_n + TN - 1) / TN), gy), \
+                          dim3(TN), 0, s, P, ctx->D))
     switch (P.tn) {
-        case 256: launch_k(pdl, k_nlist_density<256>, dim3(std::max(1, (P.own_n + 255) / 256), gy), dim3(256), 0, s, P, ctx->D); break;
-        case 64: launch_k(pdl, k_nlist_density<64>, dim3(std::max(1, (P.own_n + 63) / 64), gy), dim3(64), 0, s, P, ctx->D); break;
-        default: launch_k(pdl, k_nlist_density<128>, dim3(std::max(1, (P.own_n + 127) / 128), gy), dim3(128), 0, s, P, ctx->D); break;
+        case 256: SPH_NLD(256); break;
+        case 64: SPH_NLD(64); break;
+        default: SPH_NLD(128); break;
     }
+#undef SPH_NLD
 }
 
 // Rebuild (only rollouts that need it) + densities.  Small path: the plan kernel builds the

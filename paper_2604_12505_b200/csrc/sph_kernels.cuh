@@ -504,7 +504,8 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_plan(DevParams P, DevPtrs D,
 // Returns max |j - i| over the list entries (the staging window of k_density / k_force).
 // DENS = true also accumulates the fluid density sum of the appended (2h + skin) candidates
 // that lie within 2h into *wf (self term included); on list overflow *wf is not valid.
-template <bool DENS = false, class PosF>
+// PP = false: the per-particle half-skin radius (B6) compiled out (callers check P.perpart).
+template <bool DENS = false, bool PP = true, class PosF>
 __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs& D, int b, int i,
                                                const uint32_t* cs, uint32_t cell, PosF&& pos,
                                                float* wf_out = nullptr) {
@@ -521,7 +522,7 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
     const int cy = (int)cell / P.nx, cx = (int)cell - cy * P.nx;
     const float RL2u = D.rs[b].rl2;  // this rollout's list radius^2 (uniform / B5 skin)
     const float* __restrict__ hs = D.hs + o;
-    const float hsi = P.perpart ? hs[i] : 0.0f;
+    const float hsi = PP && P.perpart ? hs[i] : 0.0f;
     for (int dy = -1; dy <= 1 && !ovf; ++dy) {
         const int c0 = (cy + dy) * P.nx + cx - 1;
         const int j0 = (int)cs[c0], j1 = (int)cs[c0 + 3];
@@ -533,7 +534,7 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
                 const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
                 // list radius: 2h + skin, or 2h + hs_i + hs_j (per-particle skins, B6)
                 float RL2 = RL2u;
-                if (P.perpart) {
+                if (PP && P.perpart) {
                     const float RL = __fadd_rn(P.Hf, __fadd_rn(hsi, hs[base + k]));
                     RL2 = __fmul_rn(RL, RL);
                 }
@@ -696,20 +697,19 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
 // slot cells and sorted state come from the sort (k_rebuild_small or the grid-wide
 // rebuild kernels); the list just written by a thread is read back by the same thread.
 // lists + density of slot i of the rebuilt rollout b (every lane of the warp calls it)
-template <bool NC = true>
+template <bool NC = true, bool PP = true>
 __device__ __forceinline__ void nlist_density_at(const DevParams& P, const DevPtrs& D, int b, int i) {
     RolloutState* rs = D.rs + b;
     const size_t o = (size_t)b * P.N;
     const float4* __restrict__ pv = opaque(D.pv[rs->sp ^ 1] + o);   // sorted (rebuilt) buffer
-    auto pos = [&](uint32_t j) {
-        const float4 v = ld<NC>(pv + j);
-        return make_float2(v.x, v.y);
+    auto pos = [&](uint32_t j) {   // (x, y) half of the state: one 8-byte load
+        return ld<NC>(reinterpret_cast<const float2*>(pv + j));
     };
     int span = 0;
     if (i < P.N) {
         float wf;
-        span = build_list_core<true>(P, D, b, i, D.cstart + (size_t)b * (P.ncell + 1),
-                                     D.skey[o + i], pos, &wf);
+        span = build_list_core<true, PP>(P, D, b, i, D.cstart + (size_t)b * (P.ncell + 1),
+                                         D.skey[o + i], pos, &wf);
         if (span >= 0) finish_density<NC>(P, D, b, i, pos((uint32_t)i), wf);
         else density_core<false>(P, D, b, i, pos);   // list overflow: cell-scan density
     }
@@ -717,13 +717,13 @@ __device__ __forceinline__ void nlist_density_at(const DevParams& P, const DevPt
     if ((threadIdx.x & 31) == 0 && span > 0) atomicMax(&rs->span, span);
 }
 
-template <int TN>
+template <int TN, bool PP>
 __global__ void __launch_bounds__(TN) k_nlist_density(DevParams P, DevPtrs D) {
     pdl_wait();
     pdl_trigger();
     const int count = *D.rcount;
     const int i = P.own_lo + blockIdx.x * TN + threadIdx.x;
-    for (int w = blockIdx.y; w < count; w += gridDim.y) nlist_density_at(P, D, D.rlist[w], i);
+    for (int w = blockIdx.y; w < count; w += gridDim.y) nlist_density_at<true, PP>(P, D, D.rlist[w], i);
 }
 
 // ---------------------------------------------------------------------------------------

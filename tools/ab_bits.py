@@ -34,6 +34,17 @@ for ell, B, pvf in ((1.0, 3, None), (4.0, 2, "bench_data/settled_ell4.npz")):
     out[tag + "_reb"] = ctx.counters()[1]
     print(tag, "path", ctx.exec_path(), "rebuilds", ctx.counters()[1])
     ctx.close()
+# small path (per-rollout rebuild branch, k_nlist_density) on 4 C2 tanks, 3 ticks
+t = si.make_tank(4.0)
+pv = np.ascontiguousarray(np.load("bench_data/settled_ell4.npz")["pv"], dtype=np.float32)
+ctx = SphContext(t.params, pv, t.ghost_b, n_rollouts=4, rebin_every=0, skin=0.15 * t.params.h,
+                 exec_path=1, rebuild_path=1, skin_max=0.5 * t.params.h)
+y, _ = ctx.rollout(si.ensemble_inputs(range(4), 3)[0] * 20.0)
+out["small_y"] = y
+out["small_pv"] = np.stack([ctx.get_particles(b, with_rho=True)[1] for b in range(4)])
+out["small_reb"] = ctx.counters()[1]
+print("small path rebuilds", ctx.counters()[1])
+ctx.close()
 # large tank (bsplit > 1: fused body kernel), per-particle half-skins as the C4 bench
 t = si.make_tank(42.0)
 ctx = SphContext(t.params, t.pv32(), t.ghost_b, n_rollouts=1, rebin_every=0, skin=0.15 * t.params.h,
