@@ -606,7 +606,14 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
     uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_perm + P.N);
     const int count = *D.rcount;
     const int T = RB_T, tid = threadIdx.x;
-    for (int w = blockIdx.x; w < count; w += gridDim.x) {
+    // active CTAs: about one per 3.5 rebuilding rollouts, at least gridDim / 8 -- every resident
+    // 1024-thread sort CTA takes half an SM from the concurrent densities / forces, so a few CTAs
+    // each sorting several rollouts beat one per rollout (C3 window 97.3 -> 96.6 ms per tick at
+    // 18 CTAs, but 9.3 G/s at the horizon's steady state; 74 CTAs: 13.0 -> 13.3 G/s there).
+    // Which CTA sorts a rollout does not change its bits.
+    const int G = min((int)gridDim.x, max((int)gridDim.x / 8, (2 * count + 6) / 7));
+    if ((int)blockIdx.x >= G) return;
+    for (int w = blockIdx.x; w < count; w += G) {
         const int b = D.rlist[w];
         RolloutState* rs = D.rs + b;
         const int sp = rs->sp, ip = rs->ip;
