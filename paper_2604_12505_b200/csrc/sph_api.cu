@@ -351,10 +351,13 @@ static void launch_rebin(sph_ctx* ctx, cudaStream_t s = nullptr, bool with_nlist
     if (with_nlist) k_nlist<<<gp, TILE, 0, s>>>(P, ctx->D);
 }
 
-// lists + densities of the rebuilt rollouts (work list), spread over the whole GPU
+// lists + densities of the rebuilt rollouts (work list), spread over the whole GPU: grid.y
+// work-list slots (CTAs beyond the count return at once).  128 slots: the horizon's steady
+// state (~260 rebuilding rollouts per substep) 13.37 -> 13.61 G/s against 64, the calm window
+// unchanged (256: 13.68 / slightly slower window; 16 / 32: slower in both, DESIGN.md r02.30)
 static void launch_nlist_density(sph_ctx* ctx, cudaStream_t s, bool pdl = false) {
     const DevParams& P = ctx->P;
-    const int gy = std::min(P.B, 64);
+    const int gy = std::min(P.B, 128);
     pdl = pdl && ctx->pdl;
     // the per-particle half-skin list radius (B6) only in its own instances
 #define SPH_NLD(TN)                                                                                 \
