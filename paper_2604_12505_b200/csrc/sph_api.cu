@@ -434,7 +434,7 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
     const bool np = ev == nullptr;   // no timing nodes in this substep
     if (ctx->small && !ctx->fork) {   // serial: sort + lists/densities of the rebuilt rollouts first
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
-        k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
+        k_rebuild_small<<<ctx->small_grid, RBS_T, ctx->small_smem, s>>>(P, ctx->D);
         launch_nlist_density(ctx, s);
         live_mark(ev, LV_DEN0, s);
         launch_density(ctx, s, 1);
@@ -447,7 +447,7 @@ static cudaError_t launch_rebuild_and_density(sph_ctx* ctx, bool capturing, cuda
         cudaEventRecord(ctx->ev_fork, s);
         cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
         k_rebuild_plan<<<1, RB_T, 0, ctx->side>>>(P, ctx->D, (cudaGraphConditionalHandle)0, 0);
-        k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
+        k_rebuild_small<<<ctx->small_grid, RBS_T, ctx->small_smem, ctx->side>>>(P, ctx->D);
         launch_nlist_density(ctx, ctx->side, true);
         if (ctx->m2side) {   // (timing nodes on the side stream: the force time is the sum
                              // of both launches' durations)
@@ -1405,7 +1405,7 @@ sph_status sph_profile_substeps(sph_ctx* ctx, int n_substeps, float* ms) {
     for (int it = 0; it < n_substeps; ++it) {
         cudaEventRecord(ev[0], s);
         k_rebuild_plan<<<1, RB_T, 0, s>>>(P, ctx->D, 0, 0);
-        if (ctx->small) k_rebuild_small<<<ctx->small_grid, RB_T, ctx->small_smem, s>>>(P, ctx->D);
+        if (ctx->small) k_rebuild_small<<<ctx->small_grid, RBS_T, ctx->small_smem, s>>>(P, ctx->D);
         else launch_rebin(ctx);
         cudaEventRecord(ev[5], s);
         launch_nlist_density(ctx, s);   // (runs after k_density in the step; same work)

@@ -448,6 +448,7 @@ __global__ void __launch_bounds__(TD) k_density(DevParams P, DevPtrs D, int skip
 //                    eight grid-wide launches.
 // ---------------------------------------------------------------------------------------
 constexpr int RB_T = 1024;
+constexpr int RBS_T = 1024;   // threads of the per-rollout sort CTA (k_rebuild_small; 512: slower)
 
 template <int NT>
 __device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t v, uint32_t* total,
@@ -597,15 +598,15 @@ __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) { nlist_
 // dynamic shared memory: start[ncell + 1] u32 | key[N] u32 | perm[N] u32 | rank[N] u16
 // (host guarantees N < 65536).  Sort only: the lists and the densities of the rebuilt rollouts
 // follow grid-wide in k_nlist_density.
-__global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) {
+__global__ void __launch_bounds__(RBS_T) k_rebuild_small(DevParams P, DevPtrs D) {
     extern __shared__ uint32_t smem[];
-    __shared__ uint32_t wt[RB_T / 32];
+    __shared__ uint32_t wt[RBS_T / 32];
     uint32_t* s_start = smem;
     uint32_t* s_key = s_start + ((P.ncell + 1 + 3) & ~3);   // 16-byte aligned (float2 alias)
     uint32_t* s_perm = s_key + P.N;
     uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_perm + P.N);
     const int count = *D.rcount;
-    const int T = RB_T, tid = threadIdx.x;
+    const int T = RBS_T, tid = threadIdx.x;
     // active CTAs: about one per 3.5 rebuilding rollouts, at least gridDim / 8 -- every resident
     // 1024-thread sort CTA takes half an SM from the concurrent densities / forces, so a few CTAs
     // each sorting several rollouts beat one per rollout (C3 window 97.3 -> 96.6 ms per tick at
@@ -647,7 +648,7 @@ __global__ void __launch_bounds__(RB_T) k_rebuild_small(DevParams P, DevPtrs D) 
             uint32_t s = 0;
             for (int k = 0; k < per; ++k)
                 if (c0 + k <= P.ncell) s += s_start[c0 + k];
-            uint32_t run = block_excl_scan_t<RB_T>(s, nullptr, wt);
+            uint32_t run = block_excl_scan_t<RBS_T>(s, nullptr, wt);
             uint32_t* cs = D.cstart + (size_t)b * (P.ncell + 1);
             for (int k = 0; k < per; ++k) {
                 const int c = c0 + k;
