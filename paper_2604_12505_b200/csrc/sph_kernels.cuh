@@ -532,7 +532,16 @@ __device__ __forceinline__ int build_list_core(const DevParams& P, const DevPtrs
             uint32_t m = 0u;
             for (int k = 0; k < cnt; ++k) {
                 const float2 xj = pos((uint32_t)(base + k));
+#if SPH_F32X2
+                // the canonical predicate on the packed pipe: (x_i - x_j, y_i - y_j) in one FFMA2
+                // (x_j * -1 + x_i: one rounding, = __fsub_rn), squares in one FMUL2, then the
+                // same __fadd_rn -- bit-identical to dist2(__fsub_rn(..), __fsub_rn(..))
+                const float2 dd = rsub2(xi, xj);
+                const float2 sq = __fmul2_rn(dd, dd);
+                const float r2 = __fadd_rn(sq.x, sq.y);
+#else
                 const float r2 = dist2(__fsub_rn(xi.x, xj.x), __fsub_rn(xi.y, xj.y));
+#endif
                 // list radius: 2h + skin, or 2h + hs_i + hs_j (per-particle skins, B6)
                 float RL2 = RL2u;
                 if (PP && P.perpart) {
