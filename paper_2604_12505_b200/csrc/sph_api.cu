@@ -821,7 +821,7 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
     // rebuild path: one CTA per rebuilding rollout when its cell table and sort scratch fit in
     // shared memory (rebuild_path 0 = auto, 1 = force per-rollout CTA, 2 = force multi-kernel)
     {
-        const size_t smem = (size_t)((P.ncell + 1 + 3) & ~3) * 4 + (size_t)P.N * 10 + 16;
+        const size_t smem = (size_t)((P.ncell + 1 + 3) & ~3) * 4 + (size_t)P.N * 14 + 16;
         int dev = 0, nsm = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

@@ -604,7 +604,7 @@ __device__ __forceinline__ void nlist_blk(const DevParams& P, const DevPtrs& D, 
 }
 __global__ void __launch_bounds__(TILE) k_nlist(DevParams P, DevPtrs D) { nlist_blk(P, D, blockIdx.x, blockIdx.y); }
 
-// dynamic shared memory: start[ncell + 1] u32 | key[N] u32 | perm[N] u32 | rank[N] u16
+// dynamic shared memory: start[ncell + 1] u32 | key[N] u32 | perm[N] u32 | id[N] u32 | rank[N] u16
 // (host guarantees N < 65536).  Sort only: the lists and the densities of the rebuilt rollouts
 // follow grid-wide in k_nlist_density.
 __global__ void __launch_bounds__(RBS_T) k_rebuild_small(DevParams P, DevPtrs D) {
@@ -613,7 +613,8 @@ __global__ void __launch_bounds__(RBS_T) k_rebuild_small(DevParams P, DevPtrs D)
     uint32_t* s_start = smem;
     uint32_t* s_key = s_start + ((P.ncell + 1 + 3) & ~3);   // 16-byte aligned (float2 alias)
     uint32_t* s_perm = s_key + P.N;
-    uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_perm + P.N);
+    uint32_t* s_id = s_perm + P.N;   // canonical ids of the unsorted slots (step 4's keys)
+    uint16_t* s_rank = reinterpret_cast<uint16_t*>(s_id + P.N);
     const int count = *D.rcount;
     const int T = RBS_T, tid = threadIdx.x;
     // active CTAs: about one per 3.5 rebuilding rollouts, at least gridDim / 8 -- every resident
@@ -647,6 +648,7 @@ __global__ void __launch_bounds__(RBS_T) k_rebuild_small(DevParams P, DevPtrs D)
             }
             const uint32_t c = (uint32_t)(cy * P.nx + cx);
             s_key[i] = c;
+            s_id[i] = id0[i];
             s_rank[i] = (uint16_t)atomicAdd(s_start + c, 1u);
         }
         __syncthreads();
@@ -677,9 +679,9 @@ __global__ void __launch_bounds__(RBS_T) k_rebuild_small(DevParams P, DevPtrs D)
         for (int c = tid; c < P.ncell; c += T) {
             const int s = (int)s_start[c], e = (int)s_start[c + 1];
             for (int t = s + 1; t < e; ++t) {
-                const uint32_t ss = s_perm[t], ks = id0[ss];
+                const uint32_t ss = s_perm[t], ks = s_id[ss];
                 int u = t - 1;
-                while (u >= s && id0[s_perm[u]] > ks) {
+                while (u >= s && s_id[s_perm[u]] > ks) {
                     s_perm[u + 1] = s_perm[u];
                     --u;
                 }
@@ -692,7 +694,7 @@ __global__ void __launch_bounds__(RBS_T) k_rebuild_small(DevParams P, DevPtrs D)
             const uint32_t src = s_perm[d];
             const float4 v = pv0[src];
             pv1[d] = v;
-            id1[d] = id0[src];
+            id1[d] = s_id[src];
             const uint32_t c = s_key[src];
             D.skey[o + d] = c;
             D.xb[o + d] = make_float2(v.x, v.y);   // positions at this rebuild (Verlet)
