@@ -1058,13 +1058,15 @@ def run_dd(a):
 
 def main():
     a = parse()
+    skin_default = a.skin is None
     if a.skin is None:
-        a.skin = {"P0": 0.5, "C2CL": 0.5, "SETTLE": 0.5}.get(a.workload, 0.15)
-    # Verlet skin policy (B4-B6): C3/C5 per-rollout adaptive skin 0.15h -> 0.7h (B5;
-    # calm start and sloshing steady state of the 110 s train, profiles/horizon*_r02*); C4
-    # per-particle half-skins 0.15h / 0.8h (B6: the bulk keeps short lists, the wall layer wide)
+        a.skin = {"P0": 0.5, "C2CL": 0.5, "SETTLE": 0.5, "C3": 0.10, "C5": 0.10}.get(a.workload, 0.15)
+    # Verlet skin policy (B4-B6): C3/C5 per-rollout adaptive skin 0.10h -> 0.7h (B5;
+    # calm start and sloshing steady state of the 110 s train, profiles/horizon*_r02*, r02.36 /
+    # r02.43); C4 per-particle half-skins 0.15h / 0.8h (B6: the bulk keeps short lists, the wall
+    # layer wide).  An explicit --skin without --skin-max is a fixed skin (B4).
     if a.skin_max is None:
-        a.skin_max = {"C3": 0.7, "C5": 0.7, "C4": 0.8}.get(a.workload, 0.0) if a.skin == 0.15 or a.workload == "C4" else 0.0
+        a.skin_max = {"C3": 0.7, "C5": 0.7, "C4": 0.8}.get(a.workload, 0.0) if skin_default or a.workload == "C4" else 0.0
     if a.skin_mode is None:
         a.skin_mode = 1 if a.workload == "C4" else 0
     if a.settle_seconds is None:
