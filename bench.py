@@ -46,7 +46,7 @@ METRIC = "particle-updates/sec (device-timed) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "particle-updates/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -91,7 +91,7 @@ def parse():
                          "C4: 1,000 damped substeps (SURVEY 8(d)) when no settled snapshot exists")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-substeps", type=int, default=20)
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -1056,8 +1056,9 @@ def run_dd(a):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    a = parse()
+def resolve_defaults(a):
+    """Per-workload defaults of the skin policy and the settle (the measured configuration is
+    entirely in these arguments; tests/test_bench_defaults.py pins the defaults)."""
     skin_default = a.skin is None
     if a.skin is None:
         a.skin = {"P0": 0.5, "C2CL": 0.5, "SETTLE": 0.5, "C3": 0.10, "C5": 0.10}.get(a.workload, 0.15)
@@ -1072,6 +1073,11 @@ def main():
     if a.settle_seconds is None:
         # C4: lattice start + 1,000 untimed damped warm-up substeps; dt = 1 ms / 42
         a.settle_seconds = 1000 * 1e-3 / 42.0 if a.workload == "C4" else 4.0
+    return a
+
+
+def main():
+    a = resolve_defaults(parse())
     if a.workload == "LIN":
         run_linearize(a)
         return
