@@ -211,7 +211,7 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
     {   // CTA sizes of the plain density / force / list kernels.  Small CTAs win (C3 sweeps,
         // DESIGN.md section 7): a CTA's slot frees only when its slowest warp ends, and list
         // lengths / wall work differ from warp to warp.
-        P->td = 128;
+        P->td = N >= 65536 ? 512 : 128;   // large tanks (C4: 10.70 -> 10.83 G/s, r02.46)
         P->tf = 64;
         P->tn = 128;
         // k_force walks the rollouts last to first (L2 reuse after k_density; C3 A/B: force
