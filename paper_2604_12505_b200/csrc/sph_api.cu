@@ -212,7 +212,7 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
         // DESIGN.md section 7): a CTA's slot frees only when its slowest warp ends, and list
         // lengths / wall work differ from warp to warp.
         P->td = N >= 65536 ? 512 : 128;   // large tanks (C4: 10.70 -> 10.83 G/s, r02.46)
-        P->tf = 64;
+        P->tf = N >= 65536 ? 128 : 64;   // large tanks (C4: 10.81 -> 10.95 G/s; 256: 10.89, r02.47)
         P->tn = 128;
         // k_force walks the rollouts last to first (L2 reuse after k_density; C3 A/B: force
         // 327.3 -> 326.5 us live, same bits)
@@ -316,9 +316,18 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
     const DevParams& P = ctx->P;
     const int gy = mode == 2 ? std::min(P.B, 64) : P.B;
     // 64-slot CTAs; the per-particle-skin epilogue (B6) only in its own instance
-    const dim3 g(std::max(1, (P.own_n + 63) / 64), gy);
-    if (P.perpart) launch_k(pdl, k_force<64, true>, g, dim3(64), 0, s, P, ctx->D, damping, mode);
-    else launch_k(pdl, k_force<64, false>, g, dim3(64), 0, s, P, ctx->D, damping, mode);
+#define SPH_FRC(TF)                                                                                \
+    {                                                                                              \
+        const dim3 g(std::max(1, (P.own_n + TF - 1) / TF), gy);                                    \
+        if (P.perpart) launch_k(pdl, k_force<TF, true>, g, dim3(TF), 0, s, P, ctx->D, damping, mode);   \
+        else launch_k(pdl, k_force<TF, false>, g, dim3(TF), 0, s, P, ctx->D, damping, mode);           \
+    }
+    switch (P.tf) {
+        case 256: SPH_FRC(256); break;
+        case 128: SPH_FRC(128); break;
+        default: SPH_FRC(64); break;
+    }
+#undef SPH_FRC
 }
 
 static void launch_body(sph_ctx* ctx, cudaStream_t s, int pin, float ghost_angle0, bool pdl = false) {
