@@ -859,6 +859,13 @@ sph_status sph_init_tank(const sph_fluid_params* fp, const sph_body_params* bp,
             return bail("side stream", e);
         // k_body: enough threads to reduce the per-warp partials of big tanks (N only)
         while (ctx->body_threads < 1024 && ctx->body_threads * 4 < P.npart) ctx->body_threads *= 2;
+        if (P.bsplit > 1) {   // k_body sums bsplit chunk sums: a power of two >= bsplit threads
+            // (every slot holds at most one chunk sum, so the tree -- and the bits -- equal
+            // the 1024-thread block's)
+            int bt = 32;
+            while (bt < P.bsplit && bt < 1024) bt *= 2;
+            ctx->body_threads = bt;
+        }
         {   // cooperative tick for latency-bound small batches (exec_path 2 forces it)
             bool want = tp->exec_path == 2 || (tp->exec_path == 0 && (size_t)P.B * P.N <= 65536 && !ctx->small);
             want = want && ctx->body_threads <= COOP_T && P.bsplit == 1;
