@@ -118,11 +118,12 @@ struct Geom {            // float copy of the body state used by the particle ke
 };
 
 // Per-particle half-skin (B6), set at every rebuild from the particle's speed relative
-// to the body translation: the skin it needs to last ~20 substeps, within [hs_min, hs_max]
-// (HS_TARGET sweep on C4: 10 / 20 / 40 substeps -> 10.0 / 10.45 / 10.3 G/s).  For
+// to the body translation: the skin it needs to last ~28 substeps, within [hs_min, hs_max]
+// (HS_TARGET sweeps on C4: 10 / 20 / 40 substeps -> 10.0 / 10.45 / 10.3 G/s; on the final
+// round-2 build 15 / 20 / 24 / 28 / 34 -> 10.82 / 11.01 / 11.03 / 11.07 / 11.01 G/s).  For
 // a large tank whose wall layer moves 10-50x faster than the bulk (C4), a uniform skin sized for
 // the wall makes every list long; a per-particle one keeps the bulk's lists short.
-constexpr int HS_TARGET = 20;
+constexpr int HS_TARGET = 28;
 // (Measured alternative, not kept: raising the floor per rollout with the B5 rule pushes every
 // particle's skin up to outlast the few that trip early -- C4 8.5 vs 9.6 G/s.)
 __device__ __forceinline__ float half_skin(const DevParams& P, float4 x, const Geom& gm) {
