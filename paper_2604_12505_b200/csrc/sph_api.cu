@@ -212,7 +212,9 @@ static bool make_params(const sph_fluid_params* fp, const sph_body_params* bp,
         // DESIGN.md section 7): a CTA's slot frees only when its slowest warp ends, and list
         // lengths / wall work differ from warp to warp.
         P->td = N >= 65536 ? 512 : 128;   // large tanks (C4: 10.70 -> 10.83 G/s, r02.46)
-        P->tf = N >= 65536 ? 128 : 64;   // large tanks (C4: 10.81 -> 10.95 G/s; 256: 10.89, r02.47)
+        // 128-slot force CTAs (r02.47 / r02.52: C4 10.81 -> 10.95 G/s, C3 94.97 -> 93.39 ms per
+        // tick on the round-2 graph; 64 won on the round-1 graph, 256 loses on both)
+        P->tf = 128;
         P->tn = 128;
         // k_force walks the rollouts last to first (L2 reuse after k_density; C3 A/B: force
         // 327.3 -> 326.5 us live, same bits)
@@ -315,7 +317,7 @@ static void launch_force(sph_ctx* ctx, cudaStream_t s, float damping, int mode =
     pdl = pdl && ctx->pdl;
     const DevParams& P = ctx->P;
     const int gy = mode == 2 ? std::min(P.B, 64) : P.B;
-    // 64-slot CTAs; the per-particle-skin epilogue (B6) only in its own instance
+    // P.tf-slot CTAs (128, DESIGN.md r02.52); the per-particle-skin epilogue (B6) only in its own instance
 #define SPH_FRC(TF)                                                                                \
     {                                                                                              \
         const dim3 g(std::max(1, (P.own_n + TF - 1) / TF), gy);                                    \
